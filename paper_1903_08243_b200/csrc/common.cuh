@@ -1,0 +1,73 @@
+// Shared device helpers for the FE operator kernels (sm_100a, FP64).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/fe_b200.h"
+
+#define FE_DEVICE __device__ __forceinline__
+
+namespace fe {
+
+constexpr int form_vs(int form, int dim) {
+  return (form == FE_FORM_LAPLACIAN || form == FE_FORM_ELASTICITY ||
+          form == FE_FORM_ELASTICITY_LAME || form == FE_FORM_NEOHOOKEAN) ? dim : 1;
+}
+constexpr bool form_needs_values(int form) {
+  return form == FE_FORM_MASS || form == FE_FORM_HELMHOLTZ;
+}
+constexpr bool form_needs_grads(int form) { return form != FE_FORM_MASS; }
+
+// Device-side view of a bound mesh, in the plan's internal layout.
+struct MeshView {
+  const int32_t* map;      // SoA [ndof][nc_stride] (dof ids; vertex ids in the first nv rows)
+  const int32_t* vmap;     // SoA [nvert][nc_stride] when map0[:, :nv] is not the vertex map, else == map
+  const double* coords;    // padded: [nverts][CSTRIDE] (CSTRIDE = 2 for 2D, 4 for 3D)
+  int64_t nc_stride;
+};
+
+template <int DIM> struct CStride { static constexpr int value = DIM == 2 ? 2 : 4; };
+
+template <int DIM>
+FE_DEVICE void load_vertex(const double* __restrict__ coords, int v, double* x) {
+  if constexpr (DIM == 2) {
+    double2 c = __ldg(reinterpret_cast<const double2*>(coords) + v);
+    x[0] = c.x; x[1] = c.y;
+  } else {
+    const double2* p = reinterpret_cast<const double2*>(coords) + 2 * (int64_t)v;
+    double2 a = __ldg(p), b = __ldg(p + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = b.x;
+  }
+}
+
+// determinant and inverse of a DIM x DIM matrix stored row-major J[a][b]
+template <int DIM>
+FE_DEVICE double det_inv(const double (&J)[DIM][DIM], double (&Ji)[DIM][DIM]) {
+  if constexpr (DIM == 2) {
+    double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    double r = 1.0 / det;
+    Ji[0][0] = J[1][1] * r;  Ji[0][1] = -J[0][1] * r;
+    Ji[1][0] = -J[1][0] * r; Ji[1][1] = J[0][0] * r;
+    return det;
+  } else {
+    double a00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    double a01 = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    double a02 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    double a10 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    double a11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    double a12 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    double a20 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
+    double r = 1.0 / det;
+    Ji[0][0] = a00 * r; Ji[0][1] = a01 * r; Ji[0][2] = a02 * r;
+    Ji[1][0] = a10 * r; Ji[1][1] = a11 * r; Ji[1][2] = a12 * r;
+    Ji[2][0] = a20 * r; Ji[2][1] = a21 * r; Ji[2][2] = a22 * r;
+    return det;
+  }
+}
+
+// y[idx] += v.  The global scatter P_e^T: FP64 RED at L2 (REDG.E.ADD.F64).
+FE_DEVICE void scatter_add(double* y, int64_t idx, double v) { atomicAdd(y + idx, v); }
+
+}  // namespace fe

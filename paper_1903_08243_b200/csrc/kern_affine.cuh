@@ -1,0 +1,103 @@
+// Element-tensor kernels for affine simplices (C1 mass P2 triangles, C2
+// Helmholtz P1..P3 tetrahedra).
+//
+// On an affine cell every term of mass/helmholtz/laplacian is a constant
+// geometric coefficient times a reference matrix:
+//   y_e = |det J| Mhat u_e + sum_{a<=b} K_ab (S_ab + S_ba [a!=b]) u_e,
+//   K = |det J| J^-1 J^-T,  S_ab[i][j] = int dphi_i/dxi_a dphi_j/dxi_b,
+// the "element-tensor" algorithm of SURVEY.md Appendix B (14 nd^2 + 13 nd +
+// 80 flops on tets).  It is mathematically the reference's quadrature loop
+// (kernels.py:136-252) with the quadrature sums hoisted out of the cell
+// loop; results agree to round-off.
+//
+// One thread per cell, NM reference matrices passed BY VALUE in the kernel
+// parameter block (constant bank 0): every DFMA of the unrolled S_m u_e
+// products reads its matrix entry as a uniform constant operand, so the
+// inner loop issues no shared-memory loads at all.
+#pragma once
+#include "common.cuh"
+
+namespace fe {
+
+template <int FORM, int DIM>
+constexpr int et_nmats() {
+  return (FORM == FE_FORM_MASS ? 1 : 0) + (FORM != FE_FORM_MASS ? DIM * (DIM + 1) / 2 : 0);
+}
+
+template <int NM, int ND>
+struct ETParams {
+  MeshView mesh;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  int32_t start, end;
+  double S[NM][ND][ND];  // [mass?] then S_00, S_11, (S_22), S_01+S_10, ...
+};
+
+// Geometric coefficients of the NM matrices for one cell.
+template <int FORM, int DIM, int NM>
+FE_DEVICE void et_coeffs(const double (&X)[DIM + 1][DIM], double (&cm)[NM]) {
+  double J[DIM][DIM], Ji[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+  double ad = fabs(det_inv<DIM>(J, Ji));
+  int m = 0;
+  if constexpr (FORM == FE_FORM_MASS || FORM == FE_FORM_HELMHOLTZ) cm[m++] = ad;
+  if constexpr (FORM != FE_FORM_MASS) {
+    double K[DIM][DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = a; b < DIM; ++b) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) s += Ji[a][c] * Ji[b][c];
+        K[a][b] = ad * s;
+      }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) cm[m++] = K[a][a];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = a + 1; b < DIM; ++b) cm[m++] = K[a][b];
+  }
+}
+
+template <int FORM, int DIM, int ND>
+__global__ void __launch_bounds__(128)
+affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  constexpr int NV = DIM + 1;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  int dof[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+  }
+  double w[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) w[i] = __ldg(p.u + dof[i]);
+  double cm[NM];
+  et_coeffs<FORM, DIM, NM>(X, cm);
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    double yi = 0.0;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], w[j], t);
+      yi = fma(cm[m], t, yi);
+    }
+    scatter_add(p.y, dof[i], yi);
+  }
+}
+
+}  // namespace fe

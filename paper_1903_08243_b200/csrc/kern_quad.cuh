@@ -1,0 +1,232 @@
+// Generic thread-per-cell quadrature kernel: the reference algorithm
+// (kernels.py:67-269 local kernel inlined into the transforms.py:112-266
+// gather/compute/scatter cell loop) with one GPU thread per cell -- the GPU
+// analogue of the paper's cross-element SIMD lanes (one lane per cell,
+// transforms.py:409-491).  Tables (kernels.py:97-108) are staged in shared
+// memory; every thread of a warp reads the same table entry (broadcast).
+//
+// Used for every (form, cell, degree) whose local vectors fit in registers;
+// it is the production kernel for the neo-Hookean residual (C5) and the
+// coverage kernel for the others.
+#pragma once
+#include "common.cuh"
+
+namespace fe {
+
+struct QuadParams {
+  MeshView mesh;
+  int32_t start, end;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  const double* __restrict__ mu;   // vertex fields (elasticity_lame)
+  const double* __restrict__ lam;
+  const double* __restrict__ tables;  // qw | phi | dphi | gphi | gdphi
+  double p0, p1;                      // neohookean mu, lambda
+};
+
+template <int NQ, int ND, int NV, int DIM>
+struct QuadTables {
+  static constexpr int qw = 0;
+  static constexpr int phi = qw + NQ;
+  static constexpr int dphi = phi + NQ * ND;
+  static constexpr int gphi = dphi + NQ * ND * DIM;
+  static constexpr int gdphi = gphi + NQ * NV;
+  static constexpr int size = gdphi + NQ * NV * DIM;
+};
+
+// Pointwise flux at one quadrature point.  Inputs: inverse Jacobian Ji
+// (Ji[b][a] = dxi_b/dx_a), weight tw = w_q |det J|, values uq[c] and
+// reference gradients g[c][b] of u.  Outputs: cv[c] multiplies phi_j and
+// cg[c][b] multiplies dphi_j/dxi_b in the accumulation A[j][c] += ...
+// (kernels.py:202-252 for the reference forms).
+template <int FORM, int DIM, int VS>
+FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (&uq)[VS],
+                         const double (&g)[VS][DIM], double mu, double lam,
+                         double (&cv)[VS], double (&cg)[VS][DIM]) {
+  if constexpr (form_needs_values(FORM)) {
+#pragma unroll
+    for (int c = 0; c < VS; ++c) cv[c] = tw * uq[c];
+  }
+  if constexpr (form_needs_grads(FORM)) {
+    double G[VS][DIM];  // physical gradient du_c/dx_a
+#pragma unroll
+    for (int c = 0; c < VS; ++c)
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) s += Ji[b][a] * g[c][b];
+        G[c][a] = s;
+      }
+    double T[VS][DIM];  // physical flux paired with dv_c/dx_a
+    if constexpr (FORM == FE_FORM_HELMHOLTZ || FORM == FE_FORM_LAPLACIAN_SCALAR ||
+                  FORM == FE_FORM_LAPLACIAN) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) T[c][a] = G[c][a];
+    } else if constexpr (FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_ELASTICITY_LAME) {
+      static_assert(VS == DIM, "vector form");
+      double tr = 0.0;
+#pragma unroll
+      for (int c = 0; c < VS; ++c) tr += G[c][c];
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double e = 0.5 * (G[c][a] + G[a][c]);
+          if constexpr (FORM == FE_FORM_ELASTICITY) T[c][a] = e;
+          else T[c][a] = 2.0 * mu * e + (c == a ? lam * tr : 0.0);
+        }
+    } else if constexpr (FORM == FE_FORM_NEOHOOKEAN) {
+      static_assert(VS == DIM, "vector form");
+      double F[DIM][DIM], Fi[DIM][DIM];
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) F[c][a] = G[c][a] + (c == a ? 1.0 : 0.0);
+      double Jf = det_inv<DIM>(F, Fi);
+      double ll = lam * log(Jf);
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double fit = Fi[a][c];  // F^{-T}[c][a]
+          T[c][a] = mu * (F[c][a] - fit) + ll * fit;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < VS; ++c)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) s += Ji[b][a] * T[c][a];
+        cg[c][b] = tw * s;
+      }
+  }
+}
+
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
+__global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
+  constexpr int VS = form_vs(FORM, DIM);
+  using TB = QuadTables<NQ, ND, NV, DIM>;
+  extern __shared__ double smem[];
+  for (int i = threadIdx.x; i < TB::size; i += blockDim.x) smem[i] = p.tables[i];
+  __syncthreads();
+  const double* s_qw = smem + TB::qw;
+  const double* s_phi = smem + TB::phi;
+  const double* s_dphi = smem + TB::dphi;
+  const double* s_gphi = smem + TB::gphi;
+  const double* s_gdphi = smem + TB::gdphi;
+
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+
+  int dof[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+  }
+  double w[ND][VS];
+#pragma unroll
+  for (int i = 0; i < ND; ++i)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) w[i][c] = __ldg(p.u + (int64_t)VS * dof[i] + c);
+  double muv[NV], lamv[NV];
+  if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+      muv[v] = __ldg(p.mu + vid);
+      lamv[v] = __ldg(p.lam + vid);
+    }
+  }
+  double A[ND][VS];
+#pragma unroll
+  for (int i = 0; i < ND; ++i)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) A[i][c] = 0.0;
+
+  double J[DIM][DIM], Ji[DIM][DIM], absdet = 0.0;
+  auto jacobian = [&](int q) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s += X[v][a] * s_gdphi[(q * NV + v) * DIM + b];
+        J[a][b] = s;
+      }
+    absdet = fabs(det_inv<DIM>(J, Ji));
+  };
+  if constexpr (AFFINE) jacobian(0);
+
+#pragma unroll 1
+  for (int q = 0; q < NQ; ++q) {
+    if constexpr (!AFFINE) jacobian(q);
+    const double tw = s_qw[q] * absdet;
+    double uq[VS], g[VS][DIM];
+    if constexpr (form_needs_values(FORM)) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c) uq[c] = 0.0;
+#pragma unroll
+      for (int i = 0; i < ND; ++i) {
+        double ph = s_phi[q * ND + i];
+#pragma unroll
+        for (int c = 0; c < VS; ++c) uq[c] += ph * w[i][c];
+      }
+    }
+    if constexpr (form_needs_grads(FORM)) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) g[c][b] = 0.0;
+#pragma unroll
+      for (int i = 0; i < ND; ++i)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+          double d = s_dphi[(q * ND + i) * DIM + b];
+#pragma unroll
+          for (int c = 0; c < VS; ++c) g[c][b] += d * w[i][c];
+        }
+    }
+    double mu = p.p0, lam = p.p1;
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+      mu = 0.0; lam = 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double gv = s_gphi[q * NV + v];
+        mu += gv * muv[v];
+        lam += gv * lamv[v];
+      }
+    }
+    double cv[VS], cg[VS][DIM];
+    pointwise<FORM, DIM, VS>(Ji, tw, uq, g, mu, lam, cv, cg);
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c) {
+        double acc = A[j][c];
+        if constexpr (form_needs_values(FORM)) acc += s_phi[q * ND + j] * cv[c];
+        if constexpr (form_needs_grads(FORM)) {
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) acc += s_dphi[(q * ND + j) * DIM + b] * cg[c][b];
+        }
+        A[j][c] = acc;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < ND; ++j)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) scatter_add(p.y, (int64_t)VS * dof[j] + c, A[j][c]);
+}
+
+}  // namespace fe

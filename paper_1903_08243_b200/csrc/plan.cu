@@ -1,0 +1,580 @@
+// C ABI (include/fe_b200.h): plans, mesh binding and kernel dispatch.
+//
+// Plan = everything the reference bakes into one emitted wrap_<form>
+// (codegen.py:345-447): the tables, the kernel specialisation for
+// (form, cell, degree, rule) -- here chosen from a registry of sm_100a
+// template instantiations instead of generated C -- plus the bound mesh in
+// the GPU layout (element-batched SoA maps, padded coordinates).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kern_affine.cuh"
+#include "kern_quad.cuh"
+#include "kern_tensor.cuh"
+#include "kern_dmma.cuh"
+
+using namespace fe;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(FE_ECUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_),     \
+                  __FILE__, __LINE__);                                                \
+  } while (0)
+
+int cell_dim(int cell) { return (cell == FE_CELL_TRIANGLE || cell == FE_CELL_QUADRILATERAL) ? 2 : 3; }
+int cell_nv(int cell) {
+  switch (cell) {
+    case FE_CELL_TRIANGLE: return 3;
+    case FE_CELL_QUADRILATERAL: return 4;
+    case FE_CELL_TETRAHEDRON: return 4;
+    default: return 8;
+  }
+}
+}  // namespace
+
+struct Variant;
+
+struct fe_plan {
+  // element description (scalars copied; tables copied into vectors)
+  int form, cell, degree, vs, dim, nv, nd, nq, q1d;
+  double params[4];
+  std::vector<double> qw, phi, dphi, gphi, gdphi, B1d, D1d, w1d;
+  std::vector<int32_t> lex;
+  const Variant* var = nullptr;
+  uint32_t flags = 0;
+  // device tables (kernel-family specific layout)
+  double* d_tables = nullptr;
+  size_t tables_bytes = 0;
+  void* host_params = nullptr;  // by-value kernel parameter block (element-tensor kernels)
+  size_t host_params_bytes = 0;
+  // bound mesh
+  int32_t ncells = 0, nverts = 0;
+  int64_t nglobal = 0;
+  int64_t stride = 0;
+  int32_t* d_map = nullptr;     // SoA [nd][stride]
+  int32_t* d_vmap = nullptr;    // SoA [nv][stride] or == d_map
+  int32_t* d_map_rm = nullptr;  // row-major [ncells][nd] copy for CTA-per-cell kernels
+  double* d_coords = nullptr;   // padded [nverts][cstride]
+  const void* b_coords = nullptr;
+  const void* b_map0 = nullptr;
+  const void* b_map1 = nullptr;
+  uint32_t b_flags = 0;
+  // host-entry staging
+  cudaStream_t hstream = nullptr;
+  double* d_u = nullptr;
+  double* d_y = nullptr;
+  double* d_c0 = nullptr;
+  double* d_c1 = nullptr;
+  size_t cap_u = 0, cap_c = 0;
+};
+
+typedef int (*PrepareFn)(fe_plan*);
+typedef int (*LaunchFn)(const fe_plan*, int32_t, int32_t, double*, const double*, const double*,
+                        const double*, cudaStream_t);
+
+struct Variant {
+  int form, cell, degree, nq;  // nq = -1: any rule accepted by the prepare step
+  int priority;                // higher wins
+  const char* name;
+  int block;
+  PrepareFn prepare;
+  LaunchFn launch;
+};
+
+// ---------------------------------------------------------------------------
+// generic quadrature kernel
+// ---------------------------------------------------------------------------
+
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
+int quad_prepare(fe_plan* p) {
+  using TB = QuadTables<NQ, ND, NV, DIM>;
+  std::vector<double> t(TB::size);
+  std::copy(p->qw.begin(), p->qw.end(), t.begin() + TB::qw);
+  std::copy(p->phi.begin(), p->phi.end(), t.begin() + TB::phi);
+  std::copy(p->dphi.begin(), p->dphi.end(), t.begin() + TB::dphi);
+  std::copy(p->gphi.begin(), p->gphi.end(), t.begin() + TB::gphi);
+  std::copy(p->gdphi.begin(), p->gdphi.end(), t.begin() + TB::gdphi);
+  p->tables_bytes = t.size() * sizeof(double);
+  CUDA_TRY(cudaMalloc(&p->d_tables, p->tables_bytes));
+  CUDA_TRY(cudaMemcpy(p->d_tables, t.data(), p->tables_bytes, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaFuncSetAttribute(quad_kernel<FORM, DIM, NV, ND, NQ, AFFINE>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->tables_bytes));
+  return FE_OK;
+}
+
+MeshView mesh_view(const fe_plan* p) {
+  MeshView m;
+  m.map = p->d_map;
+  m.vmap = p->d_vmap;
+  m.coords = p->d_coords;
+  m.nc_stride = p->stride;
+  return m;
+}
+
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
+int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                const double* c0, const double* c1, cudaStream_t s) {
+  QuadParams k;
+  k.mesh = mesh_view(p);
+  k.start = start;
+  k.end = end;
+  k.u = u;
+  k.y = y;
+  k.mu = c0;
+  k.lam = c1;
+  k.tables = p->d_tables;
+  k.p0 = p->params[0];
+  k.p1 = p->params[1];
+  int n = end - start;
+  quad_kernel<FORM, DIM, NV, ND, NQ, AFFINE>
+      <<<(n + 127) / 128, 128, p->tables_bytes, s>>>(k);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// element-tensor kernel (affine simplices)
+// ---------------------------------------------------------------------------
+
+// Reference matrices from the plan's quadrature tables (exact for the
+// polynomial integrands of affine cells).
+static void element_matrices(const fe_plan* p, bool mass, bool grads, std::vector<double>& S) {
+  const int nd = p->nd, nq = p->nq, d = p->dim;
+  S.clear();
+  auto push = [&](auto f) {
+    for (int i = 0; i < nd; ++i)
+      for (int j = 0; j < nd; ++j) {
+        double s = 0.0;
+        for (int q = 0; q < nq; ++q) s += p->qw[q] * f(q, i, j);
+        S.push_back(s);
+      }
+  };
+  auto dp = [&](int q, int i, int a) { return p->dphi[((size_t)q * nd + i) * d + a]; };
+  if (mass) push([&](int q, int i, int j) { return p->phi[q * nd + i] * p->phi[q * nd + j]; });
+  if (grads) {
+    for (int a = 0; a < d; ++a) push([&](int q, int i, int j) { return dp(q, i, a) * dp(q, j, a); });
+    for (int a = 0; a < d; ++a)
+      for (int b = a + 1; b < d; ++b)
+        push([&](int q, int i, int j) { return dp(q, i, a) * dp(q, j, b) + dp(q, i, b) * dp(q, j, a); });
+  }
+}
+
+template <int FORM, int DIM, int ND>
+int et_prepare(fe_plan* p) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  using P = ETParams<NM, ND>;
+  static_assert(sizeof(P) <= 32000, "parameter block too large");
+  std::vector<double> S;
+  element_matrices(p, FORM != FE_FORM_LAPLACIAN_SCALAR, FORM != FE_FORM_MASS, S);
+  if ((int)S.size() != NM * ND * ND) return fail(FE_EINVAL, "element-tensor table size mismatch");
+  P* hp = new P();
+  std::memcpy(hp->S, S.data(), S.size() * sizeof(double));
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(P);
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND>
+int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+              const double*, const double*, cudaStream_t s) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  using P = ETParams<NM, ND>;
+  P* hp = static_cast<P*>(p->host_params);
+  hp->mesh = mesh_view(p);
+  hp->u = u;
+  hp->y = y;
+  hp->start = start;
+  hp->end = end;
+  int n = end - start;
+  affine_et_kernel<FORM, DIM, ND><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// registry
+// ---------------------------------------------------------------------------
+
+#define QV(FORM, CELL, DIM, NV, K, ND, NQ, AFF)                                              \
+  {FORM, CELL, K, NQ, 0, "quad", 128, quad_prepare<FORM, DIM, NV, ND, NQ, AFF>,           \
+   quad_launch<FORM, DIM, NV, ND, NQ, AFF>}
+#define ETV(FORM, CELL, DIM, K, ND)                                                          \
+  {FORM, CELL, K, -1, 10, "element_tensor", 128, et_prepare<FORM, DIM, ND>,                  \
+   et_launch<FORM, DIM, ND>}
+
+// 2D reference forms on triangles (nq = (k+1)^2) and quadrilaterals (nq = (k+2)^2)
+#define TRI_FORM(F)                                                                           \
+  QV(F, FE_CELL_TRIANGLE, 2, 3, 1, 3, 4, true), QV(F, FE_CELL_TRIANGLE, 2, 3, 2, 6, 9, true), \
+  QV(F, FE_CELL_TRIANGLE, 2, 3, 3, 10, 16, true), QV(F, FE_CELL_TRIANGLE, 2, 3, 4, 15, 25, true)
+#define QUAD_FORM(F)                                                                          \
+  QV(F, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, false),                                         \
+  QV(F, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16, false),                                        \
+  QV(F, FE_CELL_QUADRILATERAL, 2, 4, 3, 16, 25, false),                                       \
+  QV(F, FE_CELL_QUADRILATERAL, 2, 4, 4, 25, 36, false)
+
+static const Variant kVariants[] = {
+    TRI_FORM(FE_FORM_MASS), TRI_FORM(FE_FORM_HELMHOLTZ), TRI_FORM(FE_FORM_LAPLACIAN),
+    TRI_FORM(FE_FORM_ELASTICITY), TRI_FORM(FE_FORM_LAPLACIAN_SCALAR),
+    TRI_FORM(FE_FORM_ELASTICITY_LAME), TRI_FORM(FE_FORM_NEOHOOKEAN),
+    QUAD_FORM(FE_FORM_MASS), QUAD_FORM(FE_FORM_HELMHOLTZ), QUAD_FORM(FE_FORM_LAPLACIAN),
+    QUAD_FORM(FE_FORM_ELASTICITY), QUAD_FORM(FE_FORM_LAPLACIAN_SCALAR),
+    QUAD_FORM(FE_FORM_ELASTICITY_LAME),
+    // tetrahedra: nq = (k+1)^3
+    QV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
+    QV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
+    QV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
+    QV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
+    QV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 4, 3, 20, 64, true),
+    QV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 4, 4, 35, 125, true),
+    QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
+    QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
+    QV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
+    QV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
+    QV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
+    QV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
+    // hexahedra: default rule nq = (k+2)^3, BASELINE C3 rule nq = (k+1)^3
+    QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, false),
+    QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 2, 27, 27, false),
+    QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 2, 27, 64, false),
+    QV(FE_FORM_HELMHOLTZ, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    QV(FE_FORM_MASS, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    QV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    QV(FE_FORM_ELASTICITY, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    QV(FE_FORM_LAPLACIAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    QV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
+    // element-tensor kernels (affine simplices)
+    ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 1, 3), ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 2, 6),
+    ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 3, 10), ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 4, 15),
+    ETV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 1, 3), ETV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 2, 6),
+    ETV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 3, 10), ETV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 4, 15),
+    ETV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 1, 4), ETV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 2, 10),
+    ETV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 3, 20),
+    ETV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 1, 4),
+    ETV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10),
+    ETV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 3, 20),
+    ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4),
+    ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10),
+    ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 3, 20),
+    FE_TENSOR_VARIANTS
+    FE_DMMA_VARIANTS
+};
+
+// ---------------------------------------------------------------------------
+// mesh binding kernels
+// ---------------------------------------------------------------------------
+
+__global__ void k_transpose_map(const int32_t* __restrict__ rm, int32_t* __restrict__ soa, int nc,
+                                int nd, int64_t stride) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * nd) return;
+  int c = (int)(t / nd), i = (int)(t % nd);
+  soa[i * stride + c] = rm[t];
+}
+
+__global__ void k_pad_coords(const double* __restrict__ x, double* __restrict__ out, int nv, int dim,
+                             int cstride) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  for (int a = 0; a < cstride; ++a) out[(int64_t)v * cstride + a] = a < dim ? x[(int64_t)v * dim + a] : 0.0;
+}
+
+__global__ void k_check_vmap(const int32_t* __restrict__ map0, const int32_t* __restrict__ map1, int nc,
+                             int nd, int nv, int* flag) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * nv) return;
+  int c = (int)(t / nv), v = (int)(t % nv);
+  if (map0[(int64_t)c * nd + v] != map1[t]) *flag = 1;
+}
+
+__global__ void k_check_range(const int32_t* __restrict__ m, int64_t n, int64_t hi, int* flag) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n && (m[t] < 0 || m[t] >= hi)) *flag = 1;
+}
+
+namespace {
+
+void free_mesh(fe_plan* p) {
+  if (p->d_vmap && p->d_vmap != p->d_map) cudaFree(p->d_vmap);
+  cudaFree(p->d_map);
+  cudaFree(p->d_map_rm);
+  cudaFree(p->d_coords);
+  p->d_map = p->d_vmap = p->d_map_rm = nullptr;
+  p->d_coords = nullptr;
+  p->b_coords = p->b_map0 = p->b_map1 = nullptr;
+}
+
+const Variant* select_variant(const fe_plan* p, uint32_t flags) {
+  const Variant* best = nullptr;
+  for (const Variant& v : kVariants) {
+    if (v.form != p->form || v.cell != p->cell || v.degree != p->degree) continue;
+    if (v.nq >= 0 && v.nq != p->nq) continue;
+    if (v.nq < 0 && p->q1d == 0 && v.priority >= 20) continue;  // tensor kernels need 1D factors
+    if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
+    if (!best || v.priority > best->priority) best = &v;
+  }
+  return best;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int fe_abi_version(void) { return FE_ABI_VERSION; }
+
+const char* fe_last_error(void) { return g_err.c_str(); }
+
+int fe_plan_create(fe_plan** out, const fe_element_desc* d, uint32_t flags) {
+  if (!out || !d) return fail(FE_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->cell < 0 || d->cell > 3) return fail(FE_EINVAL, "bad cell %d", d->cell);
+  if (d->form < 0 || d->form > 6) return fail(FE_EINVAL, "bad form %d", d->form);
+  fe_plan* p = new fe_plan();
+  p->form = d->form;
+  p->cell = d->cell;
+  p->degree = d->degree;
+  p->dim = cell_dim(d->cell);
+  p->nv = cell_nv(d->cell);
+  p->vs = form_vs(d->form, p->dim);
+  p->nd = d->ndof;
+  p->nq = d->nq;
+  p->q1d = d->q1d;
+  p->flags = flags;
+  std::memcpy(p->params, d->params, sizeof p->params);
+  if (d->value_size != p->vs || d->nvert != p->nv) {
+    delete p;
+    return fail(FE_EINVAL, "value_size/nvert inconsistent with form/cell");
+  }
+  if (!d->qweights || !d->phi || !d->dphi || !d->gphi || !d->gdphi) {
+    delete p;
+    return fail(FE_EINVAL, "missing tables");
+  }
+  const int nq = p->nq, nd = p->nd, nv = p->nv, dim = p->dim;
+  p->qw.assign(d->qweights, d->qweights + nq);
+  p->phi.assign(d->phi, d->phi + (size_t)nq * nd);
+  p->dphi.assign(d->dphi, d->dphi + (size_t)nq * nd * dim);
+  p->gphi.assign(d->gphi, d->gphi + (size_t)nq * nv);
+  p->gdphi.assign(d->gdphi, d->gdphi + (size_t)nq * nv * dim);
+  if (p->q1d > 0) {
+    const int pp = p->degree + 1;
+    if (!d->B1d || !d->D1d || !d->w1d || !d->lex) {
+      delete p;
+      return fail(FE_EINVAL, "missing tensor factors");
+    }
+    p->B1d.assign(d->B1d, d->B1d + (size_t)p->q1d * pp);
+    p->D1d.assign(d->D1d, d->D1d + (size_t)p->q1d * pp);
+    p->w1d.assign(d->w1d, d->w1d + p->q1d);
+    int n = 1;
+    for (int a = 0; a < dim; ++a) n *= pp;
+    p->lex.assign(d->lex, d->lex + n);
+  }
+  p->var = select_variant(p, flags);
+  if (!p->var) {
+    int form = p->form, cell = p->cell, deg = p->degree;
+    delete p;
+    return fail(FE_EUNSUPPORTED, "no sm_100a kernel for form %d cell %d degree %d nq %d", form,
+                cell, deg, nq);
+  }
+  int rc = p->var->prepare(p);
+  if (rc) {
+    std::string msg = g_err;
+    fe_plan_destroy(p);
+    g_err = msg;
+    return rc;
+  }
+  *out = p;
+  return FE_OK;
+}
+
+int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t nglobal,
+                      const double* coords, const int32_t* map0, const int32_t* map1,
+                      uint32_t ptr_flags, void* stream) {
+  if (!p || !coords || !map0) return fail(FE_EINVAL, "null argument");
+  if (ncells < 0 || nverts <= 0 || nglobal <= 0) return fail(FE_EINVAL, "bad sizes");
+  cudaStream_t s = (cudaStream_t)stream;
+  free_mesh(p);
+  const int nd = p->nd, nv = p->nv, dim = p->dim, cst = dim == 2 ? 2 : 4;
+  p->ncells = ncells;
+  p->nverts = nverts;
+  p->nglobal = nglobal;
+  p->stride = ((int64_t)ncells + 31) / 32 * 32;
+  const bool dev = ptr_flags & FE_PTR_DEVICE;
+  const size_t mbytes = (size_t)ncells * nd * sizeof(int32_t);
+  // raw (row-major) map0 on the device
+  CUDA_TRY(cudaMalloc(&p->d_map_rm, mbytes > 0 ? mbytes : 4));
+  if (mbytes) CUDA_TRY(cudaMemcpyAsync(p->d_map_rm, map0, mbytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMalloc(&p->d_map, (size_t)nd * p->stride * sizeof(int32_t) + 4));
+  int* d_flag = nullptr;
+  CUDA_TRY(cudaMalloc(&d_flag, 2 * sizeof(int)));
+  CUDA_TRY(cudaMemsetAsync(d_flag, 0, 2 * sizeof(int), s));
+  const int T = 256;
+  if (ncells > 0) {
+    int64_t n = (int64_t)ncells * nd;
+    k_transpose_map<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, p->d_map, ncells, nd, p->stride);
+    k_check_range<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, n, nglobal, d_flag);
+  }
+  p->d_vmap = p->d_map;
+  int32_t* d_m1 = nullptr;
+  if (map1 && ncells > 0) {
+    size_t b1 = (size_t)ncells * nv * sizeof(int32_t);
+    CUDA_TRY(cudaMalloc(&d_m1, b1));
+    CUDA_TRY(cudaMemcpyAsync(d_m1, map1, b1, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    int64_t n = (int64_t)ncells * nv;
+    k_check_vmap<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, d_m1, ncells, nd, nv, d_flag + 1);
+    k_check_range<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(d_m1, n, nverts, d_flag);
+  }
+  // coordinates, padded to 16/32 bytes per vertex
+  double* d_x = nullptr;
+  CUDA_TRY(cudaMalloc(&d_x, (size_t)nverts * dim * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(d_x, coords, (size_t)nverts * dim * sizeof(double),
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMalloc(&p->d_coords, (size_t)nverts * cst * sizeof(double)));
+  k_pad_coords<<<(nverts + T - 1) / T, T, 0, s>>>(d_x, p->d_coords, nverts, dim, cst);
+  int h_flag[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(h_flag, d_flag, sizeof h_flag, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(d_flag);
+  cudaFree(d_x);
+  if (h_flag[0]) {
+    cudaFree(d_m1);
+    free_mesh(p);
+    return fail(FE_EINVAL, "map entry out of range");
+  }
+  if (h_flag[1]) {
+    // map0[:, :nv] is not the vertex map: keep a separate SoA vertex map
+    CUDA_TRY(cudaMalloc(&p->d_vmap, (size_t)nv * p->stride * sizeof(int32_t) + 4));
+    int64_t n = (int64_t)ncells * nv;
+    k_transpose_map<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(d_m1, p->d_vmap, ncells, nv, p->stride);
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  cudaFree(d_m1);
+  p->b_coords = coords;
+  p->b_map0 = map0;
+  p->b_map1 = map1;
+  p->b_flags = ptr_flags;
+  return FE_OK;
+}
+
+int fe_apply(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+             const double* c0, const double* c1, uint32_t apply_flags, void* stream) {
+  if (!p) return fail(FE_EINVAL, "null plan");
+  if (!p->d_map) return fail(FE_ENOMESH, "no mesh bound to the plan");
+  if (start < 0 || end > p->ncells || start > end)
+    return fail(FE_EINVAL, "cell range [%d, %d) outside [0, %d)", start, end, p->ncells);
+  if (!y || !u) return fail(FE_EINVAL, "null dat0/dat2");
+  if (p->form == FE_FORM_ELASTICITY_LAME && (!c0 || !c1))
+    return fail(FE_EINVAL, "elasticity_lame needs the mu and lambda vertex fields");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (apply_flags & FE_APPLY_OVERWRITE)
+    CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)p->vs * p->nglobal * sizeof(double), s));
+  if (end == start) return FE_OK;
+  return p->var->launch(p, start, end, y, u, c0, c1, s);
+}
+
+int fe_wrap(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat1,
+            const double* dat2, const double* dat3, const double* dat4, const int32_t* map0,
+            const int32_t* map1, void* stream) {
+  if (!p) return fail(FE_EINVAL, "null plan");
+  if (!p->d_map || p->b_coords != dat1 || p->b_map0 != map0 || p->b_map1 != map1 ||
+      !(p->b_flags & FE_PTR_DEVICE))
+    return fail(FE_ENOMESH,
+                "fe_wrap: mesh buffers differ from the bound ones; call fe_plan_bind_mesh "
+                "(the GPU layout is built once per mesh, not per apply)");
+  return fe_apply(p, start, end, dat0, dat2, dat3, dat4, FE_APPLY_ACCUMULATE, stream);
+}
+
+int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat1,
+                 const double* dat2, const double* dat3, const double* dat4,
+                 const int32_t* map0, const int32_t* map1) {
+  if (!p) return fail(FE_EINVAL, "null plan");
+  if (!p->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream, cudaStreamNonBlocking));
+  cudaStream_t s = p->hstream;
+  if (!p->d_map || p->b_coords != dat1 || p->b_map0 != map0 || p->b_map1 != map1 ||
+      (p->b_flags & FE_PTR_DEVICE)) {
+    return fail(FE_ENOMESH,
+                "fe_wrap_host: mesh buffers differ from the bound host buffers; call "
+                "fe_plan_bind_mesh with FE_PTR_HOST first");
+  }
+  const size_t n = (size_t)p->vs * p->nglobal;
+  if (p->cap_u < n) {
+    cudaFree(p->d_u);
+    cudaFree(p->d_y);
+    p->d_u = p->d_y = nullptr;
+    CUDA_TRY(cudaMalloc(&p->d_u, n * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&p->d_y, n * sizeof(double)));
+    p->cap_u = n;
+  }
+  const double* c0 = nullptr;
+  const double* c1 = nullptr;
+  if (dat3 && dat4) {
+    if (p->cap_c < (size_t)p->nverts) {
+      cudaFree(p->d_c0);
+      cudaFree(p->d_c1);
+      CUDA_TRY(cudaMalloc(&p->d_c0, p->nverts * sizeof(double)));
+      CUDA_TRY(cudaMalloc(&p->d_c1, p->nverts * sizeof(double)));
+      p->cap_c = p->nverts;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->d_c0, dat3, p->nverts * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(p->d_c1, dat4, p->nverts * sizeof(double), cudaMemcpyHostToDevice, s));
+    c0 = p->d_c0;
+    c1 = p->d_c1;
+  }
+  CUDA_TRY(cudaMemcpyAsync(p->d_u, dat2, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(p->d_y, dat0, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  int rc = fe_apply(p, start, end, p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dat0, p->d_y, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return FE_OK;
+}
+
+int fe_plan_get_info(const fe_plan* p, fe_plan_info* info) {
+  if (!p || !info) return fail(FE_EINVAL, "null argument");
+  std::memset(info, 0, sizeof *info);
+  std::snprintf(info->kernel, sizeof info->kernel, "%s", p->var->name);
+  info->threads_per_cell = 1;
+  info->block = p->var->block;
+  info->launches_per_apply = 1;
+  info->ncells = p->ncells;
+  info->nglobal = p->nglobal;
+  return FE_OK;
+}
+
+void fe_plan_destroy(fe_plan* p) {
+  if (!p) return;
+  free_mesh(p);
+  cudaFree(p->d_tables);
+  cudaFree(p->d_u);
+  cudaFree(p->d_y);
+  cudaFree(p->d_c0);
+  cudaFree(p->d_c1);
+  if (p->hstream) cudaStreamDestroy(p->hstream);
+  ::operator delete(p->host_params);
+  delete p;
+}
+
+}  // extern "C"

@@ -1,0 +1,325 @@
+"""Verification and measurement harness (mirror of the reference
+``fevec.bench``, ``/root/reference/pkg/src/fevec/bench.py``).
+
+Same names and meaning where the reference has them: ``make_bindings``
+(``bench.py:94-101``), ``random_coefficients`` (``:104-107``),
+``flops_per_cell``, ``bytes_per_cell``, ``arithmetic_intensity``,
+``verify_target`` (``:152-164``, raises ``VerificationError``),
+``run_configuration`` (``:167-224``), ``BenchmarkRecord``/``CSV_COLUMNS``/
+``write_csv`` (``:38-42,227-231``) and ``roofline_rows`` (``:234-259``).
+
+Differences, all deliberate:
+
+* ``flops_per_cell`` is the FROZEN algorithmic count of SURVEY.md Appendix B
+  (the minimum over a documented algorithm menu, FMA = 2 flops), not an
+  interpreter tally of one implementation: a kernel doing more work is
+  measured against it, one doing less legitimately scores higher;
+* ``bytes_per_cell`` is the compulsory-traffic model of SURVEY.md 8(d)
+  (u read once, y written once, coordinates, one int32 node map whose vertex
+  columns double as the vertex map, mu/lambda fields);
+* ``verify_target`` takes the oracle as a callable (the product package
+  never imports the oracle; tests and bench.py inject it);
+* timing uses CUDA events on the launching stream with an L2 flush between
+  applies; the default roofline peaks are the B200 figures measured on this
+  pool (FP64 DMMA 37.09 TFLOP/s: profiles/r01_fp64_peaks.json; HBM
+  6547.8 GB/s: MEASURED_PEAKS.json).
+"""
+
+from __future__ import annotations
+
+import csv
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .elements import OperatorSpec, integrand_degree, quadrature_rule
+from .mesh import DofMap, Mesh
+
+__all__ = [
+    "BenchmarkRecord", "CSV_COLUMNS", "VerificationError", "DEFAULT_PEAK_GFLOPS",
+    "DEFAULT_BANDWIDTH_GBS", "make_bindings", "random_coefficients", "flops_per_cell",
+    "bytes_per_cell", "arithmetic_intensity", "verify_target", "run_configuration",
+    "write_csv", "roofline_rows", "rel_err", "rel_l2",
+]
+
+CSV_COLUMNS = (
+    "operator", "cell", "degree", "target", "width", "ncells", "trials",
+    "time_best_s", "time_mean_s", "flops_per_cell", "gflops", "ai",
+    "speedup", "flags", "seed",
+    # B200 extensions
+    "gpus", "gdofs_per_s", "roofline_fraction", "parity_rel_l2", "cpu_cores", "cpu_time_s",
+)
+
+DEFAULT_PEAK_GFLOPS = 37094.0      # FP64 (DMMA) measured on this pool's B200s
+DEFAULT_DFMA_GFLOPS = 34162.0      # FP64 DFMA measured
+DEFAULT_BANDWIDTH_GBS = 6547.8     # MEASURED_PEAKS.json hbm_gbs
+
+
+class VerificationError(Exception):
+    pass
+
+
+@dataclass(frozen=True)
+class BenchmarkRecord:
+    operator: str
+    cell: str
+    degree: int
+    target: str
+    width: int
+    ncells: int
+    trials: int
+    time_best_s: float
+    time_mean_s: float
+    flops_per_cell: int
+    gflops: float
+    ai: float
+    speedup: float
+    flags: str
+    seed: int
+    gpus: int = 1
+    gdofs_per_s: float = 0.0
+    roofline_fraction: float = 0.0
+    parity_rel_l2: float = float("nan")
+    cpu_cores: int = 0
+    cpu_time_s: float = float("nan")
+
+    def row(self) -> list:
+        return [getattr(self, c) for c in CSV_COLUMNS]
+
+
+def make_bindings(mesh: Mesh, dofmap: DofMap, u, out, mu=None, lam=None) -> dict:
+    """Binding names -> buffers (reference bench.py:94-101); dat3/dat4 carry
+    the mu/lambda vertex fields of elasticity_lame."""
+    b = {
+        "dat0": out,
+        "dat1": np.ascontiguousarray(mesh.coords, dtype=np.float64).ravel(),
+        "dat2": np.ascontiguousarray(u, dtype=np.float64),
+        "map0": np.ascontiguousarray(dofmap.cell2dof, dtype=np.int32).ravel(),
+        "map1": np.ascontiguousarray(mesh.cell2vert, dtype=np.int32).ravel(),
+    }
+    if mu is not None:
+        b["dat3"] = np.ascontiguousarray(mu, dtype=np.float64)
+        b["dat4"] = np.ascontiguousarray(lam, dtype=np.float64)
+    return b
+
+
+def random_coefficients(spec: OperatorSpec, dofmap: DofMap, seed: int) -> np.ndarray:
+    """u ~ U(-1, 1) (reference bench.py:104-107)."""
+    rng = np.random.default_rng(seed)
+    n = spec.element.value_size * dofmap.ndofs_global
+    return rng.uniform(-1.0, 1.0, n)
+
+
+# ---------------------------------------------------------------------------
+# frozen flop model and compulsory bytes (8d)
+# ---------------------------------------------------------------------------
+
+
+def _interp_sumfact(d: int, p: int, q: int) -> int:
+    colloc = sum(2 * q ** s * p ** (d - s + 1) for s in range(1, d + 1)) + 2 * d * q ** (d + 1)
+    if d == 2:
+        direct = 4 * q * p * p + 4 * q * q * p
+    else:
+        direct = 4 * q * p ** 3 + 6 * q * q * p * p + 6 * q ** 3 * p
+    return min(colloc, direct)
+
+
+def flops_per_cell(spec: OperatorSpec, rule=None) -> int:
+    """Frozen minimum flop count per cell.  For
+    (form, cell) pairs outside the BASELINE configs it is the quadrature
+    algorithm's count, noted as such in DESIGN.md."""
+    if rule is None:
+        rule = quadrature_rule(spec.cell, integrand_degree(spec))
+    form, cell = spec.form, spec.cell
+    k = spec.element.degree
+    nd = spec.element.ndof_scalar
+    nq = rule.npoints
+    d = cell.dim
+    vs = spec.element.value_size
+    if cell.simplex and form == "mass":
+        return min(2 * nd * nd + nd + 8, 4 * nd * nq + 2 * nq + 8)
+    if cell.kind == "tetrahedron" and form == "helmholtz":
+        et = 14 * nd * nd + 13 * nd + 80
+        quad = 16 * nd * nq + 20 * nq + 80
+        split = 12 * nd * k ** 3 + 15 * k ** 3 + 2 * nd * nd + 2 * nd + 80
+        return min(et, quad, split)
+    if cell.kind == "hexahedron" and form == "laplacian_scalar":
+        p, q = k + 1, rule.npoints_1d
+        return 2 * _interp_sumfact(3, p, q) + 148 * q ** 3 + 36
+    if not cell.simplex and form == "elasticity_lame":
+        p, q = k + 1, rule.npoints_1d
+        P, g = (76, 8) if d == 2 else (254, 36)
+        sf = 2 * d * _interp_sumfact(d, p, q) + P * q ** d + g
+        dense = 4 * d * d * p ** d * q ** d + P * q ** d + g
+        return min(sf, dense)
+    if cell.kind == "tetrahedron" and form == "neohookean" and k == 2:
+        return nq * 543 + 52
+    # generic quadrature algorithm: interpolation and integration of values
+    # (2 nd per component) and reference gradients (2 nd d per component)
+    per_q = 0
+    if form in ("mass", "helmholtz"):
+        per_q += 4 * nd * vs
+    if form != "mass":
+        per_q += 4 * nd * d * vs + 4 * d * d * vs + 20
+    geo = 9 * d * d if not cell.simplex else 0
+    return nq * (per_q + geo) + 8 * d * d
+
+
+def bytes_per_cell(spec: OperatorSpec, mesh: Mesh, dofmap: DofMap) -> float:
+    """Compulsory bytes per cell."""
+    vs = spec.element.value_size
+    n = dofmap.ndofs_global
+    total = 8.0 * vs * n * 2 + 8.0 * mesh.dim * mesh.nvertices
+    total += 4.0 * dofmap.cell2dof.size
+    if spec.coefficient_fields:
+        total += 8.0 * 2 * mesh.nvertices
+    return total / mesh.ncells
+
+
+def arithmetic_intensity(spec, mesh, dofmap, rule=None) -> float:
+    return flops_per_cell(spec, rule) / bytes_per_cell(spec, mesh, dofmap)
+
+
+def roofline_time(spec, mesh, dofmap, rule=None, peak_gflops=DEFAULT_PEAK_GFLOPS,
+                  bandwidth_gbs=DEFAULT_BANDWIDTH_GBS) -> float:
+    """T_roof = max(F C / P_fp64, B / BW) in seconds."""
+    F = flops_per_cell(spec, rule) * mesh.ncells
+    B = bytes_per_cell(spec, mesh, dofmap) * mesh.ncells
+    return max(F / (peak_gflops * 1e9), B / (bandwidth_gbs * 1e9))
+
+
+# ---------------------------------------------------------------------------
+# verification
+# ---------------------------------------------------------------------------
+
+
+def rel_err(out, ref) -> float:
+    """Reference metric (bench.py:147-149)."""
+    out = np.asarray(out)
+    return float(np.abs(out - ref).max()) / max(float(np.abs(ref).max()), 1.0)
+
+
+def rel_l2(out, ref) -> float:
+    """North-star metric: ||out - ref||_2 / ||ref||_2."""
+    out = np.asarray(out)
+    den = float(np.linalg.norm(ref))
+    return float(np.linalg.norm(out - ref)) / (den if den > 0 else 1.0)
+
+
+def verify_target(spec, target, mesh, dofmap, rule, handle, u, rtol, oracle,
+                  mu=None, lam=None) -> float:
+    """Run the kernel once (host path) against ``oracle(...)`` -> reference
+    vector; raises VerificationError when rel-L2 exceeds rtol."""
+    ref = oracle(spec, mesh, dofmap, rule, u, mu, lam)
+    out = np.zeros_like(ref)
+    handle(0, mesh.ncells, make_bindings(mesh, dofmap, u, out, mu, lam))
+    err = rel_l2(out, ref)
+    if not err <= rtol:
+        raise VerificationError(
+            f"{spec.form} {spec.cell.kind} p{spec.element.degree} {target.kind}: "
+            f"relative L2 error {err:.3e} exceeds {rtol:.1e}")
+    return err
+
+
+# ---------------------------------------------------------------------------
+# GPU timing
+# ---------------------------------------------------------------------------
+
+
+class L2Flusher:
+    """Writes a buffer of 2x the L2 size between timed applies."""
+
+    def __init__(self, device=0):
+        import torch
+        l2 = torch.cuda.get_device_properties(device).L2_cache_size
+        self.buf = torch.empty(max(2 * l2, 1 << 20) // 4, dtype=torch.int32, device=device)
+
+    def __call__(self):
+        self.buf.fill_(1)
+
+
+def time_device(fn, trials=20, warmup=3, flush=True, stream=None):
+    """CUDA-event timing of ``fn()`` on ``stream`` with an optional L2 flush
+    outside each event pair.  Returns a list of seconds."""
+    import torch
+    stream = stream or torch.cuda.current_stream()
+    fl = L2Flusher() if flush else None
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(trials):
+        if fl:
+            fl()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    return times
+
+
+def run_configuration(spec, target, mesh, dofmap, trials=20, seed=0, rule=None, handle=None,
+                      oracle=None, verify_rtol=1e-12, u=None, mu=None, lam=None,
+                      skip_verify=False) -> BenchmarkRecord:
+    """Create the plan, verify against the oracle (when given), then time
+    ``trials`` applies over the whole mesh with CUDA events (reference
+    bench.py:167-224: verification-gated best/mean timing)."""
+    import torch
+    from .jit import compile_and_load, emit_for
+    if rule is None:
+        rule = quadrature_rule(spec.cell, integrand_degree(spec))
+    if handle is None:
+        handle = compile_and_load(emit_for(spec, target, rule))
+    if u is None:
+        u = random_coefficients(spec, dofmap, seed)
+    err = float("nan")
+    if oracle is not None and not skip_verify:
+        err = verify_target(spec, target, mesh, dofmap, rule, handle, u, verify_rtol, oracle, mu, lam)
+    dev = torch.device("cuda")
+    handle.bind(torch.as_tensor(np.ascontiguousarray(mesh.coords).ravel(), device=dev),
+                torch.as_tensor(np.ascontiguousarray(dofmap.cell2dof, np.int32).ravel(), device=dev),
+                torch.as_tensor(np.ascontiguousarray(mesh.cell2vert, np.int32).ravel(), device=dev),
+                nglobal=dofmap.ndofs_global)
+    ud = torch.as_tensor(u, device=dev)
+    yd = torch.zeros_like(ud)
+    coef = None
+    if mu is not None:
+        coef = (torch.as_tensor(mu, device=dev), torch.as_tensor(lam, device=dev))
+    times = time_device(lambda: handle.apply(ud, yd, coef=coef, overwrite=True), trials=trials)
+    best, mean = min(times), sum(times) / len(times)
+    fpc = flops_per_cell(spec, rule)
+    bpc = bytes_per_cell(spec, mesh, dofmap)
+    troof = roofline_time(spec, mesh, dofmap, rule)
+    return BenchmarkRecord(
+        operator=spec.form, cell=spec.cell.kind, degree=spec.element.degree,
+        target=handle.info["kernel"], width=handle.info["block"], ncells=mesh.ncells,
+        trials=trials, time_best_s=best, time_mean_s=mean, flops_per_cell=fpc,
+        gflops=fpc * mesh.ncells / best / 1e9, ai=fpc / bpc, speedup=1.0, flags="sm_100a",
+        seed=seed, gdofs_per_s=spec.element.value_size * dofmap.ndofs_global / best / 1e9,
+        roofline_fraction=troof / best, parity_rel_l2=err)
+
+
+def write_csv(records, fileobj) -> None:
+    w = csv.writer(fileobj)
+    w.writerow(CSV_COLUMNS)
+    for r in records:
+        w.writerow(r.row())
+
+
+def roofline_rows(records, peak_gflops=DEFAULT_PEAK_GFLOPS, bandwidth_gbs=DEFAULT_BANDWIDTH_GBS):
+    """Attainable performance per record and the ridge point (bench.py:234-259)."""
+    ridge = peak_gflops / bandwidth_gbs
+    rows = []
+    for r in records:
+        attainable = min(peak_gflops, r.ai * bandwidth_gbs)
+        rows.append({
+            "operator": r.operator, "cell": r.cell, "degree": r.degree, "target": r.target,
+            "width": r.width, "ai": r.ai, "gflops": r.gflops,
+            "attainable_gflops": attainable, "fraction_of_attainable": r.gflops / attainable,
+            "memory_bound": r.ai < ridge,
+        })
+    return ridge, rows
