@@ -21,7 +21,8 @@ namespace fe {
 
 template <int FORM, int DIM>
 constexpr int et_nmats() {
-  return (FORM == FE_FORM_MASS ? 1 : 0) + (FORM != FE_FORM_MASS ? DIM * (DIM + 1) / 2 : 0);
+  return ((FORM == FE_FORM_MASS || FORM == FE_FORM_HELMHOLTZ) ? 1 : 0) +
+         (FORM != FE_FORM_MASS ? DIM * (DIM + 1) / 2 : 0);
 }
 
 template <int NM, int ND>

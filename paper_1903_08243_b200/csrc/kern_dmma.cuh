@@ -1,4 +1,138 @@
-// FP64 tensor-core (DMMA) element-tensor kernels for high-degree simplices.
+// FP64 tensor-core (DMMA) element-tensor kernel for high-degree affine
+// simplices (C2 Helmholtz P3/P4 tetrahedra).
+//
+// For a group of 8 cells the element-tensor action is one small GEMM
+//   Y[i][e] = sum_m sum_j S_m[i][j] * (c_m(e) u_j(e)),
+//   A = [S_1 | ... | S_NM]   (ND x NM*ND, the same for every cell)
+//   B = [c_1 u; ...; c_NM u] (NM*ND x 8 cells, built on the fly),
+// which maps onto mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4; sm_100a has no FP64
+// tcgen05 kind).  A lives in shared memory in fragment order (one
+// conflict-free LDS.64 per fragment); B fragments never touch shared memory:
+// lane l holds u_j of cell l/4 for j = l%4 (mod 4) in registers, so a B
+// fragment is one DMUL c_m * u.  Each warp owns NT n-tiles (8 NT cells) per
+// iteration; CTAs are persistent and load A once.
+//
+// The M (output dof) dimension is padded to a multiple of 8 and each S_m's
+// K extent to a multiple of 4: 85% (P4) / 83% (P3) of the DMMA flops are
+// useful.  The scatter P_e^T is FP64 RED from the accumulator registers.
 #pragma once
 #include "common.cuh"
-#define FE_DMMA_VARIANTS
+#include "kern_affine.cuh"
+
+namespace fe {
+
+struct DmmaParams {
+  MeshView mesh;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  const double* __restrict__ afrag;  // [NM][KT][MT][32] fragment-ordered A
+  int32_t start, end;
+};
+
+FE_DEVICE void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int ND> struct DmmaShape {
+  static constexpr int KT = (ND + 3) / 4;  // k-steps per reference matrix
+  static constexpr int MT = (ND + 7) / 8;  // m-tiles of output dofs
+};
+
+template <int FORM, int DIM, int ND, int NT>
+__global__ void __launch_bounds__(256, 1) dmma_et_kernel(DmmaParams p) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  constexpr int KT = DmmaShape<ND>::KT, MT = DmmaShape<ND>::MT, NV = DIM + 1;
+  constexpr int ASIZE = NM * KT * MT * 32;
+  extern __shared__ double sA[];
+  {
+    const double2* src = reinterpret_cast<const double2*>(p.afrag);
+    double2* dst = reinterpret_cast<double2*>(sA);
+    for (int i = threadIdx.x; i < ASIZE / 2; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, c4 = lane & 3;
+  const int wpb = blockDim.x >> 5;
+  const int64_t cs = p.mesh.nc_stride;
+  const int ncell = p.end - p.start;
+  const int ngroups = (ncell + 8 * NT - 1) / (8 * NT);
+  const int gstride = gridDim.x * wpb;
+
+  for (int g = blockIdx.x * wpb + (threadIdx.x >> 5); g < ngroups; g += gstride) {
+    const int base = p.start + g * 8 * NT;
+    double ureg[NT][KT];
+    double cm[NT][NM];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int cell = base + nt * 8 + r;
+      const bool valid = cell < p.end;
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        const int j = 4 * t + c4;
+        double v = 0.0;
+        if (valid && j < ND) v = __ldg(p.u + __ldg(p.mesh.map + j * cs + cell));
+        ureg[nt][t] = v;
+      }
+      double X[NV][DIM];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        int vid = 0;
+        if (valid) vid = __ldg(p.mesh.vmap + v * cs + cell);
+        load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+      }
+      et_coeffs<FORM, DIM, NM>(X, cm[nt]);
+      if (!valid) {
+#pragma unroll
+        for (int m = 0; m < NM; ++m) cm[nt][m] = 0.0;
+      }
+    }
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+#pragma unroll
+      for (int kk = 0; kk < KT; ++kk) {
+        double b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = cm[nt][m] * ureg[nt][kk];
+        const double* a_ptr = sA + ((m * KT + kk) * MT) * 32 + lane;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double a = a_ptr[mt * 32];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt], a, b[nt]);
+        }
+      }
+    }
+    // scatter: acc[mt][nt][e] = Y[row = 8 mt + r][cell = base + 8 nt + 2 c4 + e]
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cell = base + nt * 8 + 2 * c4 + e;
+        if (cell < p.end) {
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const int row = 8 * mt + r;
+            if (row < ND) scatter_add(p.y, __ldg(p.mesh.map + row * cs + cell), acc[mt][nt][e]);
+          }
+        }
+      }
+  }
+}
+
+}  // namespace fe
+
+// registry hook (plan.cu)
+#define FE_DMMA_VARIANTS                                                                     \
+  DMV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 3, 20),                                    \
+  DMV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 4, 35),                                    \
+  DMV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 4, 35),                                         \
+  DMV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 4, 35),

@@ -64,6 +64,7 @@ struct fe_plan {
   // device tables (kernel-family specific layout)
   double* d_tables = nullptr;
   size_t tables_bytes = 0;
+  int persistent_ctas = 0;
   void* host_params = nullptr;  // by-value kernel parameter block (element-tensor kernels)
   size_t host_params_bytes = 0;
   // bound mesh
@@ -212,12 +213,70 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
 }
 
 // ---------------------------------------------------------------------------
+// DMMA element-tensor kernel (high-degree affine simplices)
+// ---------------------------------------------------------------------------
+
+constexpr int kDmmaNT = 2;
+constexpr int kDmmaBlock = 256;
+
+template <int FORM, int DIM, int ND>
+int dmma_prepare(fe_plan* p) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  constexpr int KT = DmmaShape<ND>::KT, MT = DmmaShape<ND>::MT;
+  std::vector<double> S;
+  element_matrices(p, FORM != FE_FORM_LAPLACIAN_SCALAR, FORM != FE_FORM_MASS, S);
+  if ((int)S.size() != NM * ND * ND) return fail(FE_EINVAL, "DMMA table size mismatch");
+  std::vector<double> A((size_t)NM * KT * MT * 32, 0.0);
+  for (int m = 0; m < NM; ++m)
+    for (int kk = 0; kk < KT; ++kk)
+      for (int mt = 0; mt < MT; ++mt)
+        for (int lane = 0; lane < 32; ++lane) {
+          int row = 8 * mt + (lane >> 2), col = 4 * kk + (lane & 3);
+          if (row < ND && col < ND)
+            A[(((size_t)m * KT + kk) * MT + mt) * 32 + lane] = S[((size_t)m * ND + row) * ND + col];
+        }
+  p->tables_bytes = A.size() * sizeof(double);
+  CUDA_TRY(cudaMalloc(&p->d_tables, p->tables_bytes));
+  CUDA_TRY(cudaMemcpy(p->d_tables, A.data(), p->tables_bytes, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaFuncSetAttribute(dmma_et_kernel<FORM, DIM, ND, kDmmaNT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
+  int dev = 0, sms = 0, per_sm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, dmma_et_kernel<FORM, DIM, ND, kDmmaNT>, kDmmaBlock, p->tables_bytes));
+  p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND>
+int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                const double*, const double*, cudaStream_t s) {
+  DmmaParams k;
+  k.mesh = mesh_view(p);
+  k.u = u;
+  k.y = y;
+  k.afrag = p->d_tables;
+  k.start = start;
+  k.end = end;
+  const int ngroups = (end - start + 8 * kDmmaNT - 1) / (8 * kDmmaNT);
+  const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
+  const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
+  dmma_et_kernel<FORM, DIM, ND, kDmmaNT><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+// ---------------------------------------------------------------------------
 // registry
 // ---------------------------------------------------------------------------
 
 #define QV(FORM, CELL, DIM, NV, K, ND, NQ, AFF)                                              \
   {FORM, CELL, K, NQ, 0, "quad", 128, quad_prepare<FORM, DIM, NV, ND, NQ, AFF>,           \
    quad_launch<FORM, DIM, NV, ND, NQ, AFF>}
+#define DMV(FORM, CELL, DIM, K, ND)                                                          \
+  {FORM, CELL, K, -1, 20, "dmma_element_tensor", kDmmaBlock, dmma_prepare<FORM, DIM, ND>,    \
+   dmma_launch<FORM, DIM, ND>}
 #define ETV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 10, "element_tensor", 128, et_prepare<FORM, DIM, ND>,                  \
    et_launch<FORM, DIM, ND>}
@@ -329,7 +388,8 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
   for (const Variant& v : kVariants) {
     if (v.form != p->form || v.cell != p->cell || v.degree != p->degree) continue;
     if (v.nq >= 0 && v.nq != p->nq) continue;
-    if (v.nq < 0 && p->q1d == 0 && v.priority >= 20) continue;  // tensor kernels need 1D factors
+    if (v.cell == FE_CELL_HEXAHEDRON || v.cell == FE_CELL_QUADRILATERAL)
+      if (v.nq < 0 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
     if (!best || v.priority > best->priority) best = &v;
   }
