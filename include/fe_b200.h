@@ -103,6 +103,7 @@ typedef struct fe_element_desc {
   const double* B1d;       /* [q1d][degree+1] 1D basis values at 1D points */
   const double* D1d;       /* [q1d][degree+1] 1D basis derivatives */
   const double* w1d;       /* [q1d] 1D weights on [0,1] */
+  const double* x1d;       /* [q1d] 1D Gauss points on [0,1] */
   const int32_t* lex;      /* [(degree+1)^dim] local node index of tensor node (x fastest) */
   double params[4];        /* neohookean: mu, lambda */
 } fe_element_desc;

@@ -39,7 +39,7 @@ class ElementDesc(ctypes.Structure):
         ("ndof", ctypes.c_int32), ("nvert", ctypes.c_int32), ("nq", ctypes.c_int32),
         ("qweights", _dp), ("phi", _dp), ("dphi", _dp), ("gphi", _dp), ("gdphi", _dp),
         ("q1d", ctypes.c_int32),
-        ("B1d", _dp), ("D1d", _dp), ("w1d", _dp), ("lex", _ip),
+        ("B1d", _dp), ("D1d", _dp), ("w1d", _dp), ("x1d", _dp), ("lex", _ip),
         ("params", ctypes.c_double * 4),
     ]
 

@@ -57,7 +57,7 @@ struct fe_plan {
   // element description (scalars copied; tables copied into vectors)
   int form, cell, degree, vs, dim, nv, nd, nq, q1d;
   double params[4];
-  std::vector<double> qw, phi, dphi, gphi, gdphi, B1d, D1d, w1d;
+  std::vector<double> qw, phi, dphi, gphi, gdphi, B1d, D1d, w1d, x1d;
   std::vector<int32_t> lex;
   const Variant* var = nullptr;
   uint32_t flags = 0;
@@ -65,6 +65,7 @@ struct fe_plan {
   double* d_tables = nullptr;
   size_t tables_bytes = 0;
   int persistent_ctas = 0;
+  int cells_per_block = 0;
   void* host_params = nullptr;  // by-value kernel parameter block (element-tensor kernels)
   size_t host_params_bytes = 0;
   // bound mesh
@@ -73,7 +74,9 @@ struct fe_plan {
   int64_t stride = 0;
   int32_t* d_map = nullptr;     // SoA [nd][stride]
   int32_t* d_vmap = nullptr;    // SoA [nv][stride] or == d_map
-  int32_t* d_map_rm = nullptr;  // row-major [ncells][nd] copy for CTA-per-cell kernels
+  int32_t* d_map_rm = nullptr;  // row-major [ncells][nd] copy
+  int32_t* d_map_lex = nullptr; // row-major, tensor (lexicographic) local order (tensor kernels)
+  int32_t* d_lex = nullptr;     // [nd] local node of tensor node
   double* d_coords = nullptr;   // padded [nverts][cstride]
   const void* b_coords = nullptr;
   const void* b_map0 = nullptr;
@@ -268,6 +271,61 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 }
 
 // ---------------------------------------------------------------------------
+// sum-factorised tensor-cell kernel
+// ---------------------------------------------------------------------------
+
+template <int FORM, int DIM, int P, int Q>
+int tensor_prepare(fe_plan* p) {
+  using TP = TensorParams<Q, P>;
+  using SM = TensorSmem<DIM, P, Q, form_vs(FORM, DIM)>;
+  static_assert(sizeof(TP) <= 32000, "parameter block too large");
+  if (p->q1d != Q || p->degree + 1 != P) return fail(FE_EINVAL, "tensor factors do not match the kernel");
+  TP* hp = new TP();
+  for (int a = 0; a < Q; ++a) {
+    for (int i = 0; i < P; ++i) {
+      hp->B[a][i] = p->B1d[a * P + i];
+      hp->D[a][i] = p->D1d[a * P + i];
+    }
+    hp->w[a] = p->w1d[a];
+  }
+  const int stride = DIM == 3 ? Q * Q : Q;
+  (void)stride;
+  for (int a = 0; a < Q; ++a) hp->x[a] = p->x1d[a];
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(TP);
+  constexpr int TS = DIM == 3 ? Q * Q : Q;
+  constexpr int CPB = 256 / TS;
+  p->tables_bytes = (size_t)CPB * SM::size * sizeof(double);
+  CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
+  p->cells_per_block = CPB;
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int P, int Q>
+int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                  const double* c0, const double* c1, cudaStream_t s) {
+  using TP = TensorParams<Q, P>;
+  TP* hp = static_cast<TP*>(p->host_params);
+  if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
+  hp->mesh = mesh_view(p);
+  hp->maplex = p->d_map_lex;
+  hp->u = u;
+  hp->y = y;
+  hp->mu = c0;
+  hp->lam = c1;
+  hp->start = start;
+  hp->end = end;
+  hp->p0 = p->params[0];
+  hp->p1 = p->params[1];
+  const int n = end - start;
+  const int cpb = p->cells_per_block;
+  tensor_kernel<FORM, DIM, P, Q><<<(n + cpb - 1) / cpb, 256, p->tables_bytes, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+// ---------------------------------------------------------------------------
 // registry
 // ---------------------------------------------------------------------------
 
@@ -277,6 +335,9 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define DMV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 20, "dmma_element_tensor", kDmmaBlock, dmma_prepare<FORM, DIM, ND>,    \
    dmma_launch<FORM, DIM, ND>}
+#define TV(FORM, CELL, DIM, K, P, Q)                                                         \
+  {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised", 256,                 \
+   tensor_prepare<FORM, DIM, P, Q>, tensor_launch<FORM, DIM, P, Q>}
 #define ETV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 10, "element_tensor", 128, et_prepare<FORM, DIM, ND>,                  \
    et_launch<FORM, DIM, ND>}
@@ -351,6 +412,15 @@ __global__ void k_transpose_map(const int32_t* __restrict__ rm, int32_t* __restr
   soa[i * stride + c] = rm[t];
 }
 
+__global__ void k_permute_rows(const int32_t* __restrict__ rm, const int32_t* __restrict__ perm,
+                               int32_t* __restrict__ out, int nc, int nd) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * nd) return;
+  int64_t c = t / nd;
+  int l = (int)(t % nd);
+  out[t] = rm[c * nd + perm[l]];
+}
+
 __global__ void k_pad_coords(const double* __restrict__ x, double* __restrict__ out, int nv, int dim,
                              int cstride) {
   int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -377,8 +447,9 @@ void free_mesh(fe_plan* p) {
   if (p->d_vmap && p->d_vmap != p->d_map) cudaFree(p->d_vmap);
   cudaFree(p->d_map);
   cudaFree(p->d_map_rm);
+  cudaFree(p->d_map_lex);
   cudaFree(p->d_coords);
-  p->d_map = p->d_vmap = p->d_map_rm = nullptr;
+  p->d_map = p->d_vmap = p->d_map_rm = p->d_map_lex = nullptr;
   p->d_coords = nullptr;
   p->b_coords = p->b_map0 = p->b_map1 = nullptr;
 }
@@ -389,7 +460,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.form != p->form || v.cell != p->cell || v.degree != p->degree) continue;
     if (v.nq >= 0 && v.nq != p->nq) continue;
     if (v.cell == FE_CELL_HEXAHEDRON || v.cell == FE_CELL_QUADRILATERAL)
-      if (v.nq < 0 && p->q1d == 0) continue;  // tensor kernels need 1D factors
+      if (v.priority >= 20 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
     if (!best || v.priority > best->priority) best = &v;
   }
@@ -441,13 +512,14 @@ int fe_plan_create(fe_plan** out, const fe_element_desc* d, uint32_t flags) {
   p->gdphi.assign(d->gdphi, d->gdphi + (size_t)nq * nv * dim);
   if (p->q1d > 0) {
     const int pp = p->degree + 1;
-    if (!d->B1d || !d->D1d || !d->w1d || !d->lex) {
+    if (!d->B1d || !d->D1d || !d->w1d || !d->x1d || !d->lex) {
       delete p;
       return fail(FE_EINVAL, "missing tensor factors");
     }
     p->B1d.assign(d->B1d, d->B1d + (size_t)p->q1d * pp);
     p->D1d.assign(d->D1d, d->D1d + (size_t)p->q1d * pp);
     p->w1d.assign(d->w1d, d->w1d + p->q1d);
+    p->x1d.assign(d->x1d, d->x1d + p->q1d);
     int n = 1;
     for (int a = 0; a < dim; ++a) n *= pp;
     p->lex.assign(d->lex, d->lex + n);
@@ -496,6 +568,15 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     int64_t n = (int64_t)ncells * nd;
     k_transpose_map<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, p->d_map, ncells, nd, p->stride);
     k_check_range<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, n, nglobal, d_flag);
+  }
+  if (!p->lex.empty() && ncells > 0) {
+    if (!p->d_lex) {
+      CUDA_TRY(cudaMalloc(&p->d_lex, p->lex.size() * sizeof(int32_t)));
+      CUDA_TRY(cudaMemcpy(p->d_lex, p->lex.data(), p->lex.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    CUDA_TRY(cudaMalloc(&p->d_map_lex, mbytes));
+    int64_t n = (int64_t)ncells * nd;
+    k_permute_rows<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, p->d_lex, p->d_map_lex, ncells, nd);
   }
   p->d_vmap = p->d_map;
   int32_t* d_m1 = nullptr;
@@ -628,6 +709,7 @@ void fe_plan_destroy(fe_plan* p) {
   if (!p) return;
   free_mesh(p);
   cudaFree(p->d_tables);
+  cudaFree(p->d_lex);
   cudaFree(p->d_u);
   cudaFree(p->d_y);
   cudaFree(p->d_c0);

@@ -135,11 +135,13 @@ class GpuKernelHandle:
             keep["B"] = np.ascontiguousarray(tf.B)
             keep["D"] = np.ascontiguousarray(tf.D)
             keep["w"] = np.ascontiguousarray(tf.w)
+            keep["x"] = np.ascontiguousarray(tf.x)
             keep["lex"] = np.ascontiguousarray(tf.lex, dtype=np.int32)
             d.q1d = rule.npoints_1d
             d.B1d = _dptr(keep["B"])
             d.D1d = _dptr(keep["D"])
             d.w1d = _dptr(keep["w"])
+            d.x1d = _dptr(keep["x"])
             d.lex = ctypes.cast(keep["lex"].ctypes.data, ctypes.POINTER(ctypes.c_int32))
         for i, v in enumerate(spec.params[:4]):
             d.params[i] = v
