@@ -7,12 +7,19 @@ PKG := paper_1903_08243_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
 HDR := $(wildcard $(PKG)/csrc/*.cuh) include/fe_b200.h
 
-all: $(PKG)/libfeb200.so
+all: $(PKG)/libfeb200.so oracle/liboracle.so
+
+oracle: oracle/liboracle.so
+
+# the oracle's C restatement (test/baseline infrastructure); the reference's
+# BENCH_FLAGS (jit.py:27) with a portable AVX-512 target
+oracle/liboracle.so: oracle/fe_oracle.c
+	gcc -O3 -march=x86-64-v4 -ffast-math -fopenmp -shared -fPIC -o $@ $< -lm
 
 $(PKG)/libfeb200.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -o $@ $(SRC)
 
 clean:
-	rm -f $(PKG)/libfeb200.so
+	rm -f $(PKG)/libfeb200.so oracle/liboracle.so
 
-.PHONY: all clean
+.PHONY: all clean oracle

@@ -1,0 +1,189 @@
+"""Element partition across GPUs with shared-dof halo sums.
+
+The reference is single-process; the paper ran one MPI
+process per core over a partitioned mesh.  Here: one process
+per GPU (torchrun), the structured mesh is cut into z-slabs of whole cube
+layers, every rank assembles y_local = sum over ITS cells P_e^T A_e(P_e u)
+with the sm_100a kernels, and the only exchange is the sum of the partial
+results on the node planes two neighbouring slabs share:
+
+    rank r:  y[top plane]    += y_{r+1}[bottom plane]
+             y[bottom plane] += y_{r-1}[top plane]
+
+done with NCCL point-to-point send/recv (torch.distributed batch P2P, one
+group per apply).  Both neighbours end with the fully summed interface
+values, so the distributed y restricted to each slab equals the
+single-domain y (partition independence, reference test_reference.py:72-89).
+
+Slab-local numbering: nodes of the k-refined lattice in lexicographic order
+(x fastest, z slowest), so the bottom/top interface planes are the first and
+last Lx*Ly nodes -- contiguous buffers, no gather/scatter lists.  Inputs are
+drawn per lattice plane from SeedSequence((seed, stream, plane)), so a plane
+shared by two ranks gets identical coordinates and coefficients on both.
+
+Scaling mode: WEAK -- every rank owns a slab of the config's full per-GPU
+size (nx x ny x nz cubes); the global mesh is nx x ny x (nz * world).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .configs import Config
+from .elements import operator_spec, quadrature_rule
+from .mesh import DofMap, Mesh, kuhn_tets
+
+__all__ = ["Slab", "build_slab", "DistributedOperator"]
+
+
+@dataclass
+class Slab:
+    config: Config
+    spec: object
+    rule: object
+    mesh: Mesh
+    dofmap: DofMap
+    u: np.ndarray
+    mu: np.ndarray
+    lam: np.ndarray
+    z0: int            # first cube layer (global)
+    z1: int            # one past the last cube layer
+    nz_global: int
+    plane: int         # nodes per lattice plane (Lx * Ly)
+
+    @property
+    def ndofs(self) -> int:
+        return self.spec.element.value_size * self.dofmap.ndofs_global
+
+    @property
+    def has_below(self) -> bool:
+        return self.z0 > 0
+
+    @property
+    def has_above(self) -> bool:
+        return self.z1 < self.nz_global
+
+
+def _plane_rng(seed, stream, plane):
+    return np.random.default_rng(np.random.SeedSequence([seed, stream, plane]))
+
+
+def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab:
+    """Cube layers [z0, z1) of the global nx x ny x nz_global mesh of a 3D
+    config, with slab-local lattice numbering."""
+    if len(cfg.n) != 3:
+        raise ValueError("slab partition needs a 3D config")
+    nx, ny, _ = cfg.n
+    nzl = z1 - z0
+    spec = operator_spec(cfg.form, cfg.cell, cfg.degree)
+    rule = quadrature_rule(cfg.cell, cfg.qdegree)
+    k = spec.element.degree
+    vs = spec.element.value_size
+    # vertices of the slab: planes z0..z1
+    xs = np.linspace(0.0, 1.0, nx + 1)
+    ys = np.linspace(0.0, 1.0, ny + 1)
+    hz = 1.0 / nz_global
+    coords = np.empty(((nzl + 1), (ny + 1), (nx + 1), 3))
+    Y, X = np.meshgrid(ys, xs, indexing="ij")
+    h = np.array([1.0 / nx, 1.0 / ny, hz])
+    for lz in range(nzl + 1):
+        gz = z0 + lz
+        coords[lz, :, :, 0] = X
+        coords[lz, :, :, 1] = Y
+        coords[lz, :, :, 2] = gz * hz
+        if cfg.jitter and 0 < gz < nz_global:
+            d = _plane_rng(seed, 0, gz).uniform(-1.0, 1.0, size=((ny + 1) * (nx + 1), 3)) * (0.1 * h)
+            d = d.reshape(ny + 1, nx + 1, 3)
+            inner = np.zeros((ny + 1, nx + 1), bool)
+            inner[1:-1, 1:-1] = True
+            coords[lz][inner] += d[inner]
+    coords = coords.reshape(-1, 3)
+    # cells: cubes z-slowest, 6 Kuhn tets or one hex per cube
+    l, j, i = np.meshgrid(np.arange(nzl), np.arange(ny), np.arange(nx), indexing="ij")
+    base = (i + (nx + 1) * (j + (ny + 1) * l)).ravel()
+    corner = np.array([(b & 1) + (nx + 1) * (((b >> 1) & 1) + (ny + 1) * ((b >> 2) & 1))
+                       for b in range(8)], dtype=np.int64)
+    cells_bits = kuhn_tets() if cfg.cell == "tetrahedron" else np.arange(8)[None, :]
+    c2v = (base[:, None, None] + corner[cells_bits][None, :, :]).reshape(-1, cells_bits.shape[1])
+    mesh = Mesh(coords, np.ascontiguousarray(c2v, np.int32), spec.cell, (nx, ny, nzl))
+    # slab-local lattice numbering (x fastest, z slowest)
+    Lx, Ly, Lz = k * nx + 1, k * ny + 1, k * nzl + 1
+    vi = c2v % (nx + 1)
+    vj = (c2v // (nx + 1)) % (ny + 1)
+    vl = c2v // ((nx + 1) * (ny + 1))
+    V = np.stack([vi, vj, vl], axis=-1)
+    nodes = np.array([[int(x * k) for x in node] for node in spec.element.nodes], dtype=np.int64)
+    if spec.cell.simplex:
+        P = k * V[:, None, 0, :] + np.einsum("ia,cad->cid", nodes, V[:, 1:, :] - V[:, None, 0, :])
+    else:
+        P = k * V[:, None, 0, :] + nodes[None, :, :]
+    dof = P[..., 0] + Lx * (P[..., 1] + Ly * P[..., 2])
+    dm = DofMap(np.ascontiguousarray(dof, np.int32), Lx * Ly * Lz, spec.element)
+    # coefficients per lattice plane
+    plane = Lx * Ly
+    u = np.empty((Lz, plane * vs))
+    for L in range(Lz):
+        u[L] = _plane_rng(seed, 1, k * z0 + L).uniform(-1.0, 1.0, plane * vs)
+    u = u.ravel()
+    if cfg.u_scale == "h":
+        u *= 0.01 / max(nx, ny, nz_global)
+    mu = lam = None
+    if spec.coefficient_fields:
+        nvp = (nx + 1) * (ny + 1)
+        mu = np.concatenate([_plane_rng(seed, 2, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
+        lam = np.concatenate([_plane_rng(seed, 3, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
+    return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane)
+
+
+class DistributedOperator:
+    """y = A u on this rank's slab, interface planes summed with the
+    neighbouring ranks.  ``local_apply(u, y)`` computes the slab-local
+    action (overwrite); ``torch.distributed`` must be initialised (NCCL for
+    CUDA tensors, gloo for CPU tensors)."""
+
+    def __init__(self, slab: Slab, local_apply, rank: int, world: int):
+        self.slab = slab
+        self.local_apply = local_apply
+        self.rank = rank
+        self.world = world
+        self.n_if = slab.plane * slab.spec.element.value_size
+        self._bufs = None
+
+    def _buffers(self, y):
+        import torch
+        if self._bufs is None or self._bufs[0].device != y.device:
+            self._bufs = (torch.empty(self.n_if, dtype=y.dtype, device=y.device),
+                          torch.empty(self.n_if, dtype=y.dtype, device=y.device))
+        return self._bufs
+
+    def exchange(self, y):
+        """Sum the interface planes with the neighbours (in place)."""
+        import torch.distributed as dist
+        n = self.n_if
+        below, above = self._buffers(y)
+        ops = []
+        if self.slab.has_below:
+            ops.append(dist.P2POp(dist.isend, y[:n].contiguous(), self.rank - 1))
+            ops.append(dist.P2POp(dist.irecv, below, self.rank - 1))
+        if self.slab.has_above:
+            ops.append(dist.P2POp(dist.isend, y[-n:].contiguous(), self.rank + 1))
+            ops.append(dist.P2POp(dist.irecv, above, self.rank + 1))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if self.slab.has_below:
+            y[:n] += below
+        if self.slab.has_above:
+            y[-n:] += above
+
+    def apply(self, u, y):
+        self.local_apply(u, y)
+        self.exchange(y)
+        return y
+
+
+def slab_range(rank: int, world: int, nz_per_rank: int):
+    """Weak scaling: rank r owns cube layers [r nz, (r+1) nz)."""
+    return rank * nz_per_rank, (rank + 1) * nz_per_rank, world * nz_per_rank

@@ -1,0 +1,92 @@
+"""Multi-rank element partition + halo sums on CPU (gloo, world_size 2 and 3).
+
+The local slab action is the CPU oracle here (the GPU path plugs the sm_100a
+plan into the same DistributedOperator); the test checks the partition
+logic, slab-local numbering, seeded per-plane inputs and the interface
+exchange: gathered distributed y == single-domain y (reference
+test_reference.py:72-89 partition independence, SURVEY.md 8e parity)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1903_08243_b200 import configs as C
+from paper_1903_08243_b200.distributed import DistributedOperator, build_slab, slab_range
+from oracle import fe_oracle as fo
+
+
+def _oracle_apply(slab):
+    P = fo.Problem(slab.spec.form, slab.spec.cell.kind, slab.spec.element.degree,
+                   slab.rule.exactness_degree, slab.spec.params)
+
+    def apply(u, y):
+        y.copy_(torch.from_numpy(fo.assemble(P, slab.mesh.coords, slab.mesh.cell2vert,
+                                             slab.dofmap.cell2dof, u.numpy(), slab.mu, slab.lam)))
+    return apply
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, name, nz, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = C.get_config(name, (3, 2, nz))
+    z0, z1, nzg = slab_range(rank, world, nz)
+    slab = build_slab(cfg, 11, z0, z1, nzg)
+    op = DistributedOperator(slab, _oracle_apply(slab), rank, world)
+    u = torch.from_numpy(slab.u.copy())
+    y = torch.zeros_like(u)
+    op.apply(u, y)
+    q.put((rank, z0, y.numpy().copy(), slab.u.copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("C2-P2", 2), ("C5", 2), ("C3-Q2", 3), ("C4-hex-Q1", 2)])
+def test_distributed_equals_single_domain(name, world):
+    nz = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, nz, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = C.get_config(name, (3, 2, nz))
+    glob = build_slab(cfg, 11, 0, nz * world, nz * world)
+    P = fo.Problem(glob.spec.form, glob.spec.cell.kind, glob.spec.element.degree,
+                   glob.rule.exactness_degree, glob.spec.params)
+    y_glob = fo.assemble(P, glob.mesh.coords, glob.mesh.cell2vert, glob.dofmap.cell2dof, glob.u,
+                         glob.mu, glob.lam)
+    k = glob.spec.element.degree
+    per_plane = glob.plane * glob.spec.element.value_size
+    for rank, z0, y, u in results:
+        off = k * z0 * per_plane
+        assert np.array_equal(u, glob.u[off:off + u.size])          # consistent inputs
+        assert fo.rel_l2(y, y_glob[off:off + y.size]) <= 1e-14, rank
+
+
+def test_slab_of_whole_mesh_matches_config_shape():
+    cfg = C.get_config("C2-P1", (4, 4, 4))
+    s = build_slab(cfg, 0, 0, 4, 4)
+    assert s.mesh.ncells == cfg.ncells
+    assert s.dofmap.ndofs_global == 5 ** 3
+    # positive orientation everywhere
+    X = s.mesh.coords[s.mesh.cell2vert]
+    det = np.linalg.det(X[:, 1:] - X[:, :1])
+    assert (det > 0).all()
