@@ -87,15 +87,15 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
       for (int c = 0; c < VS; ++c) sU[c * ND + idx] = __ldg(p.u + VS * dof + c);
     }
-    if (t < NV) {
-      const int vid = __ldg(p.mesh.vmap + t * cs + cell);
+    for (int v = t; v < NV; v += TS) {
+      const int vid = __ldg(p.mesh.vmap + v * cs + cell);
       double xv[DIM];
       load_vertex<DIM>(p.mesh.coords, vid, xv);
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) sX[t * DIM + a] = xv[a];
+      for (int a = 0; a < DIM; ++a) sX[v * DIM + a] = xv[a];
       if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
-        sm[SM::MU + t] = __ldg(p.mu + vid);
-        sm[SM::LAM + t] = __ldg(p.lam + vid);
+        sm[SM::MU + v] = __ldg(p.mu + vid);
+        sm[SM::LAM + v] = __ldg(p.lam + vid);
       }
     }
   }
