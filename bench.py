@@ -142,7 +142,8 @@ def build_ops(names, seed, device, rank, world):
         m, dm = prob.mesh, prob.dofmap
         h.bind(torch.tensor(np.asarray(m.coords).ravel(), device=device),
                torch.tensor(np.asarray(dm.cell2dof, np.int32).ravel(), device=device),
-               None, nglobal=dm.ndofs_global)
+               torch.tensor(np.asarray(m.cell2vert, np.int32).ravel(), device=device),
+               nglobal=dm.ndofs_global)
         u = torch.tensor(prob.u, device=device)
         y = torch.zeros_like(u)
         coef = None

@@ -441,6 +441,14 @@ __global__ void k_check_range(const int32_t* __restrict__ m, int64_t n, int64_t 
   if (t < n && (m[t] < 0 || m[t] >= hi)) *flag = 1;
 }
 
+__global__ void k_check_vertex_cols(const int32_t* __restrict__ map0, int nc, int nd, int nv,
+                                    int64_t nverts, int* flag) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * nv) return;
+  int32_t v = map0[(t / nv) * nd + t % nv];
+  if (v < 0 || v >= nverts) *flag = 1;
+}
+
 namespace {
 
 void free_mesh(fe_plan* p) {
@@ -587,6 +595,12 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     int64_t n = (int64_t)ncells * nv;
     k_check_vmap<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, d_m1, ncells, nd, nv, d_flag + 1);
     k_check_range<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(d_m1, n, nverts, d_flag);
+  } else if (ncells > 0) {
+    // no vertex map given: map0[:, :nv] must be it -- at least every entry
+    // must address a vertex (guards the coordinate gathers)
+    int64_t n = (int64_t)ncells * nv;
+    k_check_vertex_cols<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, nv,
+                                                                  nverts, d_flag);
   }
   // coordinates, padded to 16/32 bytes per vertex
   double* d_x = nullptr;

@@ -153,3 +153,30 @@ def test_run_configuration_verifies_and_times():
     rec = fe.run_configuration(prob.spec, fe.Target(), prob.mesh, prob.dofmap, trials=5,
                                rule=prob.rule, oracle=oracle_fn, u=prob.u)
     assert rec.parity_rel_l2 <= TOL and rec.time_best_s > 0 and rec.gflops > 0
+
+
+@pytest.mark.parametrize("name", ["C2-P2", "C2-P4", "C3-Q2", "C4-hex-Q1", "C5"])
+def test_gpu_on_slab_numbering_with_separate_vertex_map(name):
+    """Slab-local lattice numbering (distributed.py): dof ids are NOT vertex
+    ids, so the plan must keep the separate vertex map (map1)."""
+    import torch
+    from paper_1903_08243_b200.distributed import build_slab
+    cfg = C.get_config(name, (3, 2, 2))
+    s = build_slab(cfg, 5, 0, 2, 4)
+    h = handle_for(s.spec, s.rule)
+    out = np.zeros(s.ndofs)
+    h(0, s.mesh.ncells, fe.make_bindings(s.mesh, s.dofmap, s.u, out, s.mu, s.lam))
+    ref = oracle_fn(s.spec, s.mesh, s.dofmap, s.rule, s.u, s.mu, s.lam)
+    assert fe.harness.rel_l2(out, ref) <= TOL
+
+
+def test_missing_vertex_map_with_non_vertex_numbering_is_rejected():
+    import torch
+    from paper_1903_08243_b200.distributed import build_slab
+    s = build_slab(C.get_config("C2-P2", (3, 2, 2)), 5, 0, 2, 2)
+    h = handle_for(s.spec, s.rule)
+    dev = torch.device("cuda")
+    with pytest.raises(fe.jit.KernelError, match="out of range"):
+        h.bind(torch.tensor(np.asarray(s.mesh.coords).ravel(), device=dev),
+               torch.tensor(np.asarray(s.dofmap.cell2dof, np.int32).ravel(), device=dev), None,
+               nglobal=s.dofmap.ndofs_global)

@@ -33,7 +33,8 @@ def main():
     dev = torch.device("cuda")
     m, dm = prob.mesh, prob.dofmap
     h.bind(torch.as_tensor(np.array(m.coords).ravel(), device=dev),
-           torch.as_tensor(np.array(dm.cell2dof, np.int32).ravel(), device=dev), None,
+           torch.as_tensor(np.array(dm.cell2dof, np.int32).ravel(), device=dev),
+           torch.as_tensor(np.array(m.cell2vert, np.int32).ravel(), device=dev),
            nglobal=dm.ndofs_global)
     u = torch.as_tensor(prob.u, device=dev)
     y = torch.zeros_like(u)
