@@ -291,6 +291,24 @@ int tensor_prepare(fe_plan* p) {
   const int stride = DIM == 3 ? Q * Q : Q;
   (void)stride;
   for (int a = 0; a < Q; ++a) hp->x[a] = p->x1d[a];
+  // collocation derivative at the Gauss points: Dc[a][e] = l_e'(x_a) for the
+  // Lagrange basis l_e on the Gauss points (barycentric formula)
+  double bw[Q];
+  for (int e = 0; e < Q; ++e) {
+    double prod = 1.0;
+    for (int m = 0; m < Q; ++m)
+      if (m != e) prod *= hp->x[e] - hp->x[m];
+    bw[e] = 1.0 / prod;
+  }
+  for (int a = 0; a < Q; ++a) {
+    double diag = 0.0;
+    for (int e = 0; e < Q; ++e) {
+      if (e == a) continue;
+      hp->Dc[a][e] = (bw[e] / bw[a]) / (hp->x[a] - hp->x[e]);
+      diag -= hp->Dc[a][e];
+    }
+    hp->Dc[a][a] = diag;
+  }
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
   constexpr int TS = DIM == 3 ? Q * Q : Q;
