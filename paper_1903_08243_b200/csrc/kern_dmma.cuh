@@ -40,8 +40,8 @@ template <int ND> struct DmmaShape {
   static constexpr int MT = (ND + 7) / 8;  // m-tiles of output dofs
 };
 
-template <int FORM, int DIM, int ND, int NT>
-__global__ void __launch_bounds__(256, 1) dmma_et_kernel(DmmaParams p) {
+template <int FORM, int DIM, int ND, int NT, int MINB>
+__global__ void __launch_bounds__(256, MINB) dmma_et_kernel(DmmaParams p) {
   constexpr int NM = et_nmats<FORM, DIM>();
   constexpr int KT = DmmaShape<ND>::KT, MT = DmmaShape<ND>::MT, NV = DIM + 1;
   constexpr int ASIZE = NM * KT * MT * 32;

@@ -7,6 +7,7 @@
 // the GPU layout (element-batched SoA maps, padded coordinates).
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,6 +66,7 @@ struct fe_plan {
   double* d_tables = nullptr;
   size_t tables_bytes = 0;
   int persistent_ctas = 0;
+  int dmma_cfg = 0;
   int cells_per_block = 0;
   void* host_params = nullptr;  // by-value kernel parameter block (element-tensor kernels)
   size_t host_params_bytes = 0;
@@ -219,8 +221,24 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
 // DMMA element-tensor kernel (high-degree affine simplices)
 // ---------------------------------------------------------------------------
 
-constexpr int kDmmaNT = 2;
 constexpr int kDmmaBlock = 256;
+
+// (NT, MINB) configurations of the DMMA kernel: 0 = (2,1), 1 = (1,2),
+// 2 = (2,2), 3 = (1,1); FE_DMMA_CFG selects one for experiments, the
+// default is the measured best.
+
+template <int FORM, int DIM, int ND, int NT, int MINB>
+int dmma_setup(fe_plan* p) {
+  CUDA_TRY(cudaFuncSetAttribute(dmma_et_kernel<FORM, DIM, ND, NT, MINB>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
+  int dev = 0, sms = 0, per_sm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, dmma_et_kernel<FORM, DIM, ND, NT, MINB>, kDmmaBlock, p->tables_bytes));
+  p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  return FE_OK;
+}
 
 template <int FORM, int DIM, int ND>
 int dmma_prepare(fe_plan* p) {
@@ -241,14 +259,24 @@ int dmma_prepare(fe_plan* p) {
   p->tables_bytes = A.size() * sizeof(double);
   CUDA_TRY(cudaMalloc(&p->d_tables, p->tables_bytes));
   CUDA_TRY(cudaMemcpy(p->d_tables, A.data(), p->tables_bytes, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaFuncSetAttribute(dmma_et_kernel<FORM, DIM, ND, kDmmaNT>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
-  int dev = 0, sms = 0, per_sm = 0;
-  CUDA_TRY(cudaGetDevice(&dev));
-  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, dmma_et_kernel<FORM, DIM, ND, kDmmaNT>, kDmmaBlock, p->tables_bytes));
-  p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  const char* env = getenv("FE_DMMA_CFG");
+  p->dmma_cfg = env ? atoi(env) : 0;
+  if (p->dmma_cfg < 0 || p->dmma_cfg > 3) p->dmma_cfg = 0;
+  switch (p->dmma_cfg) {
+    case 1: return dmma_setup<FORM, DIM, ND, 1, 2>(p);
+    case 2: return dmma_setup<FORM, DIM, ND, 2, 2>(p);
+    case 3: return dmma_setup<FORM, DIM, ND, 1, 1>(p);
+    default: return dmma_setup<FORM, DIM, ND, 2, 1>(p);
+  }
+}
+
+template <int FORM, int DIM, int ND, int NT, int MINB>
+int dmma_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_t s) {
+  const int ngroups = (n + 8 * NT - 1) / (8 * NT);
+  const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
+  const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
+  dmma_et_kernel<FORM, DIM, ND, NT, MINB><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k);
+  CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
 
@@ -262,12 +290,12 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   k.afrag = p->d_tables;
   k.start = start;
   k.end = end;
-  const int ngroups = (end - start + 8 * kDmmaNT - 1) / (8 * kDmmaNT);
-  const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
-  const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
-  dmma_et_kernel<FORM, DIM, ND, kDmmaNT><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k);
-  CUDA_TRY(cudaGetLastError());
-  return FE_OK;
+  switch (p->dmma_cfg) {
+    case 1: return dmma_run<FORM, DIM, ND, 1, 2>(p, k, end - start, s);
+    case 2: return dmma_run<FORM, DIM, ND, 2, 2>(p, k, end - start, s);
+    case 3: return dmma_run<FORM, DIM, ND, 1, 1>(p, k, end - start, s);
+    default: return dmma_run<FORM, DIM, ND, 2, 1>(p, k, end - start, s);
+  }
 }
 
 // ---------------------------------------------------------------------------
