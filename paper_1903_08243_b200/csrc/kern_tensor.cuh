@@ -17,17 +17,28 @@
 //    polynomial, which its q Gauss values determine.
 // followed by the pointwise flux and the transposed chain back to the nodes.
 //
-// GPU mapping: a TEAM of Q^2 threads (3D) or Q threads (2D) per cell,
-// 256-thread CTAs holding 256/team cells.  Every contraction stage assigns
-// one thread per 1D pencil: the thread loads the inputs along the
-// contraction direction from shared memory into registers once and emits a
-// whole output pencil, so each shared-memory load feeds Q FMAs; B, D and Dc
-// are passed by value in the kernel parameter block and enter the DFMAs as
-// uniform constant-bank operands.  After the x-stage one thread holds all Q
-// points of an x-pencil and evaluates the flux there: the trilinear Jacobian
-// is recomputed per point (as kernels.py:136-151 does per qp on quads) from
-// per-thread factors -- its d/dxi column is constant along the pencil and
-// the other two are linear in xi (6 FMAs per point).
+// GPU mapping
+//  * a TEAM of Q^2 threads (3D) or Q threads (2D) per cell, 256-thread CTAs
+//    holding CPB = 256/team cells; CTAs are PERSISTENT and walk batches of
+//    CPB cells.  While a batch is being computed, the dof indices of the
+//    batch after next and the u values / vertex data of the next batch are
+//    already in flight into registers, and are parked in shared memory at
+//    the end of the iteration -- the indirect gather P_e u overlaps the
+//    arithmetic instead of stalling every CTA at its start.
+//  * every contraction stage gives one thread one 1D pencil: it loads the
+//    inputs along the contraction direction into registers once and emits
+//    a whole output pencil (each shared-memory load feeds Q FMAs); B, D and
+//    Dc are passed by value in the kernel parameter block and enter the
+//    DFMAs as uniform constant-bank operands.
+//  * shared-memory layouts put the CONSUMER's pencil index innermost (reads
+//    are contiguous), and each buffer's outer stride is chosen at compile
+//    time (pick_stride) so the producer's transposed writes are spread over
+//    the 16 eight-byte banks.
+//  * after the x-stage one thread holds all Q points of an x-pencil and
+//    evaluates the flux there: the trilinear Jacobian is recomputed per point
+//    (as kernels.py:136-151 does per qp on quads) from per-thread factors --
+//    its d/dxi column is constant along the pencil and the other two are
+//    linear in xi (6 FMAs per point).
 #pragma once
 #include "common.cuh"
 #include "kern_quad.cuh"
@@ -47,17 +58,78 @@ struct TensorParams {
   double B[Q][P], D[Q][P], Dc[Q][Q], x[Q], w[Q];
 };
 
+// ---- compile-time bank-conflict-aware strides --------------------------------
+// Worst number of distinct 8-byte addresses sharing a bank (addr mod 16) in a
+// half-warp, for lanes enumerating (s fastest over ns values, then r over nr)
+// and address = r * rstep + s * sstep.
+constexpr int bank_degree(int rstep, int sstep, int nr, int ns) {
+  int worst = 0;
+  const int n = nr * ns;
+  for (int h = 0; h < n; h += 16) {
+    int cnt[16] = {0};
+    for (int l = h; l < h + 16 && l < n; ++l) {
+      const int a = (l / ns) * rstep + (l % ns) * sstep;
+      ++cnt[((a % 16) + 16) % 16];
+    }
+    for (int k = 0; k < 16; ++k) worst = cnt[k] > worst ? cnt[k] : worst;
+  }
+  return worst;
+}
+// smallest stride >= lo minimising conflicts when it multiplies r (outer) ...
+constexpr int pick_outer(int lo, int nr, int ns, int sstep) {
+  int best = lo, bd = bank_degree(lo, sstep, nr, ns);
+  for (int st = lo + 1; st < lo + 16; ++st) {
+    const int d = bank_degree(st, sstep, nr, ns);
+    if (d < bd) { bd = d; best = st; }
+  }
+  return best;
+}
+// ... or the lane-fastest index s (inner)
+constexpr int pick_inner(int lo, int nr, int ns, int rstep) {
+  int best = lo, bd = bank_degree(rstep, lo, nr, ns);
+  for (int st = lo + 1; st < lo + 16; ++st) {
+    const int d = bank_degree(rstep, st, nr, ns);
+    if (d < bd) { bd = d; best = st; }
+  }
+  return best;
+}
+constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+
 template <int DIM, int P, int Q, int VS>
-struct TensorSmem {
-  static constexpr int ND = DIM == 3 ? P * P * P : P * P;
+struct TensorLayout {
+  static constexpr int TS = DIM == 3 ? Q * Q : Q;          // threads per cell (team)
+  static constexpr int CPB = 256 / TS;                     // cells per CTA batch
+  static constexpr int ND = DIM == 3 ? P * P * P : P * P;  // scalar dofs per cell
   static constexpr int NV = DIM == 3 ? 8 : 4;
+  static constexpr int RU = (ND + TS - 1) / TS;            // dofs gathered per thread
+  static constexpr int RX = (NV * DIM + TS - 1) / TS;      // vertex coordinates per thread
+  static constexpr int RM = (NV + TS - 1) / TS;            // vertex field values per thread
+  static constexpr bool COLLOC = DIM == 3 && P == Q;
+  // 3D buffers (producer pencil -> consumer pencil):
+  //  Z[j][c][i]  stride SZ: written by (i,j) over c, read by (i,c) over j
+  //  Y[i][c][b]  stride SY: written by (i,c) over b, read by (b,c) over i
+  //  G[a][c][b]  stride Q^2 (collocation: u and flux at the points)
+  //  A[b][c][i]  stride SA: written by (b,c) over i, read by (i,c) over b
+  //  W[c][j][i]  stride SW: written by (i,c) over j, read by (i,j) over c
+  // 2D: Y[b][i], A[b][i], stride S2 = 1 (mod 16)
+  static constexpr int SZ = pick_outer(Q * P, P, P, 1);
+  static constexpr int SY = pick_inner(Q * Q, Q, P, Q);
+  static constexpr int SA = pick_inner(Q * P, Q, Q, P);
+  static constexpr int SW = pick_outer(P * P, Q, P, 1);
+  static constexpr int S2 = P + ((17 - P) % 16 + 16) % 16;
+  static constexpr int NZ = COLLOC ? 1 : 2;
+  static constexpr int NY = COLLOC ? 1 : 3;
+  static constexpr int R1 = DIM == 3 ? cmax3(NZ * P * SZ, 2 * Q * Q * Q, 2 * Q * SW) : 0;
+  static constexpr int R2 = DIM == 3 ? cmax3(NY * P * SY, 3 * Q * SA, 0) : 2 * Q * S2;
+  // per-cell region
   static constexpr int U = 0;
-  static constexpr int Z = U + VS * ND;                          // 3D: 2 x Q P^2
-  static constexpr int Y = Z + (DIM == 3 ? 2 * Q * P * P : 0);    // 3D: 3 x Q^2 P; 2D: 2 x Q P
-  static constexpr int X = Y + (DIM == 3 ? 3 * Q * Q * P : 2 * Q * P);
+  static constexpr int O1 = U + VS * ND;
+  static constexpr int O2 = O1 + R1;
+  static constexpr int X = O2 + R2;
   static constexpr int MU = X + NV * DIM;
   static constexpr int LAM = MU + NV;
-  static constexpr int size = LAM + NV;
+  static constexpr int raw = LAM + NV;
+  static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
 template <int FORM, int DIM, int P, int Q>
@@ -65,465 +137,522 @@ __global__ void __launch_bounds__(256)
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);
-  constexpr int TS = DIM == 3 ? Q * Q : Q;
-  constexpr int CPB = 256 / TS;
-  constexpr bool COLLOC = DIM == 3 && P == Q;
-  using SM = TensorSmem<DIM, P, Q, VS>;
-  constexpr int ND = SM::ND, NV = SM::NV;
-  constexpr int QQQ = Q * Q * Q;
+  using L = TensorLayout<DIM, P, Q, VS>;
+  constexpr int TS = L::TS, CPB = L::CPB, ND = L::ND, NV = L::NV, RU = L::RU;
+  constexpr bool COLLOC = L::COLLOC;
+  constexpr int QQ = Q * Q;
   extern __shared__ double smem_all[];
 
   const int team = threadIdx.x / TS;
   const int t = threadIdx.x % TS;
-  const int cell = p.start + blockIdx.x * CPB + team;
-  const bool active = team < CPB && cell < p.end;
-  double* sm = smem_all + (team < CPB ? team : 0) * SM::size;
-  double* sU = sm + SM::U;
-  double* sZ = sm + SM::Z;
-  double* sY = sm + SM::Y;
-  double* sX = sm + SM::X;
+  const bool in_team = team < CPB;
+  double* sm = smem_all + (in_team ? team : 0) * L::size;
+  double* sU = sm + L::U;
+  double* s1 = sm + L::O1;
+  double* s2 = sm + L::O2;
+  double* sX = sm + L::X;
   const int64_t cs = p.mesh.nc_stride;
+  const int ncell = p.end - p.start;
+  const int nbatch = (ncell + CPB - 1) / CPB;
 
-  // ---- gather u, vertex coordinates, vertex fields --------------------------
-  if (active) {
-    const int32_t* mrow = p.maplex + (int64_t)cell * ND;
-    for (int idx = t; idx < ND; idx += TS) {
-      const int64_t dof = __ldg(mrow + idx);
+  // ---- prefetch pipeline: map indices two batches ahead, data one ahead ----
+  constexpr int RX = L::RX, RM = L::RM;
+  int pf_map[RU];
+  double pf_u[RU][VS];
+  double pf_x[RX], pf_m[RM], pf_l[RM];
+  auto cell_of = [&](int batch) { return p.start + batch * CPB + team; };
+  auto load_map = [&](int batch) {
+    const int c = cell_of(batch);
+    const bool ok = in_team && batch < nbatch && c < p.end;
 #pragma unroll
-      for (int c = 0; c < VS; ++c) sU[c * ND + idx] = __ldg(p.u + VS * dof + c);
+    for (int r = 0; r < RU; ++r) {
+      const int idx = t + r * TS;
+      pf_map[r] = (ok && idx < ND) ? __ldg(p.maplex + (int64_t)c * ND + idx) : -1;
     }
-    for (int v = t; v < NV; v += TS) {
-      const int vid = __ldg(p.mesh.vmap + v * cs + cell);
-      double xv[DIM];
-      load_vertex<DIM>(p.mesh.coords, vid, xv);
+  };
+  auto load_data = [&](int batch) {
+    const int c = cell_of(batch);
+    const bool ok = in_team && batch < nbatch && c < p.end;
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) sX[v * DIM + a] = xv[a];
-      if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
-        sm[SM::MU + v] = __ldg(p.mu + vid);
-        sm[SM::LAM + v] = __ldg(p.lam + vid);
+    for (int r = 0; r < RU; ++r)
+#pragma unroll
+      for (int k = 0; k < VS; ++k)
+        pf_u[r][k] = pf_map[r] >= 0 ? __ldg(p.u + (int64_t)VS * pf_map[r] + k) : 0.0;
+#pragma unroll
+    for (int r = 0; r < RX; ++r) {
+      const int e = t + r * TS;
+      pf_x[r] = 0.0;
+      if (ok && e < NV * DIM) {
+        const int vid = __ldg(p.mesh.vmap + (e / DIM) * cs + c);
+        pf_x[r] = __ldg(p.mesh.coords + (int64_t)vid * CStride<DIM>::value + e % DIM);
       }
     }
-  }
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const int v = t + r * TS;
+        pf_m[r] = pf_l[r] = 0.0;
+        if (ok && v < NV) {
+          const int vid = __ldg(p.mesh.vmap + v * cs + c);
+          pf_m[r] = __ldg(p.mu + vid);
+          pf_l[r] = __ldg(p.lam + vid);
+        }
+      }
+    }
+  };
+  auto park = [&]() {  // prefetched registers -> this team's shared memory
+    if (!in_team) return;
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      const int idx = t + r * TS;
+      if (idx < ND)
+#pragma unroll
+        for (int k = 0; k < VS; ++k) sU[k * ND + idx] = pf_u[r][k];
+    }
+#pragma unroll
+    for (int r = 0; r < RX; ++r)
+      if (t + r * TS < NV * DIM) sX[t + r * TS] = pf_x[r];
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+#pragma unroll
+      for (int r = 0; r < RM; ++r)
+        if (t + r * TS < NV) {
+          sm[L::MU + t + r * TS] = pf_m[r];
+          sm[L::LAM + t + r * TS] = pf_l[r];
+        }
+    }
+  };
+
+  int batch = blockIdx.x;
+  load_map(batch);
+  load_data(batch);
+  park();
+  load_map(batch + gridDim.x);
   __syncthreads();
 
-  // ---- forward: reference gradients at the points of this thread's x-pencil
-  // thread (b, c) = (t % Q, t / Q) in 3D, b = t in 2D
-  double g[VS][DIM][Q];
+  for (; batch < nbatch; batch += gridDim.x) {
+    const int cell = cell_of(batch);
+    const bool active = in_team && cell < p.end;
+    // issue the next batch's gathers now; they land while this batch computes
+    load_data(batch + gridDim.x);
+    load_map(batch + 2 * gridDim.x);
+
+    // ---- forward: reference gradients at the points of this thread's x-pencil
+    double g[VS][DIM][Q];
 #pragma unroll
-  for (int comp = 0; comp < VS; ++comp) {
-    const double* uc = sU + comp * ND;
-    if constexpr (DIM == 3) {
-      // z: pencil (i, j) over k -> Z0 = B u (and Z1 = D u, direct only)
-      if (active && t < P * P) {
-        const int i = t % P, j = t / P;
-        double pen[P];
+    for (int comp = 0; comp < VS; ++comp) {
+      const double* uc = sU + comp * ND;
+      if constexpr (DIM == 3) {
+        // z: pencil (i, j) over k -> Z0 = B u (Z1 = D u: direct)      Z[j][c][i]
+        if (active && t < P * P) {
+          const int i = t % P, j = t / P;
+          double pen[P];
 #pragma unroll
-        for (int k = 0; k < P; ++k) pen[k] = uc[(k * P + j) * P + i];
+          for (int k = 0; k < P; ++k) pen[k] = uc[k * P * P + t];
 #pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double z0 = 0.0, z1 = 0.0;
+          for (int c = 0; c < Q; ++c) {
+            double z0 = 0.0, z1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < P; ++k) {
-            z0 = fma(p.B[c][k], pen[k], z0);
-            if constexpr (!COLLOC) z1 = fma(p.D[c][k], pen[k], z1);
+            for (int k = 0; k < P; ++k) {
+              z0 = fma(p.B[c][k], pen[k], z0);
+              if constexpr (!COLLOC) z1 = fma(p.D[c][k], pen[k], z1);
+            }
+            s1[j * L::SZ + c * P + i] = z0;
+            if constexpr (!COLLOC) s1[P * L::SZ + j * L::SZ + c * P + i] = z1;
           }
-          sZ[(c * P + j) * P + i] = z0;
-          if constexpr (!COLLOC) sZ[Q * P * P + (c * P + j) * P + i] = z1;
         }
-      }
-      __syncthreads();
-      // y: pencil (i, c) over j -> Y0 = B Z0 (Y1 = D Z0, Y2 = B Z1: direct)
-      if (active && t < Q * P) {
-        const int i = t % P, c = t / P;
-        double p0[P], p1[P];
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          p0[j] = sZ[(c * P + j) * P + i];
-          if constexpr (!COLLOC) p1[j] = sZ[Q * P * P + (c * P + j) * P + i];
-        }
-#pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+        __syncthreads();
+        // y: pencil (i, c) over j -> Y0 = B Z0 (Y1 = D Z0, Y2 = B Z1)    Y[i][c][b]
+        if (active && t < Q * P) {
+          const int i = t % P, c = t / P;
+          double p0[P], p1[P];
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            y0 = fma(p.B[b][j], p0[j], y0);
+            p0[j] = s1[j * L::SZ + t];
+            if constexpr (!COLLOC) p1[j] = s1[P * L::SZ + j * L::SZ + t];
+          }
+#pragma unroll
+          for (int b = 0; b < Q; ++b) {
+            double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+              y0 = fma(p.B[b][j], p0[j], y0);
+              if constexpr (!COLLOC) {
+                y1 = fma(p.D[b][j], p0[j], y1);
+                y2 = fma(p.B[b][j], p1[j], y2);
+              }
+            }
+            s2[i * L::SY + c * Q + b] = y0;
             if constexpr (!COLLOC) {
-              y1 = fma(p.D[b][j], p0[j], y1);
-              y2 = fma(p.B[b][j], p1[j], y2);
+              s2[P * L::SY + i * L::SY + c * Q + b] = y1;
+              s2[2 * P * L::SY + i * L::SY + c * Q + b] = y2;
             }
-          }
-          sY[(c * Q + b) * P + i] = y0;
-          if constexpr (!COLLOC) {
-            sY[Q * Q * P + (c * Q + b) * P + i] = y1;
-            sY[2 * Q * Q * P + (c * Q + b) * P + i] = y2;
-          }
-        }
-      }
-      __syncthreads();
-      if constexpr (COLLOC) {
-        // x: pencil (b, c) over i -> u at the Gauss points; d/dxi locally
-        if (active) {
-          const int b = t % Q, c = t / Q;
-          double q0[P], uq[Q];
-#pragma unroll
-          for (int i = 0; i < P; ++i) q0[i] = sY[(c * Q + b) * P + i];
-#pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            double s = 0.0;
-#pragma unroll
-            for (int i = 0; i < P; ++i) s = fma(p.B[a][i], q0[i], s);
-            uq[a] = s;
-            sZ[(c * Q + b) * Q + a] = s;
-          }
-#pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            double s = 0.0;
-#pragma unroll
-            for (int e = 0; e < Q; ++e) s = fma(p.Dc[a][e], uq[e], s);
-            g[comp][0][a] = s;
           }
         }
         __syncthreads();
-        // d/deta, d/dzeta with Dc across the pencils of the team
-        if (active) {
-          const int b = t % Q, c = t / Q;
+        if constexpr (COLLOC) {
+          // x: pencil (b, c) over i -> u at the points; d/dxi locally      G[a][c][b]
+          if (active) {
+            const int b = t % Q, c = t / Q;
+            double q0[P], uq[Q];
 #pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            double s1 = 0.0, s2 = 0.0;
+            for (int i = 0; i < P; ++i) q0[i] = s2[i * L::SY + t];
 #pragma unroll
-            for (int e = 0; e < Q; ++e) {
-              s1 = fma(p.Dc[b][e], sZ[(c * Q + e) * Q + a], s1);
-              s2 = fma(p.Dc[c][e], sZ[(e * Q + b) * Q + a], s2);
+            for (int a = 0; a < Q; ++a) {
+              double s = 0.0;
+#pragma unroll
+              for (int i = 0; i < P; ++i) s = fma(p.B[a][i], q0[i], s);
+              uq[a] = s;
+              s1[a * QQ + t] = s;
             }
-            g[comp][1][a] = s1;
-            g[comp][2][a] = s2;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+              double s = 0.0;
+#pragma unroll
+              for (int e = 0; e < Q; ++e) s = fma(p.Dc[a][e], uq[e], s);
+              g[comp][0][a] = s;
+            }
+            (void)b;
+            (void)c;
           }
+          __syncthreads();
+          // d/deta, d/dzeta with Dc across the pencils of the team
+          if (active) {
+            const int b = t % Q, c = t / Q;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+              double sa = 0.0, sb = 0.0;
+#pragma unroll
+              for (int e = 0; e < Q; ++e) {
+                sa = fma(p.Dc[b][e], s1[a * QQ + c * Q + e], sa);
+                sb = fma(p.Dc[c][e], s1[a * QQ + e * Q + b], sb);
+              }
+              g[comp][1][a] = sa;
+              g[comp][2][a] = sb;
+            }
+          }
+          __syncthreads();
+        } else {
+          // x: pencil (b, c) over i -> d/dxi = D Y0, d/deta = B Y1, d/dzeta = B Y2
+          if (active) {
+            double q0[P], q1[P], q2[P];
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              q0[i] = s2[i * L::SY + t];
+              q1[i] = s2[P * L::SY + i * L::SY + t];
+              q2[i] = s2[2 * P * L::SY + i * L::SY + t];
+            }
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+              double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+#pragma unroll
+              for (int i = 0; i < P; ++i) {
+                g0 = fma(p.D[a][i], q0[i], g0);
+                g1 = fma(p.B[a][i], q1[i], g1);
+                g2 = fma(p.B[a][i], q2[i], g2);
+              }
+              g[comp][0][a] = g0;
+              g[comp][1][a] = g1;
+              g[comp][2][a] = g2;
+            }
+          }
+          __syncthreads();
         }
-        __syncthreads();
       } else {
-        // x: pencil (b, c) over i -> d/dxi = D Y0, d/deta = B Y1, d/dzeta = B Y2
+        // y: pencil i over j -> Y0 = B u, Y1 = D u                         Y[b][i]
+        if (active && t < P) {
+          const int i = t;
+          double pen[P];
+#pragma unroll
+          for (int j = 0; j < P; ++j) pen[j] = uc[j * P + i];
+#pragma unroll
+          for (int b = 0; b < Q; ++b) {
+            double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+              y0 = fma(p.B[b][j], pen[j], y0);
+              y1 = fma(p.D[b][j], pen[j], y1);
+            }
+            s2[b * L::S2 + i] = y0;
+            s2[Q * L::S2 + b * L::S2 + i] = y1;
+          }
+        }
+        __syncthreads();
         if (active) {
-          const int b = t % Q, c = t / Q;
-          double q0[P], q1[P], q2[P];
+          const int b = t;
+          double q0[P], q1[P];
 #pragma unroll
           for (int i = 0; i < P; ++i) {
-            q0[i] = sY[(c * Q + b) * P + i];
-            q1[i] = sY[Q * Q * P + (c * Q + b) * P + i];
-            q2[i] = sY[2 * Q * Q * P + (c * Q + b) * P + i];
+            q0[i] = s2[b * L::S2 + i];
+            q1[i] = s2[Q * L::S2 + b * L::S2 + i];
           }
 #pragma unroll
           for (int a = 0; a < Q; ++a) {
-            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+            double g0 = 0.0, g1 = 0.0;
 #pragma unroll
             for (int i = 0; i < P; ++i) {
               g0 = fma(p.D[a][i], q0[i], g0);
               g1 = fma(p.B[a][i], q1[i], g1);
-              g2 = fma(p.B[a][i], q2[i], g2);
             }
             g[comp][0][a] = g0;
             g[comp][1][a] = g1;
-            g[comp][2][a] = g2;
           }
         }
         __syncthreads();
       }
-    } else {
-      // y: pencil i over j -> Y0 = B u, Y1 = D u
-      if (active && t < P) {
-        const int i = t;
-        double pen[P];
-#pragma unroll
-        for (int j = 0; j < P; ++j) pen[j] = uc[j * P + i];
-#pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-          for (int j = 0; j < P; ++j) {
-            y0 = fma(p.B[b][j], pen[j], y0);
-            y1 = fma(p.D[b][j], pen[j], y1);
-          }
-          sY[b * P + i] = y0;
-          sY[Q * P + b * P + i] = y1;
-        }
-      }
-      __syncthreads();
-      if (active) {
-        const int b = t;
-        double q0[P], q1[P];
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          q0[i] = sY[b * P + i];
-          q1[i] = sY[Q * P + b * P + i];
-        }
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-          double g0 = 0.0, g1 = 0.0;
-#pragma unroll
-          for (int i = 0; i < P; ++i) {
-            g0 = fma(p.D[a][i], q0[i], g0);
-            g1 = fma(p.B[a][i], q1[i], g1);
-          }
-          g[comp][0][a] = g0;
-          g[comp][1][a] = g1;
-        }
-      }
-      __syncthreads();
     }
-  }
 
-  // ---- pointwise flux at the Q points of the x-pencil ----------------------
-  if (active) {
-    const int b = t % Q, c = DIM == 3 ? t / Q : 0;
-    const double eta = p.x[b], zeta = DIM == 3 ? p.x[c] : 0.0;
-    const double wbc = DIM == 3 ? p.w[b] * p.w[c] : p.w[b];
-    const double Ly[2] = {1.0 - eta, eta}, Lz[2] = {1.0 - zeta, zeta};
-    auto Xv = [&](int vx, int vy, int vz, int d) { return sX[(vx + 2 * vy + 4 * vz) * DIM + d]; };
-    // J(:, 0) constant along the pencil; J(:, e>0) = J0e + xi * dJe
-    double c0[DIM], j1[DIM], d1[DIM], j2[DIM], d2[DIM];
-    double m0 = 0.0, dm = 0.0, l0 = 0.0, dl = 0.0;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      if constexpr (DIM == 3) {
-        double s = 0.0;
-#pragma unroll
-        for (int vy = 0; vy < 2; ++vy)
-#pragma unroll
-          for (int vz = 0; vz < 2; ++vz) s += (Xv(1, vy, vz, d) - Xv(0, vy, vz, d)) * (Ly[vy] * Lz[vz]);
-        c0[d] = s;
-        double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0;
-#pragma unroll
-        for (int o = 0; o < 2; ++o) {
-          e0 += (Xv(0, 1, o, d) - Xv(0, 0, o, d)) * Lz[o];
-          e1 += (Xv(1, 1, o, d) - Xv(1, 0, o, d)) * Lz[o];
-          f0 += (Xv(0, o, 1, d) - Xv(0, o, 0, d)) * Ly[o];
-          f1 += (Xv(1, o, 1, d) - Xv(1, o, 0, d)) * Ly[o];
-        }
-        j1[d] = e0; d1[d] = e1 - e0;
-        j2[d] = f0; d2[d] = f1 - f0;
-      } else {
-        c0[d] = (Xv(1, 0, 0, d) - Xv(0, 0, 0, d)) * Ly[0] + (Xv(1, 1, 0, d) - Xv(0, 1, 0, d)) * Ly[1];
-        const double e0 = Xv(0, 1, 0, d) - Xv(0, 0, 0, d), e1 = Xv(1, 1, 0, d) - Xv(1, 0, 0, d);
-        j1[d] = e0; d1[d] = e1 - e0;
-      }
-    }
-    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
-      double mx[2] = {0.0, 0.0}, lx[2] = {0.0, 0.0};
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
-        const double wgt = DIM == 3 ? Ly[vy] * Lz[vz] : Ly[vy];
-        mx[vx] += wgt * sm[SM::MU + v];
-        lx[vx] += wgt * sm[SM::LAM + v];
-      }
-      m0 = mx[0]; dm = mx[1] - mx[0];
-      l0 = lx[0]; dl = lx[1] - lx[0];
-    }
-#pragma unroll
-    for (int a = 0; a < Q; ++a) {
-      const double xi = p.x[a];
-      double J[DIM][DIM], Ji[DIM][DIM];
+    // ---- pointwise flux at the Q points of the x-pencil --------------------
+    if (active) {
+      const int b = t % Q, c = DIM == 3 ? t / Q : 0;
+      const double eta = p.x[b], zeta = DIM == 3 ? p.x[c] : 0.0;
+      const double wbc = DIM == 3 ? p.w[b] * p.w[c] : p.w[b];
+      const double Ly[2] = {1.0 - eta, eta}, Lz[2] = {1.0 - zeta, zeta};
+      auto Xv = [&](int vx, int vy, int vz, int d) { return sX[(vx + 2 * vy + 4 * vz) * DIM + d]; };
+      // J(:, 0) constant along the pencil; J(:, e>0) = J0e + xi * dJe
+      double c0[DIM], j1[DIM], d1[DIM], j2[DIM], d2[DIM];
+      double m0 = 0.0, dm = 0.0, l0 = 0.0, dl = 0.0;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        J[d][0] = c0[d];
-        J[d][1] = fma(xi, d1[d], j1[d]);
-        if constexpr (DIM == 3) J[d][2] = fma(xi, d2[d], j2[d]);
+        if constexpr (DIM == 3) {
+          double s = 0.0;
+#pragma unroll
+          for (int vy = 0; vy < 2; ++vy)
+#pragma unroll
+            for (int vz = 0; vz < 2; ++vz) s += (Xv(1, vy, vz, d) - Xv(0, vy, vz, d)) * (Ly[vy] * Lz[vz]);
+          c0[d] = s;
+          double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            e0 += (Xv(0, 1, o, d) - Xv(0, 0, o, d)) * Lz[o];
+            e1 += (Xv(1, 1, o, d) - Xv(1, 0, o, d)) * Lz[o];
+            f0 += (Xv(0, o, 1, d) - Xv(0, o, 0, d)) * Ly[o];
+            f1 += (Xv(1, o, 1, d) - Xv(1, o, 0, d)) * Ly[o];
+          }
+          j1[d] = e0; d1[d] = e1 - e0;
+          j2[d] = f0; d2[d] = f1 - f0;
+        } else {
+          c0[d] = (Xv(1, 0, 0, d) - Xv(0, 0, 0, d)) * Ly[0] + (Xv(1, 1, 0, d) - Xv(0, 1, 0, d)) * Ly[1];
+          const double e0 = Xv(0, 1, 0, d) - Xv(0, 0, 0, d), e1 = Xv(1, 1, 0, d) - Xv(1, 0, 0, d);
+          j1[d] = e0; d1[d] = e1 - e0;
+        }
       }
-      const double det = det_inv<DIM>(J, Ji);
-      const double tw = (p.w[a] * wbc) * fabs(det);
-      double mu = p.p0, lam = p.p1;
       if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
-        mu = fma(xi, dm, m0);
-        lam = fma(xi, dl, l0);
+        double mx[2] = {0.0, 0.0}, lx[2] = {0.0, 0.0};
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
+          const double wgt = DIM == 3 ? Ly[vy] * Lz[vz] : Ly[vy];
+          mx[vx] += wgt * sm[L::MU + v];
+          lx[vx] += wgt * sm[L::LAM + v];
+        }
+        m0 = mx[0]; dm = mx[1] - mx[0];
+        l0 = lx[0]; dl = lx[1] - lx[0];
       }
-      double gq[VS][DIM], uq[VS], cv[VS], cg[VS][DIM];
 #pragma unroll
-      for (int comp = 0; comp < VS; ++comp) {
-        uq[comp] = 0.0;
+      for (int a = 0; a < Q; ++a) {
+        const double xi = p.x[a];
+        double J[DIM][DIM], Ji[DIM][DIM];
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) gq[comp][d] = g[comp][d][a];
+        for (int d = 0; d < DIM; ++d) {
+          J[d][0] = c0[d];
+          J[d][1] = fma(xi, d1[d], j1[d]);
+          if constexpr (DIM == 3) J[d][2] = fma(xi, d2[d], j2[d]);
+        }
+        const double det = det_inv<DIM>(J, Ji);
+        const double tw = (p.w[a] * wbc) * fabs(det);
+        double mu = p.p0, lam = p.p1;
+        if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+          mu = fma(xi, dm, m0);
+          lam = fma(xi, dl, l0);
+        }
+        double gq[VS][DIM], uq[VS], cv[VS], cg[VS][DIM];
+#pragma unroll
+        for (int comp = 0; comp < VS; ++comp) {
+          uq[comp] = 0.0;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) gq[comp][d] = g[comp][d][a];
+        }
+        pointwise<FORM, DIM, VS>(Ji, tw, uq, gq, mu, lam, cv, cg);
+#pragma unroll
+        for (int comp = 0; comp < VS; ++comp)
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) g[comp][d][a] = cg[comp][d];
       }
-      pointwise<FORM, DIM, VS>(Ji, tw, uq, gq, mu, lam, cv, cg);
-#pragma unroll
-      for (int comp = 0; comp < VS; ++comp)
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) g[comp][d][a] = cg[comp][d];
     }
-  }
 
-  // ---- transposed chain and scatter, one component at a time --------------
+    // ---- transposed chain and scatter, one component at a time ------------
+    const int32_t* mrow = p.maplex + (int64_t)cell * ND;
 #pragma unroll
-  for (int comp = 0; comp < VS; ++comp) {
-    if constexpr (DIM == 3) {
-      if constexpr (COLLOC) {
-        // Dc^T in eta/zeta needs the team's pencils: stage F1, F2
-        if (active) {
-          const int b = t % Q, c = t / Q;
+    for (int comp = 0; comp < VS; ++comp) {
+      if constexpr (DIM == 3) {
+        if constexpr (COLLOC) {
+          // Dc^T in eta/zeta needs the team's pencils: stage F1, F2     G[a][c][b]
+          if (active) {
 #pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            sZ[(c * Q + b) * Q + a] = g[comp][1][a];
-            sZ[QQQ + (c * Q + b) * Q + a] = g[comp][2][a];
-          }
-        }
-        __syncthreads();
-        // V = Dc^T F0 (local) + Dc^T F1 (eta) + Dc^T F2 (zeta); x^T: A = B^T V
-        if (active) {
-          const int b = t % Q, c = t / Q;
-          double V[Q];
-#pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            double s = 0.0;
-#pragma unroll
-            for (int e = 0; e < Q; ++e) {
-              s = fma(p.Dc[e][a], g[comp][0][e], s);
-              s = fma(p.Dc[e][b], sZ[(c * Q + e) * Q + a], s);
-              s = fma(p.Dc[e][c], sZ[QQQ + (e * Q + b) * Q + a], s);
+            for (int a = 0; a < Q; ++a) {
+              s1[a * QQ + t] = g[comp][1][a];
+              s1[Q * QQ + a * QQ + t] = g[comp][2][a];
             }
-            V[a] = s;
           }
+          __syncthreads();
+          // V = Dc^T F0 (local) + Dc^T F1 (eta) + Dc^T F2 (zeta); x^T: A = B^T V
+          if (active) {
+            const int b = t % Q, c = t / Q;
+            double V[Q];
 #pragma unroll
-          for (int i = 0; i < P; ++i) {
-            double s = 0.0;
+            for (int a = 0; a < Q; ++a) {
+              double s = 0.0;
 #pragma unroll
-            for (int a = 0; a < Q; ++a) s = fma(p.B[a][i], V[a], s);
-            sY[(c * Q + b) * P + i] = s;
+              for (int e = 0; e < Q; ++e) {
+                s = fma(p.Dc[e][a], g[comp][0][e], s);
+                s = fma(p.Dc[e][b], s1[a * QQ + c * Q + e], s);
+                s = fma(p.Dc[e][c], s1[Q * QQ + a * QQ + e * Q + b], s);
+              }
+              V[a] = s;
+            }
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              double s = 0.0;
+#pragma unroll
+              for (int a = 0; a < Q; ++a) s = fma(p.B[a][i], V[a], s);
+              s2[b * L::SA + c * P + i] = s;                            // A[b][c][i]
+            }
           }
+          __syncthreads();
+          // y^T: pencil (i, c) over b: W = B^T A                           W[c][j][i]
+          if (active && t < Q * P) {
+            const int i = t % P, c = t / P;
+            double a0[Q];
+#pragma unroll
+            for (int b = 0; b < Q; ++b) a0[b] = s2[b * L::SA + t];
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+              double s = 0.0;
+#pragma unroll
+              for (int b = 0; b < Q; ++b) s = fma(p.B[b][j], a0[b], s);
+              s1[c * L::SW + j * P + i] = s;
+            }
+          }
+          __syncthreads();
+          // z^T: pencil (i, j) over c: y_k = B^T W; scatter
+          if (active && t < P * P) {
+            double w1[Q];
+#pragma unroll
+            for (int c = 0; c < Q; ++c) w1[c] = s1[c * L::SW + t];
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int c = 0; c < Q; ++c) s = fma(p.B[c][k], w1[c], s);
+              scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
+            }
+          }
+          __syncthreads();
+        } else {
+          // x^T: thread (b, c): A0 = D^T F0, A1 = B^T F1, A2 = B^T F2 over i  A[b][c][i]
+          if (active) {
+            const int b = t % Q, c = t / Q;
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+              for (int a = 0; a < Q; ++a) {
+                a0 = fma(p.D[a][i], g[comp][0][a], a0);
+                a1 = fma(p.B[a][i], g[comp][1][a], a1);
+                a2 = fma(p.B[a][i], g[comp][2][a], a2);
+              }
+              s2[b * L::SA + c * P + i] = a0;
+              s2[Q * L::SA + b * L::SA + c * P + i] = a1;
+              s2[2 * Q * L::SA + b * L::SA + c * P + i] = a2;
+            }
+          }
+          __syncthreads();
+          // y^T: pencil (i, c) over b: W1 = B^T A0 + D^T A1, W2 = B^T A2    W[c][j][i]
+          if (active && t < Q * P) {
+            const int i = t % P, c = t / P;
+            double a0[Q], a1[Q], a2[Q];
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+              a0[b] = s2[b * L::SA + t];
+              a1[b] = s2[Q * L::SA + b * L::SA + t];
+              a2[b] = s2[2 * Q * L::SA + b * L::SA + t];
+            }
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+              double w1 = 0.0, w2 = 0.0;
+#pragma unroll
+              for (int b = 0; b < Q; ++b) {
+                w1 = fma(p.B[b][j], a0[b], w1);
+                w1 = fma(p.D[b][j], a1[b], w1);
+                w2 = fma(p.B[b][j], a2[b], w2);
+              }
+              s1[c * L::SW + j * P + i] = w1;
+              s1[Q * L::SW + c * L::SW + j * P + i] = w2;
+            }
+          }
+          __syncthreads();
+          // z^T: pencil (i, j) over c: y_k = B^T W1 + D^T W2; scatter
+          if (active && t < P * P) {
+            double w1[Q], w2[Q];
+#pragma unroll
+            for (int c = 0; c < Q; ++c) {
+              w1[c] = s1[c * L::SW + t];
+              w2[c] = s1[Q * L::SW + c * L::SW + t];
+            }
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+              double s = 0.0;
+#pragma unroll
+              for (int c = 0; c < Q; ++c) {
+                s = fma(p.B[c][k], w1[c], s);
+                s = fma(p.D[c][k], w2[c], s);
+              }
+              scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
+            }
+          }
+          __syncthreads();
         }
-        __syncthreads();
-        // y^T: pencil (i, c) over b: W = B^T A
-        if (active && t < Q * P) {
-          const int i = t % P, c = t / P;
-          double a0[Q];
-#pragma unroll
-          for (int b = 0; b < Q; ++b) a0[b] = sY[(c * Q + b) * P + i];
-#pragma unroll
-          for (int j = 0; j < P; ++j) {
-            double s = 0.0;
-#pragma unroll
-            for (int b = 0; b < Q; ++b) s = fma(p.B[b][j], a0[b], s);
-            sZ[(c * P + j) * P + i] = s;
-          }
-        }
-        __syncthreads();
-        // z^T: pencil (i, j) over c: y_k = B^T W; scatter
-        if (active && t < P * P) {
-          const int i = t % P, j = t / P;
-          double w1[Q];
-#pragma unroll
-          for (int c = 0; c < Q; ++c) w1[c] = sZ[(c * P + j) * P + i];
-          const int32_t* mrow = p.maplex + (int64_t)cell * ND;
-#pragma unroll
-          for (int k = 0; k < P; ++k) {
-            double s = 0.0;
-#pragma unroll
-            for (int c = 0; c < Q; ++c) s = fma(p.B[c][k], w1[c], s);
-            scatter_add(p.y, (int64_t)VS * __ldg(mrow + (k * P + j) * P + i) + comp, s);
-          }
-        }
-        __syncthreads();
       } else {
-        // x^T: thread (b, c): A0 = D^T F0, A1 = B^T F1, A2 = B^T F2 over i
         if (active) {
-          const int b = t % Q, c = t / Q;
+          const int b = t;
 #pragma unroll
           for (int i = 0; i < P; ++i) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+            double a0 = 0.0, a1 = 0.0;
 #pragma unroll
             for (int a = 0; a < Q; ++a) {
               a0 = fma(p.D[a][i], g[comp][0][a], a0);
               a1 = fma(p.B[a][i], g[comp][1][a], a1);
-              a2 = fma(p.B[a][i], g[comp][2][a], a2);
             }
-            sY[(c * Q + b) * P + i] = a0;
-            sY[Q * Q * P + (c * Q + b) * P + i] = a1;
-            sY[2 * Q * Q * P + (c * Q + b) * P + i] = a2;
+            s2[b * L::S2 + i] = a0;
+            s2[Q * L::S2 + b * L::S2 + i] = a1;
           }
         }
         __syncthreads();
-        // y^T: pencil (i, c) over b: W1 = B^T A0 + D^T A1, W2 = B^T A2
-        if (active && t < Q * P) {
-          const int i = t % P, c = t / P;
-          double a0[Q], a1[Q], a2[Q];
+        if (active && t < P) {
+          const int i = t;
+          double a0[Q], a1[Q];
 #pragma unroll
           for (int b = 0; b < Q; ++b) {
-            a0[b] = sY[(c * Q + b) * P + i];
-            a1[b] = sY[Q * Q * P + (c * Q + b) * P + i];
-            a2[b] = sY[2 * Q * Q * P + (c * Q + b) * P + i];
+            a0[b] = s2[b * L::S2 + i];
+            a1[b] = s2[Q * L::S2 + b * L::S2 + i];
           }
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            double w1 = 0.0, w2 = 0.0;
-#pragma unroll
-            for (int b = 0; b < Q; ++b) {
-              w1 = fma(p.B[b][j], a0[b], w1);
-              w1 = fma(p.D[b][j], a1[b], w1);
-              w2 = fma(p.B[b][j], a2[b], w2);
-            }
-            sZ[(c * P + j) * P + i] = w1;
-            sZ[Q * P * P + (c * P + j) * P + i] = w2;
-          }
-        }
-        __syncthreads();
-        // z^T: pencil (i, j) over c: y_k = B^T W1 + D^T W2; scatter
-        if (active && t < P * P) {
-          const int i = t % P, j = t / P;
-          double w1[Q], w2[Q];
-#pragma unroll
-          for (int c = 0; c < Q; ++c) {
-            w1[c] = sZ[(c * P + j) * P + i];
-            w2[c] = sZ[Q * P * P + (c * P + j) * P + i];
-          }
-          const int32_t* mrow = p.maplex + (int64_t)cell * ND;
-#pragma unroll
-          for (int k = 0; k < P; ++k) {
             double s = 0.0;
 #pragma unroll
-            for (int c = 0; c < Q; ++c) {
-              s = fma(p.B[c][k], w1[c], s);
-              s = fma(p.D[c][k], w2[c], s);
+            for (int b = 0; b < Q; ++b) {
+              s = fma(p.B[b][j], a0[b], s);
+              s = fma(p.D[b][j], a1[b], s);
             }
-            scatter_add(p.y, (int64_t)VS * __ldg(mrow + (k * P + j) * P + i) + comp, s);
+            scatter_add(p.y, (int64_t)VS * __ldg(mrow + j * P + i) + comp, s);
           }
         }
         __syncthreads();
       }
-    } else {
-      if (active) {
-        const int b = t;
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-          for (int a = 0; a < Q; ++a) {
-            a0 = fma(p.D[a][i], g[comp][0][a], a0);
-            a1 = fma(p.B[a][i], g[comp][1][a], a1);
-          }
-          sY[b * P + i] = a0;
-          sY[Q * P + b * P + i] = a1;
-        }
-      }
-      __syncthreads();
-      if (active && t < P) {
-        const int i = t;
-        double a0[Q], a1[Q];
-#pragma unroll
-        for (int b = 0; b < Q; ++b) {
-          a0[b] = sY[b * P + i];
-          a1[b] = sY[Q * P + b * P + i];
-        }
-        const int32_t* mrow = p.maplex + (int64_t)cell * ND;
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < Q; ++b) {
-            s = fma(p.B[b][j], a0[b], s);
-            s = fma(p.D[b][j], a1[b], s);
-          }
-          scatter_add(p.y, (int64_t)VS * __ldg(mrow + j * P + i) + comp, s);
-        }
-      }
-      __syncthreads();
     }
+    // the next batch's data (loads issued at the top of this iteration)
+    park();
+    __syncthreads();
   }
 }
 

@@ -307,7 +307,7 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 template <int FORM, int DIM, int P, int Q>
 int tensor_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
-  using SM = TensorSmem<DIM, P, Q, form_vs(FORM, DIM)>;
+  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM)>;
   static_assert(sizeof(TP) <= 32000, "parameter block too large");
   if (p->q1d != Q || p->degree + 1 != P) return fail(FE_EINVAL, "tensor factors do not match the kernel");
   TP* hp = new TP();
@@ -341,12 +341,17 @@ int tensor_prepare(fe_plan* p) {
   }
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
-  constexpr int TS = DIM == 3 ? Q * Q : Q;
-  constexpr int CPB = 256 / TS;
+  constexpr int CPB = SM::CPB;
   p->tables_bytes = (size_t)CPB * SM::size * sizeof(double);
   CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
   p->cells_per_block = CPB;
+  int dev = 0, sms = 0, per_sm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q>, 256,
+                                                         p->tables_bytes));
+  p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
   return FE_OK;
 }
 
@@ -368,7 +373,9 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   hp->p1 = p->params[1];
   const int n = end - start;
   const int cpb = p->cells_per_block;
-  tensor_kernel<FORM, DIM, P, Q><<<(n + cpb - 1) / cpb, 256, p->tables_bytes, s>>>(*hp);
+  const int nbatch = (n + cpb - 1) / cpb;
+  const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
+  tensor_kernel<FORM, DIM, P, Q><<<grid, 256, p->tables_bytes, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
