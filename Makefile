@@ -2,12 +2,16 @@
 # with the repo snapshot) and the oracle's C restatement.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -shared --expt-relaxed-constexpr -lgomp
 PKG := paper_1903_08243_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
 HDR := $(wildcard $(PKG)/csrc/*.cuh) include/fe_b200.h
 
 all: $(PKG)/libfeb200.so oracle/liboracle.so
+
+# experiment build: make variant V=minb2 FLAGS=-DFE_TENSOR_MINB=2
+variant: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) $(FLAGS) -o $(PKG)/libfeb200_$(V).so $(SRC)
 
 oracle: oracle/liboracle.so
 
@@ -22,4 +26,4 @@ $(PKG)/libfeb200.so: $(SRC) $(HDR)
 clean:
 	rm -f $(PKG)/libfeb200.so oracle/liboracle.so
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle variant

@@ -12,7 +12,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfeb200.so")
+LIB_PATH = os.environ.get("FE_LIB_PATH") or os.path.join(HERE, "libfeb200.so")
 
 FORMS = {
     "mass": 0, "helmholtz": 1, "laplacian": 2, "elasticity": 3,

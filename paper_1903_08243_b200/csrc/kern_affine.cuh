@@ -101,4 +101,83 @@ affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Patch-aggregated variant (low degree: C1, C2-P1/P2).  At these intensities
+// the global FP64 RED stream (one per cell-dof pair: 6.3M for P1, 15.7M for
+// P2) rivals the arithmetic.  The plan groups each CTA's 128 consecutive
+// cells into a PATCH with a sorted list of its distinct dofs and a uint16
+// patch-local index per cell-dof (built once at bind time): the CTA stages
+// u of the patch in shared memory (one coalesced-ish read per distinct dof),
+// accumulates the element vectors into a shared-memory patch vector, and
+// flushes one global RED per distinct dof (3-6x fewer).
+// ---------------------------------------------------------------------------
+
+struct PatchView {
+  const int32_t* __restrict__ off;    // [npatch + 1]
+  const int32_t* __restrict__ dofs;   // [off[npatch]] sorted distinct dofs per patch
+  const uint16_t* __restrict__ pidx;  // SoA [nd][nc_stride] patch-local index of each cell dof
+};
+
+constexpr int kPatchCells = 128;
+
+template <int NM, int ND>
+struct ETPatchParams {
+  MeshView mesh;
+  PatchView patch;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  int32_t start, end;
+  double S[NM][ND][ND];
+};
+
+template <int FORM, int DIM, int ND>
+__global__ void __launch_bounds__(kPatchCells)
+affine_et_patch_kernel(const __grid_constant__ ETPatchParams<et_nmats<FORM, DIM>(), ND> p) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  constexpr int NV = DIM + 1;
+  extern __shared__ double sp[];
+  const int blk = p.start / kPatchCells + blockIdx.x;
+  const int off = __ldg(p.patch.off + blk);
+  const int nu = __ldg(p.patch.off + blk + 1) - off;
+  double* su = sp;
+  double* sacc = sp + nu;
+  for (int k = threadIdx.x; k < nu; k += kPatchCells) {
+    su[k] = __ldg(p.u + __ldg(p.patch.dofs + off + k));
+    sacc[k] = 0.0;
+  }
+  __syncthreads();
+  const int cell = blk * kPatchCells + threadIdx.x;
+  if (cell >= p.start && cell < p.end) {
+    const int64_t cs = p.mesh.nc_stride;
+    int li[ND];
+#pragma unroll
+    for (int i = 0; i < ND; ++i) li[i] = __ldg(p.patch.pidx + i * cs + cell);
+    double X[NV][DIM];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) load_vertex<DIM>(p.mesh.coords, __ldg(p.mesh.vmap + v * cs + cell), X[v]);
+    double w[ND];
+#pragma unroll
+    for (int i = 0; i < ND; ++i) w[i] = su[li[i]];
+    double cm[NM];
+    et_coeffs<FORM, DIM, NM>(X, cm);
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+      double yi = 0.0;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], w[j], t);
+        yi = fma(cm[m], t, yi);
+      }
+      atomicAdd(sacc + li[i], yi);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nu; k += kPatchCells) {
+    const double v = sacc[k];
+    if (v != 0.0) scatter_add(p.y, __ldg(p.patch.dofs + off + k), v);
+  }
+}
+
 }  // namespace fe

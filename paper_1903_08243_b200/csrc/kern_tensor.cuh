@@ -132,8 +132,12 @@ struct TensorLayout {
   static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
+#ifndef FE_TENSOR_MINB
+#define FE_TENSOR_MINB 1
+#endif
+
 template <int FORM, int DIM, int P, int Q>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, FE_TENSOR_MINB)
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -79,6 +80,12 @@ struct fe_plan {
   int32_t* d_map_rm = nullptr;  // row-major [ncells][nd] copy
   int32_t* d_map_lex = nullptr; // row-major, tensor (lexicographic) local order (tensor kernels)
   int32_t* d_lex = nullptr;     // [nd] local node of tensor node
+  // patches (CTA-level dof aggregation, kern_affine.cuh)
+  bool wants_patch = false;
+  int32_t* d_patch_off = nullptr;
+  int32_t* d_patch_dofs = nullptr;
+  uint16_t* d_pidx = nullptr;
+  int patch_maxu = 0;
   double* d_coords = nullptr;   // padded [nverts][cstride]
   const void* b_coords = nullptr;
   const void* b_map0 = nullptr;
@@ -213,6 +220,44 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->end = end;
   int n = end - start;
   affine_et_kernel<FORM, DIM, ND><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND>
+int etp_prepare(fe_plan* p) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  using P = ETPatchParams<NM, ND>;
+  static_assert(sizeof(P) <= 32000, "parameter block too large");
+  std::vector<double> S;
+  element_matrices(p, FORM != FE_FORM_LAPLACIAN_SCALAR, FORM != FE_FORM_MASS, S);
+  if ((int)S.size() != NM * ND * ND) return fail(FE_EINVAL, "element-tensor table size mismatch");
+  P* hp = new P();
+  std::memcpy(hp->S, S.data(), S.size() * sizeof(double));
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(P);
+  p->wants_patch = true;
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND>
+int etp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+               const double*, const double*, cudaStream_t s) {
+  constexpr int NM = et_nmats<FORM, DIM>();
+  using P = ETPatchParams<NM, ND>;
+  if (!p->d_patch_off) return fail(FE_ENOMESH, "patch plan without patches");
+  P* hp = static_cast<P*>(p->host_params);
+  hp->mesh = mesh_view(p);
+  hp->patch.off = p->d_patch_off;
+  hp->patch.dofs = p->d_patch_dofs;
+  hp->patch.pidx = p->d_pidx;
+  hp->u = u;
+  hp->y = y;
+  hp->start = start;
+  hp->end = end;
+  const int b0 = start / kPatchCells, b1 = (end - 1) / kPatchCells;
+  const size_t smem = 2 * (size_t)p->patch_maxu * sizeof(double);
+  affine_et_patch_kernel<FORM, DIM, ND><<<b1 - b0 + 1, kPatchCells, smem, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -393,6 +438,9 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 #define TV(FORM, CELL, DIM, K, P, Q)                                                         \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised", 256,                 \
    tensor_prepare<FORM, DIM, P, Q>, tensor_launch<FORM, DIM, P, Q>}
+#define ETPV(FORM, CELL, DIM, K, ND)                                                         \
+  {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
+   etp_launch<FORM, DIM, ND>}
 #define ETV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 10, "element_tensor", 128, et_prepare<FORM, DIM, ND>,                  \
    et_launch<FORM, DIM, ND>}
@@ -439,6 +487,14 @@ static const Variant kVariants[] = {
     QV(FE_FORM_LAPLACIAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
     QV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
     // element-tensor kernels (affine simplices)
+    ETPV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 1, 3), ETPV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 2, 6),
+    ETPV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 3, 10), ETPV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 1, 3),
+    ETPV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 2, 6), ETPV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 3, 10),
+    ETPV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 1, 4), ETPV(FE_FORM_MASS, FE_CELL_TETRAHEDRON, 3, 2, 10),
+    ETPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 1, 4),
+    ETPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10),
+    ETPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4),
+    ETPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10),
     ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 1, 3), ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 2, 6),
     ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 3, 10), ETV(FE_FORM_MASS, FE_CELL_TRIANGLE, 2, 4, 15),
     ETV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 1, 3), ETV(FE_FORM_HELMHOLTZ, FE_CELL_TRIANGLE, 2, 2, 6),
@@ -513,6 +569,11 @@ void free_mesh(fe_plan* p) {
   cudaFree(p->d_map_lex);
   cudaFree(p->d_coords);
   p->d_map = p->d_vmap = p->d_map_rm = p->d_map_lex = nullptr;
+  cudaFree(p->d_patch_off);
+  cudaFree(p->d_patch_dofs);
+  cudaFree(p->d_pidx);
+  p->d_patch_off = p->d_patch_dofs = nullptr;
+  p->d_pidx = nullptr;
   p->d_coords = nullptr;
   p->b_coords = p->b_map0 = p->b_map1 = nullptr;
 }
@@ -525,12 +586,57 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.cell == FE_CELL_HEXAHEDRON || v.cell == FE_CELL_QUADRILATERAL)
       if (v.priority >= 20 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
+    if ((flags & 2u) && v.priority == 15) continue;              // FE_PLAN_NO_PATCH
     if (!best || v.priority > best->priority) best = &v;
   }
   return best;
 }
 
 }  // namespace
+
+// Patches of kPatchCells consecutive cells: sorted distinct dofs and the
+// patch-local index of every cell dof (host side, once per bound mesh).
+static int build_patches(fe_plan* p, const int32_t* map0, bool dev, cudaStream_t s) {
+  const int nc = p->ncells, nd = p->nd;
+  std::vector<int32_t> m((size_t)nc * nd);
+  if (dev) {
+    CUDA_TRY(cudaMemcpyAsync(m.data(), map0, m.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+    std::memcpy(m.data(), map0, m.size() * sizeof(int32_t));
+  }
+  const int np = (nc + kPatchCells - 1) / kPatchCells;
+  std::vector<int32_t> off(np + 1, 0);
+  std::vector<std::vector<int32_t>> uniq(np);
+  std::vector<uint16_t> pidx((size_t)nd * p->stride, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int b = 0; b < np; ++b) {
+    const int c0 = b * kPatchCells, c1 = std::min(nc, c0 + kPatchCells);
+    std::vector<int32_t>& u = uniq[b];
+    u.assign(m.begin() + (size_t)c0 * nd, m.begin() + (size_t)c1 * nd);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    for (int c = c0; c < c1; ++c)
+      for (int i = 0; i < nd; ++i)
+        pidx[(size_t)i * p->stride + c] =
+            (uint16_t)(std::lower_bound(u.begin(), u.end(), m[(size_t)c * nd + i]) - u.begin());
+  }
+  int maxu = 0;
+  for (int b = 0; b < np; ++b) {
+    off[b + 1] = off[b] + (int)uniq[b].size();
+    maxu = std::max(maxu, (int)uniq[b].size());
+  }
+  std::vector<int32_t> dofs(off[np]);
+  for (int b = 0; b < np; ++b) std::copy(uniq[b].begin(), uniq[b].end(), dofs.begin() + off[b]);
+  CUDA_TRY(cudaMalloc(&p->d_patch_off, off.size() * sizeof(int32_t)));
+  CUDA_TRY(cudaMalloc(&p->d_patch_dofs, std::max<size_t>(1, dofs.size()) * sizeof(int32_t)));
+  CUDA_TRY(cudaMalloc(&p->d_pidx, pidx.size() * sizeof(uint16_t)));
+  CUDA_TRY(cudaMemcpy(p->d_patch_off, off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_patch_dofs, dofs.data(), dofs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_pidx, pidx.data(), pidx.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  p->patch_maxu = maxu;
+  return FE_OK;
+}
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -587,6 +693,7 @@ int fe_plan_create(fe_plan** out, const fe_element_desc* d, uint32_t flags) {
     for (int a = 0; a < dim; ++a) n *= pp;
     p->lex.assign(d->lex, d->lex + n);
   }
+  if (getenv("FE_NO_PATCH")) flags |= 2u;  // experiments: disable patch aggregation
   p->var = select_variant(p, flags);
   if (!p->var) {
     int form = p->form, cell = p->cell, deg = p->degree;
@@ -682,6 +789,13 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     CUDA_TRY(cudaStreamSynchronize(s));
   }
   cudaFree(d_m1);
+  if (p->wants_patch && ncells > 0) {
+    int rc = build_patches(p, map0, dev, s);
+    if (rc) {
+      free_mesh(p);
+      return rc;
+    }
+  }
   p->b_coords = coords;
   p->b_map0 = map0;
   p->b_map1 = map1;
