@@ -275,6 +275,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()   # collective first: the communicator exists before any P2P batch
     names = WORKLOADS[args.config]
     ops = build_ops(names, args.seed, dev, rank, world)
     parity = parity_sample(ops) if rank == 0 else None

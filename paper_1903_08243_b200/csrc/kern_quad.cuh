@@ -229,4 +229,122 @@ __global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
     for (int c = 0; c < VS; ++c) scatter_add(p.y, (int64_t)VS * dof[j] + c, A[j][c]);
 }
 
+// ---------------------------------------------------------------------------
+// Affine-simplex quadrature kernel with the tables in the kernel parameter
+// block (C5: neo-Hookean P2 tetrahedra, 27 points).  On an affine cell the
+// Jacobian and its inverse are computed once per cell from vertex
+// differences, and every table entry enters its DFMA as a uniform
+// constant-bank operand (all threads of a warp read the same entry), so the
+// quadrature loop issues no shared-memory loads.
+// ---------------------------------------------------------------------------
+
+template <int NQ, int ND, int DIM, bool VALUES>
+struct QuadConstParams {
+  MeshView mesh;
+  int32_t start, end;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  const double* __restrict__ mu;
+  const double* __restrict__ lam;
+  double p0, p1;
+  double qw[NQ];
+  double phi[VALUES ? NQ : 1][ND];
+  double dphi[NQ][ND][DIM];
+  double gphi[NQ][DIM + 1];
+};
+
+template <int FORM, int DIM, int ND, int NQ>
+__global__ void __launch_bounds__(128)
+quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, form_needs_values(FORM)> p) {
+  constexpr int VS = form_vs(FORM, DIM);
+  constexpr int NV = DIM + 1;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  int dof[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
+  int vid[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    vid[v] = __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid[v], X[v]);
+  }
+  double w[ND][VS];
+#pragma unroll
+  for (int i = 0; i < ND; ++i)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) w[i][c] = __ldg(p.u + (int64_t)VS * dof[i] + c);
+  double muv[NV], lamv[NV];
+  if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      muv[v] = __ldg(p.mu + vid[v]);
+      lamv[v] = __ldg(p.lam + vid[v]);
+    }
+  }
+  double J[DIM][DIM], Ji[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+  const double absdet = fabs(det_inv<DIM>(J, Ji));
+  double A[ND][VS];
+#pragma unroll
+  for (int i = 0; i < ND; ++i)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) A[i][c] = 0.0;
+#pragma unroll 1
+  for (int q = 0; q < NQ; ++q) {
+    const double tw = p.qw[q] * absdet;
+    double uq[VS], g[VS][DIM];
+#pragma unroll
+    for (int c = 0; c < VS; ++c) {
+      uq[c] = 0.0;
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) g[c][b] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c) {
+        if constexpr (form_needs_values(FORM)) uq[c] = fma(p.phi[q][i], w[i][c], uq[c]);
+        if constexpr (form_needs_grads(FORM)) {
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) g[c][b] = fma(p.dphi[q][i][b], w[i][c], g[c][b]);
+        }
+      }
+    }
+    double mu = p.p0, lam = p.p1;
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+      mu = 0.0;
+      lam = 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        mu = fma(p.gphi[q][v], muv[v], mu);
+        lam = fma(p.gphi[q][v], lamv[v], lam);
+      }
+    }
+    double cv[VS], cg[VS][DIM];
+    pointwise<FORM, DIM, VS>(Ji, tw, uq, g, mu, lam, cv, cg);
+#pragma unroll
+    for (int j = 0; j < ND; ++j)
+#pragma unroll
+      for (int c = 0; c < VS; ++c) {
+        double acc = A[j][c];
+        if constexpr (form_needs_values(FORM)) acc = fma(p.phi[q][j], cv[c], acc);
+        if constexpr (form_needs_grads(FORM)) {
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) acc = fma(p.dphi[q][j][b], cg[c][b], acc);
+        }
+        A[j][c] = acc;
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < ND; ++j)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) scatter_add(p.y, (int64_t)VS * dof[j] + c, A[j][c]);
+}
+
 }  // namespace fe

@@ -132,12 +132,10 @@ struct TensorLayout {
   static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
-#ifndef FE_TENSOR_MINB
-#define FE_TENSOR_MINB 1
-#endif
-
-template <int FORM, int DIM, int P, int Q>
-__global__ void __launch_bounds__(256, FE_TENSOR_MINB)
+// MINB: CTAs per SM the register allocation must allow (1 or 2), chosen per
+// variant from measurements (profiles/r01/sweep_minb2.jsonl)
+template <int FORM, int DIM, int P, int Q, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);
@@ -662,35 +660,35 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
 }  // namespace fe
 
-// registry hook (plan.cu): TV(form, cell, dim, degree, P, Q)
+// registry hook (plan.cu): TV(form, cell, dim, degree, P, Q, MINB)
 #define FE_TENSOR_VARIANTS                                                                   \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 2),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 3),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 4),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 5),                             \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 1, 2, 3),                              \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 2, 3, 4),                              \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 3, 4, 5),                              \
-  TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 1, 2, 3),                                   \
-  TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 2, 3, 4),                                   \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 1, 2, 3),                           \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 2, 3, 4),                           \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 3, 4, 5),                           \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 5, 6),                           \
-  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 1, 2, 3),                                \
-  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 2, 3, 4),                                \
-  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 3, 4, 5),                                \
-  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 4, 5, 6),                                \
-  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 1, 2, 3),                                 \
-  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 2, 3, 4),                                 \
-  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 3, 4, 5),                                 \
-  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 4, 5, 6),                                 \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 1, 2, 3),                          \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 2, 3, 4),                          \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 3, 4, 5),                          \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 4, 5, 6),
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 2, 1),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3, 1),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4, 1),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 2),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, 2),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, 2),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                             \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 2),                              \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 2),                              \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                              \
+  TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                                   \
+  TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                                   \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 1, 2, 3, 2),                           \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 2, 3, 4, 2),                           \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 3, 4, 5, 2),                           \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 5, 6, 2),                           \
+  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 1, 2, 3, 2),                                \
+  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 2, 3, 4, 2),                                \
+  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 3, 4, 5, 2),                                \
+  TV(FE_FORM_ELASTICITY, FE_CELL_QUADRILATERAL, 2, 4, 5, 6, 2),                                \
+  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 1, 2, 3, 2),                                 \
+  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 2, 3, 4, 2),                                 \
+  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 3, 4, 5, 2),                                 \
+  TV(FE_FORM_LAPLACIAN, FE_CELL_QUADRILATERAL, 2, 4, 5, 6, 2),                                 \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 1, 2, 3, 2),                          \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 2, 3, 4, 2),                          \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 3, 4, 5, 2),                          \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_QUADRILATERAL, 2, 4, 5, 6, 2),

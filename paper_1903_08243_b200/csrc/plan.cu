@@ -166,6 +166,49 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 }
 
 // ---------------------------------------------------------------------------
+// quadrature kernel with tables in the parameter block (affine simplices)
+// ---------------------------------------------------------------------------
+
+template <int FORM, int DIM, int ND, int NQ>
+int qc_prepare(fe_plan* p) {
+  using P = QuadConstParams<NQ, ND, DIM, form_needs_values(FORM)>;
+  static_assert(sizeof(P) <= 32000, "parameter block too large");
+  if (p->nq != NQ || p->nd != ND) return fail(FE_EINVAL, "quad_const table size mismatch");
+  P* hp = new P();
+  for (int q = 0; q < NQ; ++q) {
+    hp->qw[q] = p->qw[q];
+    for (int i = 0; i < ND; ++i) {
+      if constexpr (form_needs_values(FORM)) hp->phi[q][i] = p->phi[q * ND + i];
+      for (int b = 0; b < DIM; ++b) hp->dphi[q][i][b] = p->dphi[((size_t)q * ND + i) * DIM + b];
+    }
+    for (int v = 0; v < DIM + 1; ++v) hp->gphi[q][v] = p->gphi[q * (DIM + 1) + v];
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(P);
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND, int NQ>
+int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+              const double* c0, const double* c1, cudaStream_t s) {
+  using P = QuadConstParams<NQ, ND, DIM, form_needs_values(FORM)>;
+  P* hp = static_cast<P*>(p->host_params);
+  hp->mesh = mesh_view(p);
+  hp->start = start;
+  hp->end = end;
+  hp->u = u;
+  hp->y = y;
+  hp->mu = c0;
+  hp->lam = c1;
+  hp->p0 = p->params[0];
+  hp->p1 = p->params[1];
+  const int n = end - start;
+  quad_const_kernel<FORM, DIM, ND, NQ><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+// ---------------------------------------------------------------------------
 // element-tensor kernel (affine simplices)
 // ---------------------------------------------------------------------------
 
@@ -349,7 +392,7 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // sum-factorised tensor-cell kernel
 // ---------------------------------------------------------------------------
 
-template <int FORM, int DIM, int P, int Q>
+template <int FORM, int DIM, int P, int Q, int MINB>
 int tensor_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
   using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM)>;
@@ -388,19 +431,19 @@ int tensor_prepare(fe_plan* p) {
   p->host_params_bytes = sizeof(TP);
   constexpr int CPB = SM::CPB;
   p->tables_bytes = (size_t)CPB * SM::size * sizeof(double);
-  CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q>,
+  CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q, MINB>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
   p->cells_per_block = CPB;
   int dev = 0, sms = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q>, 256,
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q, MINB>, 256,
                                                          p->tables_bytes));
   p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
   return FE_OK;
 }
 
-template <int FORM, int DIM, int P, int Q>
+template <int FORM, int DIM, int P, int Q, int MINB>
 int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                   const double* c0, const double* c1, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
@@ -420,7 +463,7 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   const int cpb = p->cells_per_block;
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
-  tensor_kernel<FORM, DIM, P, Q><<<grid, 256, p->tables_bytes, s>>>(*hp);
+  tensor_kernel<FORM, DIM, P, Q, MINB><<<grid, 256, p->tables_bytes, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -435,12 +478,15 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 #define DMV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 20, "dmma_element_tensor", kDmmaBlock, dmma_prepare<FORM, DIM, ND>,    \
    dmma_launch<FORM, DIM, ND>}
-#define TV(FORM, CELL, DIM, K, P, Q)                                                         \
+#define TV(FORM, CELL, DIM, K, P, Q, MINB)                                                   \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised", 256,                 \
-   tensor_prepare<FORM, DIM, P, Q>, tensor_launch<FORM, DIM, P, Q>}
+   tensor_prepare<FORM, DIM, P, Q, MINB>, tensor_launch<FORM, DIM, P, Q, MINB>}
 #define ETPV(FORM, CELL, DIM, K, ND)                                                         \
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
+#define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
+  {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, ND, NQ>,                   \
+   qc_launch<FORM, DIM, ND, NQ>}
 #define ETV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 10, "element_tensor", 128, et_prepare<FORM, DIM, ND>,                  \
    et_launch<FORM, DIM, ND>}
@@ -507,6 +553,12 @@ static const Variant kVariants[] = {
     ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4),
     ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10),
     ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 3, 20),
+    QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
+    QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 2, 10, 27),
+    QCV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
+    QCV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 2, 10, 27),
+    QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 1, 3, 4),
+    QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 2, 6, 9),
     FE_TENSOR_VARIANTS
     FE_DMMA_VARIANTS
 };
@@ -586,7 +638,9 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.cell == FE_CELL_HEXAHEDRON || v.cell == FE_CELL_QUADRILATERAL)
       if (v.priority >= 20 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
-    if ((flags & 2u) && v.priority == 15) continue;              // FE_PLAN_NO_PATCH
+    // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
+    // opt-in only (FE_PATCH=1) for experiments
+    if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;
     if (!best || v.priority > best->priority) best = &v;
   }
   return best;
