@@ -41,6 +41,7 @@ class ElementDesc(ctypes.Structure):
         ("q1d", ctypes.c_int32),
         ("B1d", _dp), ("D1d", _dp), ("w1d", _dp), ("x1d", _dp), ("lex", _ip),
         ("params", ctypes.c_double * 4),
+        ("nq_aux", ctypes.c_int32), ("qw_aux", _dp), ("dphi_aux", _dp),
     ]
 
 

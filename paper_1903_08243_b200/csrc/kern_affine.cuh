@@ -102,6 +102,103 @@ affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) 
 }
 
 // ---------------------------------------------------------------------------
+// "Split" algorithm for Helmholtz / scalar Laplacian on affine simplices
+// (the frozen-flop choice for C2-P1/P2): the stiffness
+// term sum_ab K_ab int dphi_i/dxi_a dphi_j/dxi_b is integrated with the
+// collapsed rule exact for degree 2k-2 (k^d points: 1 for P1, 8 for P2),
+// i.e. interpolate the reference gradient at each point, multiply by K,
+// integrate back (12 nd k^3 flops on tets), and the mass term uses the
+// reference mass matrix (2 nd^2).  Exact on affine cells, so it equals the
+// reference's quadrature result to round-off.
+// ---------------------------------------------------------------------------
+
+template <int NQS, int ND, int DIM>
+struct SplitParams {
+  MeshView mesh;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  int32_t start, end;
+  double qw[NQS];                 // weights of the low-order rule
+  double dphi[NQS][ND][DIM];      // reference gradients at its points
+  double M[ND][ND];               // reference mass matrix (unused for laplacian_scalar)
+};
+
+template <int FORM, int DIM, int ND, int NQS>
+__global__ void __launch_bounds__(128)
+affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
+  constexpr int NV = DIM + 1;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  int dof[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+  }
+  double w[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) w[i] = __ldg(p.u + dof[i]);
+  // geometry: K = |det J| J^-1 J^-T (symmetric)
+  double J[DIM][DIM], Ji[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+  const double ad = fabs(det_inv<DIM>(J, Ji));
+  double K[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = a; b < DIM; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) s = fma(Ji[a][c], Ji[b][c], s);
+      K[a][b] = K[b][a] = ad * s;
+    }
+  double yv[ND];
+  // mass term
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    double s = 0.0;
+    if constexpr (FORM == FE_FORM_HELMHOLTZ) {
+#pragma unroll
+      for (int j = 0; j < ND; ++j) s = fma(p.M[i][j], w[j], s);
+      s *= ad;
+    }
+    yv[i] = s;
+  }
+  // stiffness term on the low-order rule
+#pragma unroll
+  for (int q = 0; q < NQS; ++q) {
+    double g[DIM];
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) g[b] = 0.0;
+#pragma unroll
+    for (int i = 0; i < ND; ++i)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) g[b] = fma(p.dphi[q][i][b], w[i], g[b]);
+    double f[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) s = fma(K[a][b], g[b], s);
+      f[a] = p.qw[q] * s;
+    }
+#pragma unroll
+    for (int j = 0; j < ND; ++j)
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) yv[j] = fma(p.dphi[q][j][a], f[a], yv[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < ND; ++i) scatter_add(p.y, dof[i], yv[i]);
+}
+
+// ---------------------------------------------------------------------------
 // Patch-aggregated variant (low degree: C1, C2-P1/P2).  At these intensities
 // the global FP64 RED stream (one per cell-dof pair: 6.3M for P1, 15.7M for
 // P2) rivals the arithmetic.  The plan groups each CTA's 128 consecutive

@@ -59,7 +59,7 @@ struct fe_plan {
   // element description (scalars copied; tables copied into vectors)
   int form, cell, degree, vs, dim, nv, nd, nq, q1d;
   double params[4];
-  std::vector<double> qw, phi, dphi, gphi, gdphi, B1d, D1d, w1d, x1d;
+  std::vector<double> qw, phi, dphi, gphi, gdphi, B1d, D1d, w1d, x1d, qw_aux, dphi_aux;
   std::vector<int32_t> lex;
   const Variant* var = nullptr;
   uint32_t flags = 0;
@@ -305,6 +305,41 @@ int etp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const do
   return FE_OK;
 }
 
+template <int FORM, int DIM, int ND, int NQS>
+int split_prepare(fe_plan* p) {
+  using P = SplitParams<NQS, ND, DIM>;
+  static_assert(sizeof(P) <= 32000, "parameter block too large");
+  if ((int)p->qw_aux.size() != NQS) return fail(FE_EUNSUPPORTED, "split kernel needs the degree 2k-2 rule");
+  std::vector<double> S;
+  element_matrices(p, true, false, S);  // reference mass matrix
+  P* hp = new P();
+  for (int q = 0; q < NQS; ++q) {
+    hp->qw[q] = p->qw_aux[q];
+    for (int i = 0; i < ND; ++i)
+      for (int b = 0; b < DIM; ++b) hp->dphi[q][i][b] = p->dphi_aux[((size_t)q * ND + i) * DIM + b];
+  }
+  std::memcpy(hp->M, S.data(), sizeof(hp->M));
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(P);
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND, int NQS>
+int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                 const double*, const double*, cudaStream_t s) {
+  using P = SplitParams<NQS, ND, DIM>;
+  P* hp = static_cast<P*>(p->host_params);
+  hp->mesh = mesh_view(p);
+  hp->u = u;
+  hp->y = y;
+  hp->start = start;
+  hp->end = end;
+  const int n = end - start;
+  affine_split_kernel<FORM, DIM, ND, NQS><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
 // ---------------------------------------------------------------------------
 // DMMA element-tensor kernel (high-degree affine simplices)
 // ---------------------------------------------------------------------------
@@ -487,6 +522,9 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 #define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
   {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, ND, NQ>,                   \
    qc_launch<FORM, DIM, ND, NQ>}
+#define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
+  {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
+   split_launch<FORM, DIM, ND, NQS>}
 #define ETV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 10, "element_tensor", 128, et_prepare<FORM, DIM, ND>,                  \
    et_launch<FORM, DIM, ND>}
@@ -559,6 +597,10 @@ static const Variant kVariants[] = {
     QCV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 2, 10, 27),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 1, 3, 4),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 2, 6, 9),
+    SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
+    SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
+    SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
+    SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
     FE_TENSOR_VARIANTS
     FE_DMMA_VARIANTS
 };
@@ -638,6 +680,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.cell == FE_CELL_HEXAHEDRON || v.cell == FE_CELL_QUADRILATERAL)
       if (v.priority >= 20 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
+    if (v.priority == 12 && (p->qw_aux.empty() || getenv("FE_NO_SPLIT"))) continue;  // split needs the aux rule
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;
@@ -748,6 +791,10 @@ int fe_plan_create(fe_plan** out, const fe_element_desc* d, uint32_t flags) {
     p->lex.assign(d->lex, d->lex + n);
   }
   if (getenv("FE_NO_PATCH")) flags |= 2u;  // experiments: disable patch aggregation
+  if (d->nq_aux > 0 && d->qw_aux && d->dphi_aux) {
+    p->qw_aux.assign(d->qw_aux, d->qw_aux + d->nq_aux);
+    p->dphi_aux.assign(d->dphi_aux, d->dphi_aux + (size_t)d->nq_aux * nd * dim);
+  }
   p->var = select_variant(p, flags);
   if (!p->var) {
     int form = p->form, cell = p->cell, deg = p->degree;

@@ -145,6 +145,15 @@ class GpuKernelHandle:
             d.lex = ctypes.cast(keep["lex"].ctypes.data, ctypes.POINTER(ctypes.c_int32))
         for i, v in enumerate(spec.params[:4]):
             d.params[i] = v
+        d.nq_aux = 0
+        if cell.simplex and spec.form in ("helmholtz", "laplacian_scalar") and el.degree <= 2:
+            # stiffness integrand of an affine cell has degree 2k-2
+            aux = quadrature_rule(cell, 2 * el.degree - 2)
+            keep["qw_aux"] = np.ascontiguousarray(aux.weights, dtype=np.float64)
+            keep["dphi_aux"] = np.ascontiguousarray(tabulate(el, aux).grads, dtype=np.float64)
+            d.nq_aux = aux.npoints
+            d.qw_aux = _dptr(keep["qw_aux"])
+            d.dphi_aux = _dptr(keep["dphi_aux"])
         plan = ctypes.c_void_p()
         flags = _lib.FE_PLAN_GENERIC if unit.target.generic else 0
         rc = lib.fe_plan_create(ctypes.byref(plan), ctypes.byref(d), flags)
