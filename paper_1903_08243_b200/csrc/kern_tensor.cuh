@@ -148,17 +148,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   const int team = threadIdx.x / TS;
   const int t = threadIdx.x % TS;
   const bool in_team = team < CPB;
-  // thread-dependent rows/columns of Dc come from shared memory (a divergent
-  // constant-bank index would serialise the warp); team regions follow
-  double* sDc = smem_all;           // Dc[a][e]
-  double* sDcT = smem_all + QQ;     // Dc[e][a]
-  if constexpr (COLLOC) {
-    for (int k = threadIdx.x; k < QQ; k += blockDim.x) {
-      sDc[k] = p.Dc[k / Q][k % Q];
-      sDcT[k] = p.Dc[k % Q][k / Q];
-    }
-  }
-  double* sm = smem_all + (COLLOC ? 2 * QQ : 0) + (in_team ? team : 0) * L::size;
+  double* sm = smem_all + (in_team ? team : 0) * L::size;
   double* sU = sm + L::U;
   double* s1 = sm + L::O1;
   double* s2 = sm + L::O2;
@@ -335,8 +325,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               double sa = 0.0, sb = 0.0;
 #pragma unroll
               for (int e = 0; e < Q; ++e) {
-                sa = fma(sDc[b * Q + e], s1[a * QQ + c * Q + e], sa);
-                sb = fma(sDc[c * Q + e], s1[a * QQ + e * Q + b], sb);
+                sa = fma(p.Dc[b][e], s1[a * QQ + c * Q + e], sa);
+                sb = fma(p.Dc[c][e], s1[a * QQ + e * Q + b], sb);
               }
               g[comp][1][a] = sa;
               g[comp][2][a] = sb;
@@ -517,8 +507,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
               for (int e = 0; e < Q; ++e) {
                 s = fma(p.Dc[e][a], g[comp][0][e], s);
-                s = fma(sDcT[b * Q + e], s1[a * QQ + c * Q + e], s);
-                s = fma(sDcT[c * Q + e], s1[Q * QQ + a * QQ + e * Q + b], s);
+                s = fma(p.Dc[e][b], s1[a * QQ + c * Q + e], s);
+                s = fma(p.Dc[e][c], s1[Q * QQ + a * QQ + e * Q + b], s);
               }
               V[a] = s;
             }

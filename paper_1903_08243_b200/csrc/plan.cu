@@ -465,7 +465,7 @@ int tensor_prepare(fe_plan* p) {
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
   constexpr int CPB = SM::CPB;
-  p->tables_bytes = ((size_t)CPB * SM::size + (SM::COLLOC ? 2 * Q * Q : 0)) * sizeof(double);
+  p->tables_bytes = (size_t)CPB * SM::size * sizeof(double);
   CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q, MINB>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
   p->cells_per_block = CPB;
