@@ -230,15 +230,19 @@ __global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Affine-simplex quadrature kernel with the tables in the kernel parameter
-// block (C5: neo-Hookean P2 tetrahedra, 27 points).  On an affine cell the
-// Jacobian and its inverse are computed once per cell from vertex
-// differences, and every table entry enters its DFMA as a uniform
-// constant-bank operand (all threads of a warp read the same entry), so the
-// quadrature loop issues no shared-memory loads.
+// Quadrature kernel with the tables in the kernel parameter block.
+//  * affine simplices (C5: neo-Hookean P2 tetrahedra, 27 points): the
+//    Jacobian and its inverse are computed once per cell from vertex
+//    differences;
+//  * low-order tensor cells (Q1 quads/hexes: C3-Q1, C4-quad-Q1, C4-hex-Q1):
+//    the Jacobian is recomputed per point from the vertex basis gradients
+//    (kernels.py:136-151), every cell fully in registers -- at p = 2 a
+//    team-of-threads sum factorisation only adds synchronisation.
+// Every table entry enters its DFMA as a uniform constant-bank operand (all
+// threads of a warp read the same entry): no shared-memory traffic at all.
 // ---------------------------------------------------------------------------
 
-template <int NQ, int ND, int DIM, bool VALUES>
+template <int NQ, int ND, int DIM, int NV, bool VALUES, bool AFFINE>
 struct QuadConstParams {
   MeshView mesh;
   int32_t start, end;
@@ -250,14 +254,14 @@ struct QuadConstParams {
   double qw[NQ];
   double phi[VALUES ? NQ : 1][ND];
   double dphi[NQ][ND][DIM];
-  double gphi[NQ][DIM + 1];
+  double gphi[NQ][NV];
+  double gdphi[AFFINE ? 1 : NQ][NV][DIM];
 };
 
-template <int FORM, int DIM, int ND, int NQ>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
 __global__ void __launch_bounds__(128)
-quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, form_needs_values(FORM)> p) {
+quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFFINE> p) {
   constexpr int VS = form_vs(FORM, DIM);
-  constexpr int NV = DIM + 1;
   const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
   if (cell >= p.end) return;
   const int64_t cs = p.mesh.nc_stride;
@@ -284,12 +288,14 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, form_need
       lamv[v] = __ldg(p.lam + vid[v]);
     }
   }
-  double J[DIM][DIM], Ji[DIM][DIM];
+  double J[DIM][DIM], Ji[DIM][DIM], absdet = 0.0;
+  if constexpr (AFFINE) {
 #pragma unroll
-  for (int a = 0; a < DIM; ++a)
+    for (int a = 0; a < DIM; ++a)
 #pragma unroll
-    for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
-  const double absdet = fabs(det_inv<DIM>(J, Ji));
+      for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+    absdet = fabs(det_inv<DIM>(J, Ji));
+  }
   double A[ND][VS];
 #pragma unroll
   for (int i = 0; i < ND; ++i)
@@ -297,6 +303,18 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, form_need
     for (int c = 0; c < VS; ++c) A[i][c] = 0.0;
 #pragma unroll 1
   for (int q = 0; q < NQ; ++q) {
+    if constexpr (!AFFINE) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+          double s = 0.0;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) s = fma(X[v][a], p.gdphi[q][v][b], s);
+          J[a][b] = s;
+        }
+      absdet = fabs(det_inv<DIM>(J, Ji));
+    }
     const double tw = p.qw[q] * absdet;
     double uq[VS], g[VS][DIM];
 #pragma unroll

@@ -169,11 +169,11 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // quadrature kernel with tables in the parameter block (affine simplices)
 // ---------------------------------------------------------------------------
 
-template <int FORM, int DIM, int ND, int NQ>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF>
 int qc_prepare(fe_plan* p) {
-  using P = QuadConstParams<NQ, ND, DIM, form_needs_values(FORM)>;
+  using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
   static_assert(sizeof(P) <= 32000, "parameter block too large");
-  if (p->nq != NQ || p->nd != ND) return fail(FE_EINVAL, "quad_const table size mismatch");
+  if (p->nq != NQ || p->nd != ND || p->nv != NV) return fail(FE_EINVAL, "quad_const table size mismatch");
   P* hp = new P();
   for (int q = 0; q < NQ; ++q) {
     hp->qw[q] = p->qw[q];
@@ -181,17 +181,21 @@ int qc_prepare(fe_plan* p) {
       if constexpr (form_needs_values(FORM)) hp->phi[q][i] = p->phi[q * ND + i];
       for (int b = 0; b < DIM; ++b) hp->dphi[q][i][b] = p->dphi[((size_t)q * ND + i) * DIM + b];
     }
-    for (int v = 0; v < DIM + 1; ++v) hp->gphi[q][v] = p->gphi[q * (DIM + 1) + v];
+    for (int v = 0; v < NV; ++v) {
+      hp->gphi[q][v] = p->gphi[q * NV + v];
+      if constexpr (!AFF)
+        for (int b = 0; b < DIM; ++b) hp->gdphi[q][v][b] = p->gdphi[((size_t)q * NV + v) * DIM + b];
+    }
   }
   p->host_params = hp;
   p->host_params_bytes = sizeof(P);
   return FE_OK;
 }
 
-template <int FORM, int DIM, int ND, int NQ>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF>
 int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
               const double* c0, const double* c1, cudaStream_t s) {
-  using P = QuadConstParams<NQ, ND, DIM, form_needs_values(FORM)>;
+  using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
   P* hp = static_cast<P*>(p->host_params);
   hp->mesh = mesh_view(p);
   hp->start = start;
@@ -203,7 +207,7 @@ int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_const_kernel<FORM, DIM, ND, NQ><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF><<<(n + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -520,8 +524,11 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
 #define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
-  {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, ND, NQ>,                   \
-   qc_launch<FORM, DIM, ND, NQ>}
+  {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true>,    \
+   qc_launch<FORM, DIM, DIM + 1, ND, NQ, true>}
+#define QCT(FORM, CELL, DIM, NV, K, ND, NQ)                                                  \
+  {FORM, CELL, K, NQ, 25, "quad_const_tensor", 128, qc_prepare<FORM, DIM, NV, ND, NQ, false>, \
+   qc_launch<FORM, DIM, NV, ND, NQ, false>}
 #define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
   {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
    split_launch<FORM, DIM, ND, NQS>}
@@ -601,6 +608,11 @@ static const Variant kVariants[] = {
     SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9),
+    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
     FE_TENSOR_VARIANTS
     FE_DMMA_VARIANTS
 };
@@ -681,6 +693,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
       if (v.priority >= 20 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
     if (v.priority == 12 && (p->qw_aux.empty() || getenv("FE_NO_SPLIT"))) continue;  // split needs the aux rule
+    if (v.priority == 25 && getenv("FE_NO_QCT")) continue;  // experiments: team kernel instead
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;
