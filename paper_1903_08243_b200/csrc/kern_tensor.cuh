@@ -104,7 +104,11 @@ struct TensorLayout {
   static constexpr int RU = (ND + TS - 1) / TS;            // dofs gathered per thread
   static constexpr int RX = (NV * DIM + TS - 1) / TS;      // vertex coordinates per thread
   static constexpr int RM = (NV + TS - 1) / TS;            // vertex field values per thread
+#ifdef FE_TENSOR_DIRECT  // experiment build: direct algorithm everywhere
+  static constexpr bool COLLOC = false;
+#else
   static constexpr bool COLLOC = DIM == 3 && P == Q;
+#endif
   // 3D buffers (producer pencil -> consumer pencil):
   //  Z[j][c][i]  stride SZ: written by (i,j) over c, read by (i,c) over j
   //  Y[i][c][b]  stride SY: written by (i,c) over b, read by (b,c) over i
