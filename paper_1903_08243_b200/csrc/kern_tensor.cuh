@@ -95,7 +95,10 @@ constexpr int pick_inner(int lo, int nr, int ns, int rstep) {
 }
 constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
 
-template <int DIM, int P, int Q, int VS>
+// DIRECT: use the direct algorithm even when p == q (measured faster at
+// Q5/Q6, where the collocation stages' cross-pencil Dc reads, 2 q^4 shared
+// loads per component, outweigh its 25% flop saving)
+template <int DIM, int P, int Q, int VS, bool DIRECT = false>
 struct TensorLayout {
   static constexpr int TS = DIM == 3 ? Q * Q : Q;          // threads per cell (team)
   static constexpr int CPB = 256 / TS;                     // cells per CTA batch
@@ -104,11 +107,7 @@ struct TensorLayout {
   static constexpr int RU = (ND + TS - 1) / TS;            // dofs gathered per thread
   static constexpr int RX = (NV * DIM + TS - 1) / TS;      // vertex coordinates per thread
   static constexpr int RM = (NV + TS - 1) / TS;            // vertex field values per thread
-#ifdef FE_TENSOR_DIRECT  // experiment build: direct algorithm everywhere
-  static constexpr bool COLLOC = false;
-#else
-  static constexpr bool COLLOC = DIM == 3 && P == Q;
-#endif
+  static constexpr bool COLLOC = !DIRECT && DIM == 3 && P == Q;
   // 3D buffers (producer pencil -> consumer pencil):
   //  Z[j][c][i]  stride SZ: written by (i,j) over c, read by (i,c) over j
   //  Y[i][c][b]  stride SY: written by (i,c) over b, read by (b,c) over i
@@ -138,12 +137,12 @@ struct TensorLayout {
 
 // MINB: CTAs per SM the register allocation must allow (1 or 2), chosen per
 // variant from measurements (profiles/r01/sweep_minb2.jsonl)
-template <int FORM, int DIM, int P, int Q, int MINB>
+template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(256, MINB)
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);
-  using L = TensorLayout<DIM, P, Q, VS>;
+  using L = TensorLayout<DIM, P, Q, VS, DIRECT>;
   constexpr int TS = L::TS, CPB = L::CPB, ND = L::ND, NV = L::NV, RU = L::RU;
   constexpr bool COLLOC = L::COLLOC;
   constexpr int QQ = Q * Q;
@@ -664,14 +663,14 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
 }  // namespace fe
 
-// registry hook (plan.cu): TV(form, cell, dim, degree, P, Q, MINB)
+// registry hook (plan.cu): TV(form, cell, dim, degree, P, Q, MINB[, DIRECT])
 #define FE_TENSOR_VARIANTS                                                                   \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 2, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 2),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, 2),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, 2),                             \
+  TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, 2),                            \
+  TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, 2),                            \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                             \

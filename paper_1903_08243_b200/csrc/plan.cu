@@ -431,10 +431,10 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // sum-factorised tensor-cell kernel
 // ---------------------------------------------------------------------------
 
-template <int FORM, int DIM, int P, int Q, int MINB>
+template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 int tensor_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
-  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM)>;
+  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT>;
   static_assert(sizeof(TP) <= 32000, "parameter block too large");
   if (p->q1d != Q || p->degree + 1 != P) return fail(FE_EINVAL, "tensor factors do not match the kernel");
   TP* hp = new TP();
@@ -470,19 +470,19 @@ int tensor_prepare(fe_plan* p) {
   p->host_params_bytes = sizeof(TP);
   constexpr int CPB = SM::CPB;
   p->tables_bytes = (size_t)CPB * SM::size * sizeof(double);
-  CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q, MINB>,
+  CUDA_TRY(cudaFuncSetAttribute(tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
   p->cells_per_block = CPB;
   int dev = 0, sms = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q, MINB>, 256,
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT>, 256,
                                                          p->tables_bytes));
   p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
   return FE_OK;
 }
 
-template <int FORM, int DIM, int P, int Q, int MINB>
+template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                   const double* c0, const double* c1, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
@@ -502,7 +502,7 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   const int cpb = p->cells_per_block;
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
-  tensor_kernel<FORM, DIM, P, Q, MINB><<<grid, 256, p->tables_bytes, s>>>(*hp);
+  tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT><<<grid, 256, p->tables_bytes, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -519,7 +519,10 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
    dmma_launch<FORM, DIM, ND>}
 #define TV(FORM, CELL, DIM, K, P, Q, MINB)                                                   \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised", 256,                 \
-   tensor_prepare<FORM, DIM, P, Q, MINB>, tensor_launch<FORM, DIM, P, Q, MINB>}
+   tensor_prepare<FORM, DIM, P, Q, MINB, false>, tensor_launch<FORM, DIM, P, Q, MINB, false>}
+#define TVD(FORM, CELL, DIM, K, P, Q, MINB)                                                  \
+  {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised_direct", 256,          \
+   tensor_prepare<FORM, DIM, P, Q, MINB, true>, tensor_launch<FORM, DIM, P, Q, MINB, true>}
 #define ETPV(FORM, CELL, DIM, K, ND)                                                         \
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
@@ -613,7 +616,6 @@ static const Variant kVariants[] = {
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 3, 16, 25),
     QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
     FE_TENSOR_VARIANTS
     FE_DMMA_VARIANTS
