@@ -59,6 +59,17 @@ WORKLOAD_TEXT = {
 }
 
 
+def ncu_traffic(label):
+    """DRAM bytes per launch of a kernel from a committed ncu --set full
+    capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            entry = json.load(f).get(label)
+    except (OSError, ValueError):
+        return None
+    return None if entry is None else entry["dram_bytes_per_launch"]
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -360,7 +371,9 @@ def run_ours(args):
                 "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                "traffic": None,
+                "traffic": ncu_traffic(ops[dom]["name"] + ":" + ops[dom]["h"].info["kernel"]),
+                "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, one "
+                                  "ncu --set full capture (profiles/traffic.json)",
                 "peak_source": "measured FP64 (DMMA) peak on this pool's B200s, profiles/r01_fp64_peaks.json "
                                "(MEASURED_PEAKS.json has no FP64 entry)",
                 "algorithmic_flop_per_launch": ops[dom]["F"] * ops[dom]["C"],

@@ -666,8 +666,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 // registry hook (plan.cu): TV(form, cell, dim, degree, P, Q, MINB[, DIRECT])
 #define FE_TENSOR_VARIANTS                                                                   \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 2, 1),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3, 1),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4, 1),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3, 2),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4, 2),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 2),                             \
   TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, 2),                            \
   TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, 2),                            \
