@@ -101,7 +101,11 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 template <int DIM, int P, int Q, int VS, bool DIRECT = false>
 struct TensorLayout {
   static constexpr int TS = DIM == 3 ? Q * Q : Q;          // threads per cell (team)
-  static constexpr int CPB = 256 / TS;                     // cells per CTA batch
+  // teams of <= 32 threads are packed whole into warps, so every team-level
+  // barrier is a __syncwarp and warps never wait for each other
+  static constexpr bool WARP_TEAMS = TS <= 32;
+  static constexpr int TPW = WARP_TEAMS ? 32 / TS : 0;      // teams per warp
+  static constexpr int CPB = WARP_TEAMS ? 8 * TPW : 256 / TS;  // cells per 256-thread CTA
   static constexpr int ND = DIM == 3 ? P * P * P : P * P;  // scalar dofs per cell
   static constexpr int NV = DIM == 3 ? 8 : 4;
   static constexpr int RU = (ND + TS - 1) / TS;            // dofs gathered per thread
@@ -148,9 +152,14 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   constexpr int QQ = Q * Q;
   extern __shared__ double smem_all[];
 
-  const int team = threadIdx.x / TS;
-  const int t = threadIdx.x % TS;
-  const bool in_team = team < CPB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int team = L::WARP_TEAMS ? warp * L::TPW + lane / TS : threadIdx.x / TS;
+  const int t = L::WARP_TEAMS ? lane % TS : threadIdx.x % TS;
+  const bool in_team = L::WARP_TEAMS ? lane < L::TPW * TS : team < CPB;
+  auto team_sync = []() {
+    if constexpr (L::WARP_TEAMS) __syncwarp();
+    else __syncthreads();
+  };
   double* sm = smem_all + (in_team ? team : 0) * L::size;
   double* sU = sm + L::U;
   double* s1 = sm + L::O1;
@@ -232,7 +241,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   load_data(batch);
   park();
   load_map(batch + gridDim.x);
-  __syncthreads();
+  team_sync();
 
   for (; batch < nbatch; batch += gridDim.x) {
     const int cell = cell_of(batch);
@@ -265,7 +274,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             if constexpr (!COLLOC) s1[P * L::SZ + j * L::SZ + c * P + i] = z1;
           }
         }
-        __syncthreads();
+        team_sync();
         // y: pencil (i, c) over j -> Y0 = B Z0 (Y1 = D Z0, Y2 = B Z1)    Y[i][c][b]
         if (active && t < Q * P) {
           const int i = t % P, c = t / P;
@@ -293,7 +302,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             }
           }
         }
-        __syncthreads();
+        team_sync();
         if constexpr (COLLOC) {
           // x: pencil (b, c) over i -> u at the points; d/dxi locally      G[a][c][b]
           if (active) {
@@ -319,7 +328,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             (void)b;
             (void)c;
           }
-          __syncthreads();
+          team_sync();
           // d/deta, d/dzeta with Dc across the pencils of the team
           if (active) {
             const int b = t % Q, c = t / Q;
@@ -335,7 +344,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               g[comp][2][a] = sb;
             }
           }
-          __syncthreads();
+          team_sync();
         } else {
           // x: pencil (b, c) over i -> d/dxi = D Y0, d/deta = B Y1, d/dzeta = B Y2
           if (active) {
@@ -360,7 +369,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               g[comp][2][a] = g2;
             }
           }
-          __syncthreads();
+          team_sync();
         }
       } else {
         // y: pencil i over j -> Y0 = B u, Y1 = D u                         Y[b][i]
@@ -381,7 +390,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             s2[Q * L::S2 + b * L::S2 + i] = y1;
           }
         }
-        __syncthreads();
+        team_sync();
         if (active) {
           const int b = t;
           double q0[P], q1[P];
@@ -402,7 +411,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             g[comp][1][a] = g1;
           }
         }
-        __syncthreads();
+        team_sync();
       }
     }
 
@@ -499,7 +508,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               s1[Q * QQ + a * QQ + t] = g[comp][2][a];
             }
           }
-          __syncthreads();
+          team_sync();
           // V = Dc^T F0 (local) + Dc^T F1 (eta) + Dc^T F2 (zeta); x^T: A = B^T V
           if (active) {
             const int b = t % Q, c = t / Q;
@@ -523,7 +532,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               s2[b * L::SA + c * P + i] = s;                            // A[b][c][i]
             }
           }
-          __syncthreads();
+          team_sync();
           // y^T: pencil (i, c) over b: W = B^T A                           W[c][j][i]
           if (active && t < Q * P) {
             const int i = t % P, c = t / P;
@@ -538,7 +547,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               s1[c * L::SW + j * P + i] = s;
             }
           }
-          __syncthreads();
+          team_sync();
           // z^T: pencil (i, j) over c: y_k = B^T W; scatter
           if (active && t < P * P) {
             double w1[Q];
@@ -552,7 +561,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
             }
           }
-          __syncthreads();
+          team_sync();
         } else {
           // x^T: thread (b, c): A0 = D^T F0, A1 = B^T F1, A2 = B^T F2 over i  A[b][c][i]
           if (active) {
@@ -571,7 +580,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               s2[2 * Q * L::SA + b * L::SA + c * P + i] = a2;
             }
           }
-          __syncthreads();
+          team_sync();
           // y^T: pencil (i, c) over b: W1 = B^T A0 + D^T A1, W2 = B^T A2    W[c][j][i]
           if (active && t < Q * P) {
             const int i = t % P, c = t / P;
@@ -595,7 +604,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               s1[Q * L::SW + c * L::SW + j * P + i] = w2;
             }
           }
-          __syncthreads();
+          team_sync();
           // z^T: pencil (i, j) over c: y_k = B^T W1 + D^T W2; scatter
           if (active && t < P * P) {
             double w1[Q], w2[Q];
@@ -615,7 +624,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
             }
           }
-          __syncthreads();
+          team_sync();
         }
       } else {
         if (active) {
@@ -632,7 +641,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             s2[Q * L::S2 + b * L::S2 + i] = a1;
           }
         }
-        __syncthreads();
+        team_sync();
         if (active && t < P) {
           const int i = t;
           double a0[Q], a1[Q];
@@ -652,12 +661,12 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             scatter_add(p.y, (int64_t)VS * __ldg(mrow + j * P + i) + comp, s);
           }
         }
-        __syncthreads();
+        team_sync();
       }
     }
     // the next batch's data (loads issued at the top of this iteration)
     park();
-    __syncthreads();
+    team_sync();
   }
 }
 
