@@ -61,30 +61,62 @@ __global__ void __launch_bounds__(256, MINB) dmma_et_kernel(DmmaParams p) {
   const int ngroups = (ncell + 8 * NT - 1) / (8 * NT);
   const int gstride = gridDim.x * wpb;
 
-  for (int g = blockIdx.x * wpb + (threadIdx.x >> 5); g < ngroups; g += gstride) {
+  // The map entries of the NEXT group (gather positions, vertex ids and the
+  // scatter rows) are loaded one group ahead, so at the top of a group the
+  // u / coordinate loads issue at once: one memory round trip per group on
+  // the critical path instead of two (map -> data).
+  int pf_dof[NT][KT], pf_vid[NT][NV], pf_row[NT][2][MT];
+  auto load_maps = [&](int g) {
     const int base = p.start + g * 8 * NT;
-    double ureg[NT][KT];
-    double cm[NT][NM];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int cell = base + nt * 8 + r;
-      const bool valid = cell < p.end;
+      const bool valid = g < ngroups && cell < p.end;
 #pragma unroll
       for (int t = 0; t < KT; ++t) {
         const int j = 4 * t + c4;
-        double v = 0.0;
-        if (valid && j < ND) v = __ldg(p.u + __ldg(p.mesh.map + j * cs + cell));
-        ureg[nt][t] = v;
+        pf_dof[nt][t] = (valid && j < ND) ? __ldg(p.mesh.map + j * cs + cell) : -1;
       }
-      double X[NV][DIM];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        int vid = 0;
-        if (valid) vid = __ldg(p.mesh.vmap + v * cs + cell);
-        load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+      for (int v = 0; v < NV; ++v) pf_vid[nt][v] = valid ? __ldg(p.mesh.vmap + v * cs + cell) : -1;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int sc = base + nt * 8 + 2 * c4 + e;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int row = 8 * mt + r;
+          pf_row[nt][e][mt] =
+              (g < ngroups && sc < p.end && row < ND) ? __ldg(p.mesh.map + row * cs + sc) : -1;
+        }
       }
-      et_coeffs<FORM, DIM, NM>(X, cm[nt]);
-      if (!valid) {
+    }
+  };
+  int g = blockIdx.x * wpb + (threadIdx.x >> 5);
+  load_maps(g);
+  for (; g < ngroups; g += gstride) {
+    double ureg[NT][KT];
+    double cm[NT][NM];
+    double X[NT][NV][DIM];
+    int row_dof[NT][2][MT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int t = 0; t < KT; ++t) ureg[nt][t] = pf_dof[nt][t] >= 0 ? __ldg(p.u + pf_dof[nt][t]) : 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) load_vertex<DIM>(p.mesh.coords, pf_vid[nt][v] >= 0 ? pf_vid[nt][v] : 0, X[nt][v]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) row_dof[nt][e][mt] = pf_row[nt][e][mt];
+    }
+    int vid0[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) vid0[nt] = pf_vid[nt][0];
+    load_maps(g + gstride);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      et_coeffs<FORM, DIM, NM>(X[nt], cm[nt]);
+      if (vid0[nt] < 0) {
 #pragma unroll
         for (int m = 0; m < NM; ++m) cm[nt][m] = 0.0;
       }
@@ -115,16 +147,10 @@ __global__ void __launch_bounds__(256, MINB) dmma_et_kernel(DmmaParams p) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cell = base + nt * 8 + 2 * c4 + e;
-        if (cell < p.end) {
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const int row = 8 * mt + r;
-            if (row < ND) scatter_add(p.y, __ldg(p.mesh.map + row * cs + cell), acc[mt][nt][e]);
-          }
-        }
-      }
+        for (int mt = 0; mt < MT; ++mt)
+          if (row_dof[nt][e][mt] >= 0) scatter_add(p.y, row_dof[nt][e][mt], acc[mt][nt][e]);
   }
 }
 

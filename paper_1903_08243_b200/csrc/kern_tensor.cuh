@@ -18,9 +18,11 @@
 // followed by the pointwise flux and the transposed chain back to the nodes.
 //
 // GPU mapping
-//  * a TEAM of Q^2 threads (3D) or Q threads (2D) per cell, 256-thread CTAs
-//    holding CPB = 256/team cells; CTAs are PERSISTENT and walk batches of
-//    CPB cells.  While a batch is being computed, the dof indices of the
+//  * a TEAM of Q^2 threads (3D) or Q threads (2D) per cell.  Teams of <= 32
+//    threads are packed whole into warps (32/team per warp), so every
+//    team-level barrier is a __syncwarp and warps run independently; larger
+//    teams (Q >= 6 in 3D) share CTA barriers.  256-thread CTAs are
+//    PERSISTENT and walk batches of CPB cells.  While a batch is being computed, the dof indices of the
 //    batch after next and the u values / vertex data of the next batch are
 //    already in flight into registers, and are parked in shared memory at
 //    the end of the iteration -- the indirect gather P_e u overlaps the
