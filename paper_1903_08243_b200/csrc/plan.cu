@@ -387,9 +387,9 @@ int dmma_prepare(fe_plan* p) {
   CUDA_TRY(cudaMalloc(&p->d_tables, p->tables_bytes));
   CUDA_TRY(cudaMemcpy(p->d_tables, A.data(), p->tables_bytes, cudaMemcpyHostToDevice));
   const char* env = getenv("FE_DMMA_CFG");
-  // measured (profiles/r01/dmma_cfg_v2.txt): P4 prefers 1 n-tile x 2 CTAs/SM,
-  // P3 2 n-tiles x 1 CTA/SM
-  p->dmma_cfg = env ? atoi(env) : (ND >= 30 ? 1 : 0);
+  // measured with the map prefetch (profiles/r01/dmma_cfg_v3.txt): 1 n-tile
+  // per warp x 2 CTAs/SM is best (P4 71.7%, P3 62.3% of the FP64 roof)
+  p->dmma_cfg = env ? atoi(env) : 1;
   if (p->dmma_cfg < 0 || p->dmma_cfg > 3) p->dmma_cfg = 0;
   switch (p->dmma_cfg) {
     case 1: return dmma_setup<FORM, DIM, ND, 1, 2>(p);
