@@ -100,14 +100,15 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 // DIRECT: use the direct algorithm even when p == q (measured faster at
 // Q5/Q6, where the collocation stages' cross-pencil Dc reads, 2 q^4 shared
 // loads per component, outweigh its 25% flop saving)
-template <int DIM, int P, int Q, int VS, bool DIRECT = false>
+template <int DIM, int P, int Q, int VS, bool DIRECT = false, int BLOCK_ = 256>
 struct TensorLayout {
+  static constexpr int BLOCK = BLOCK_;                       // threads per CTA
   static constexpr int TS = DIM == 3 ? Q * Q : Q;          // threads per cell (team)
   // teams of <= 32 threads are packed whole into warps, so every team-level
   // barrier is a __syncwarp and warps never wait for each other
   static constexpr bool WARP_TEAMS = TS <= 32;
   static constexpr int TPW = WARP_TEAMS ? 32 / TS : 0;      // teams per warp
-  static constexpr int CPB = WARP_TEAMS ? 8 * TPW : 256 / TS;  // cells per 256-thread CTA
+  static constexpr int CPB = WARP_TEAMS ? (BLOCK / 32) * TPW : BLOCK / TS;  // cells per CTA
   static constexpr int ND = DIM == 3 ? P * P * P : P * P;  // scalar dofs per cell
   static constexpr int NV = DIM == 3 ? 8 : 4;
   static constexpr int RU = (ND + TS - 1) / TS;            // dofs gathered per thread
@@ -141,14 +142,17 @@ struct TensorLayout {
   static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
-// MINB: CTAs per SM the register allocation must allow (1 or 2), chosen per
-// variant from measurements (profiles/r01/sweep_minb2.jsonl)
+// MINB: CTAs per SM the register allocation must allow, chosen per variant
+// from measurements (profiles/r01/sweep_minb2.jsonl): 1 or 2 with 256-thread
+// CTAs, 3 with 128-thread CTAs (<= 170 registers, 12 warps per SM)
+template <int MINB> constexpr int tensor_block() { return MINB >= 3 ? 128 : 256; }
+
 template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
-__global__ void __launch_bounds__(256, MINB)
+__global__ void __launch_bounds__(tensor_block<MINB>(), MINB)
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);
-  using L = TensorLayout<DIM, P, Q, VS, DIRECT>;
+  using L = TensorLayout<DIM, P, Q, VS, DIRECT, tensor_block<MINB>()>;
   constexpr int TS = L::TS, CPB = L::CPB, ND = L::ND, NV = L::NV, RU = L::RU;
   constexpr bool COLLOC = L::COLLOC;
   constexpr int QQ = Q * Q;
@@ -679,7 +683,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 2, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3, 2),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4, 2),                             \
-  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 2),                             \
+  TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 3),                             \
   TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, 2),                            \
   TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, 2),                            \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                             \
@@ -687,7 +691,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                             \
   TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 2),                              \
   TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 2),                              \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                              \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 3),                              \
   TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                                   \
   TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                                   \
   TV(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 1, 2, 3, 2),                           \

@@ -266,7 +266,8 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->start = start;
   hp->end = end;
   int n = end - start;
-  affine_et_kernel<FORM, DIM, ND><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  constexpr int per_cta = 128 * kAffineCPT;
+  affine_et_kernel<FORM, DIM, ND><<<(n + per_cta - 1) / per_cta, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -339,7 +340,8 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   hp->start = start;
   hp->end = end;
   const int n = end - start;
-  affine_split_kernel<FORM, DIM, ND, NQS><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  constexpr int per_cta = 128 * kAffineCPT;
+  affine_split_kernel<FORM, DIM, ND, NQS><<<(n + per_cta - 1) / per_cta, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -434,7 +436,7 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 int tensor_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
-  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT>;
+  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT, tensor_block<MINB>()>;
   static_assert(sizeof(TP) <= 32000, "parameter block too large");
   if (p->q1d != Q || p->degree + 1 != P) return fail(FE_EINVAL, "tensor factors do not match the kernel");
   TP* hp = new TP();
@@ -476,7 +478,7 @@ int tensor_prepare(fe_plan* p) {
   int dev = 0, sms = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT>, 256,
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT>, SM::BLOCK,
                                                          p->tables_bytes));
   p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
   return FE_OK;
@@ -502,7 +504,7 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   const int cpb = p->cells_per_block;
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
-  tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT><<<grid, 256, p->tables_bytes, s>>>(*hp);
+  tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT><<<grid, tensor_block<MINB>(), p->tables_bytes, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
