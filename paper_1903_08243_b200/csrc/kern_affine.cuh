@@ -103,7 +103,9 @@ FE_DEVICE void gather_cells(const MeshView& m, const double* __restrict__ u, int
   }
 }
 
-constexpr int kAffineCPT = 2;
+// 2 cells per thread measured slower (profiles/r01/sweep_cpt.jsonl: the
+// low-degree kernels are bound by the L2 RED stream, not by latency)
+constexpr int kAffineCPT = 1;
 
 template <int FORM, int DIM, int ND>
 __global__ void __launch_bounds__(128)
@@ -113,7 +115,6 @@ affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) 
   gather_cells<DIM, ND, kAffineCPT>(p.mesh, p.u, p.start, p.end, g);
 #pragma unroll
   for (int k = 0; k < kAffineCPT; ++k) {
-    if (!g.ok[k]) continue;
     double cm[NM];
     et_coeffs<FORM, DIM, NM>(g.X[k], cm);
 #pragma unroll
@@ -126,7 +127,7 @@ affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) 
         for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], g.w[k][j], t);
         yi = fma(cm[m], t, yi);
       }
-      scatter_add(p.y, g.dof[k][i], yi);
+      scatter_add_warp(p.y, g.dof[k][i], yi, g.ok[k]);
     }
   }
 }
@@ -155,7 +156,7 @@ struct SplitParams {
 
 template <int FORM, int DIM, int ND, int NQS>
 FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[ND],
-                          const double (&X)[DIM + 1][DIM], const double (&w)[ND]);
+                          const double (&X)[DIM + 1][DIM], const double (&w)[ND], bool ok);
 
 template <int FORM, int DIM, int ND, int NQS>
 __global__ void __launch_bounds__(128)
@@ -164,12 +165,12 @@ affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
   gather_cells<DIM, ND, kAffineCPT>(p.mesh, p.u, p.start, p.end, gc);
 #pragma unroll
   for (int k = 0; k < kAffineCPT; ++k)
-    if (gc.ok[k]) split_cell<FORM, DIM, ND, NQS>(p, gc.dof[k], gc.X[k], gc.w[k]);
+    split_cell<FORM, DIM, ND, NQS>(p, gc.dof[k], gc.X[k], gc.w[k], gc.ok[k]);
 }
 
 template <int FORM, int DIM, int ND, int NQS>
 FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[ND],
-                          const double (&X)[DIM + 1][DIM], const double (&w)[ND]) {
+                          const double (&X)[DIM + 1][DIM], const double (&w)[ND], bool ok) {
   // geometry: K = |det J| J^-1 J^-T (symmetric)
   double J[DIM][DIM], Ji[DIM][DIM];
 #pragma unroll
@@ -223,7 +224,7 @@ FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[N
       for (int a = 0; a < DIM; ++a) yv[j] = fma(p.dphi[q][j][a], f[a], yv[j]);
   }
 #pragma unroll
-  for (int i = 0; i < ND; ++i) scatter_add(p.y, dof[i], yv[i]);
+  for (int i = 0; i < ND; ++i) scatter_add_warp(p.y, dof[i], yv[i], ok);
 }
 
 // ---------------------------------------------------------------------------

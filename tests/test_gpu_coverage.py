@@ -1,0 +1,64 @@
+"""Every (form, cell, degree) the sm_100a registry supports, checked against
+the CPU oracle on a small jittered mesh, for the selected (specialised)
+kernel and for the generic reference-structured quadrature kernel where it
+exists.  Unsupported combinations must raise ToolchainError at plan time
+(never fall back)."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+import paper_1903_08243_b200 as fe
+from paper_1903_08243_b200.configs import Config, build_problem
+from oracle import fe_oracle as fo
+
+pytestmark = pytest.mark.gpu
+
+FORMS = fe.OPERATOR_FORMS
+CELLS = {"triangle": (1, 2, 3, 4), "quadrilateral": (1, 2, 3, 4),
+         "tetrahedron": (1, 2, 3, 4), "hexahedron": (1, 2, 3, 4, 5, 6)}
+N = {"triangle": (5, 4), "quadrilateral": (5, 4), "tetrahedron": (3, 2, 2), "hexahedron": (2, 2, 2)}
+
+CASES = [(f, c, k) for f in FORMS for c, ks in CELLS.items() for k in ks
+         if not (f == "neohookean" and k > 2)]
+
+
+def _run(form, cell, k, generic):
+    cfg = Config(f"{form}-{cell}-{k}", "cov", form, cell, k, N[cell],
+                 2 * k + (0 if cell in ("triangle", "tetrahedron") else 2),
+                 u_scale="h" if form == "neohookean" else "unit")
+    prob = build_problem(cfg, seed=k)
+    h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(generic=generic), prob.rule))
+    out = np.zeros(prob.ndofs)
+    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam))
+    P = fo.Problem(form, cell, k, prob.rule.exactness_degree, prob.spec.params)
+    ref = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                      prob.mu, prob.lam)
+    return h.info["kernel"], fo.rel_l2(out, ref)
+
+
+@pytest.mark.parametrize("form,cell,k", CASES)
+def test_registry_kernel_matches_oracle(form, cell, k):
+    try:
+        kernel, err = _run(form, cell, k, False)
+    except fe.ToolchainError:
+        pytest.skip("no sm_100a kernel registered for this combination (raises, no fallback)")
+    assert err <= 1e-12, (kernel, err)
+
+
+@pytest.mark.parametrize("form,cell,k", CASES)
+def test_generic_kernel_matches_oracle(form, cell, k):
+    try:
+        kernel, err = _run(form, cell, k, True)
+    except fe.ToolchainError:
+        pytest.skip("no generic kernel for this combination")
+    assert kernel == "quad"
+    assert err <= 1e-12, (kernel, err)
+
+
+def test_bench_configs_are_all_supported():
+    from paper_1903_08243_b200 import configs as C
+    for name, cfg in C.CONFIGS.items():
+        spec = fe.operator_spec(cfg.form, cfg.cell, cfg.degree)
+        fe.compile_and_load(fe.emit_for(spec, fe.Target(), fe.quadrature_rule(cfg.cell, cfg.qdegree)))
