@@ -70,29 +70,4 @@ FE_DEVICE double det_inv(const double (&J)[DIM][DIM], double (&Ji)[DIM][DIM]) {
 // y[idx] += v.  The global scatter P_e^T: FP64 RED at L2 (REDG.E.ADD.F64).
 FE_DEVICE void scatter_add(double* y, int64_t idx, double v) { atomicAdd(y + idx, v); }
 
-// Warp-aggregated scatter for kernels bound by the L2 RED stream (low-degree
-// simplices: one RED per cell-dof pair, ~4-10 flops each).  Lanes of a warp
-// that target the same dof (consecutive cells share vertices and edges:
-// the 6 Kuhn tets of a cube share local vertices 0 and 3 and the diagonal)
-// are found with __match_any_sync, every lane sums its group's values over
-// shuffles, and only the group's lowest lane issues the RED.  All 32 lanes
-// must call it (pass valid = false for lanes without a cell).
-FE_DEVICE void scatter_add_warp(double* y, int idx, double v, bool valid) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int key = valid ? idx : -1 - lane;
-  const unsigned peers = __match_any_sync(full, key);
-  unsigned rest = peers & ~(1u << lane);
-  double s = v;
-  while (__any_sync(full, rest != 0)) {
-    const int src = rest ? __ffs(rest) - 1 : lane;
-    const double t = __shfl_sync(full, v, src);
-    if (rest) {
-      s += t;
-      rest &= rest - 1;
-    }
-  }
-  if (valid && lane == __ffs(peers) - 1) atomicAdd(y + idx, s);
-}
-
 }  // namespace fe

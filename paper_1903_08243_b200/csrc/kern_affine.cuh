@@ -127,7 +127,7 @@ affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) 
         for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], g.w[k][j], t);
         yi = fma(cm[m], t, yi);
       }
-      scatter_add_warp(p.y, g.dof[k][i], yi, g.ok[k]);
+      if (g.ok[k]) scatter_add(p.y, g.dof[k][i], yi);
     }
   }
 }
@@ -224,7 +224,9 @@ FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[N
       for (int a = 0; a < DIM; ++a) yv[j] = fma(p.dphi[q][j][a], f[a], yv[j]);
   }
 #pragma unroll
-  for (int i = 0; i < ND; ++i) scatter_add_warp(p.y, dof[i], yv[i], ok);
+  if (ok)
+#pragma unroll
+    for (int i = 0; i < ND; ++i) scatter_add(p.y, dof[i], yv[i]);
 }
 
 // ---------------------------------------------------------------------------
