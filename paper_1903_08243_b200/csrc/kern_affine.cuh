@@ -223,7 +223,6 @@ FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[N
 #pragma unroll
       for (int a = 0; a < DIM; ++a) yv[j] = fma(p.dphi[q][j][a], f[a], yv[j]);
   }
-#pragma unroll
   if (!ok) return;
 #pragma unroll
   for (int i = 0; i < ND; ++i) scatter_add(p.y, dof[i], yv[i]);
