@@ -184,6 +184,16 @@ class DistributedOperator:
         return y
 
 
+def exchange_loopback(ys, n_if):
+    """In-process equivalent of DistributedOperator.exchange for a list of
+    consecutive slabs' y vectors (one process driving several slabs, e.g. on
+    one GPU): both neighbours of every interface end with the sum."""
+    for lo, hi in zip(ys[:-1], ys[1:]):
+        s = lo[-n_if:] + hi[:n_if]
+        lo[-n_if:] = s
+        hi[:n_if] = s
+
+
 def slab_range(rank: int, world: int, nz_per_rank: int):
     """Weak scaling: rank r owns cube layers [r nz, (r+1) nz)."""
     return rank * nz_per_rank, (rank + 1) * nz_per_rank, world * nz_per_rank

@@ -90,3 +90,12 @@ def test_slab_of_whole_mesh_matches_config_shape():
     X = s.mesh.coords[s.mesh.cell2vert]
     det = np.linalg.det(X[:, 1:] - X[:, :1])
     assert (det > 0).all()
+
+
+def test_loopback_exchange_matches_distributed_semantics():
+    from paper_1903_08243_b200.distributed import exchange_loopback
+    a, b, c = torch.arange(6.0), torch.arange(6.0) + 10, torch.arange(6.0) + 20
+    exchange_loopback([a, b, c], 2)
+    assert a.tolist() == [0, 1, 2, 3, 14, 16]
+    assert b.tolist() == [14, 16, 12, 13, 34, 36]
+    assert c.tolist() == [34, 36, 22, 23, 24, 25]
