@@ -97,14 +97,21 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
+    def sample(self):
+        """One reading (also called from the timed loop after every step, so
+        short timed regions are covered even if the thread is starved)."""
+        if not self.nv:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.reasons.update(n for b, n in self.REASONS.items() if r & b)
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.reasons.update(n for b, n in self.REASONS.items() if r & b)
-            except Exception:
-                pass
+            self.sample()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -312,6 +319,7 @@ def run_ours(args):
                 e0.record(stream)
                 op["run"](op["u"], op["y"])
                 e1.record(stream)
+            clk.sample()                 # while this step is executing on the GPU
             ev[-1][1].synchronize()
             ts = [e0.elapsed_time(e1) * 1e-3 for e0, e1 in ev]
             per_op += ts

@@ -65,70 +65,39 @@ FE_DEVICE void et_coeffs(const double (&X)[DIM + 1][DIM], double (&cm)[NM]) {
   }
 }
 
-// The low-degree kernels are latency-bound on the dependent gather chain
-// (map -> coordinates / u; ncu: long-scoreboard stalls dominate).  Each
-// thread therefore gathers CPT cells (cells t, t + blockDim, ... of its
-// CTA's range) with all map loads issued first and then all data loads, so
-// CPT independent chains are in flight per thread.
-template <int DIM, int ND, int CPT>
-struct CellGather {
-  bool ok[CPT];
-  int dof[CPT][ND];
-  double X[CPT][DIM + 1][DIM];
-  double w[CPT][ND];
-};
-
-template <int DIM, int ND, int CPT>
-FE_DEVICE void gather_cells(const MeshView& m, const double* __restrict__ u, int start, int end,
-                            CellGather<DIM, ND, CPT>& g) {
-  const int64_t cs = m.nc_stride;
-  const int base = start + blockIdx.x * blockDim.x * CPT + threadIdx.x;
-  int vid[CPT][DIM + 1];
-#pragma unroll
-  for (int k = 0; k < CPT; ++k) {
-    const int cell = base + k * blockDim.x;
-    g.ok[k] = cell < end;
-#pragma unroll
-    for (int i = 0; i < ND; ++i) g.dof[k][i] = g.ok[k] ? __ldg(m.map + i * cs + cell) : 0;
-#pragma unroll
-    for (int v = 0; v <= DIM; ++v)
-      vid[k][v] = !g.ok[k] ? 0 : (m.vmap == m.map) ? g.dof[k][v] : __ldg(m.vmap + v * cs + cell);
-  }
-#pragma unroll
-  for (int k = 0; k < CPT; ++k) {
-#pragma unroll
-    for (int v = 0; v <= DIM; ++v) load_vertex<DIM>(m.coords, vid[k][v], g.X[k][v]);
-#pragma unroll
-    for (int i = 0; i < ND; ++i) g.w[k][i] = g.ok[k] ? __ldg(u + g.dof[k][i]) : 0.0;
-  }
-}
-
-// 2 cells per thread measured slower (profiles/r01/sweep_cpt.jsonl: the
-// low-degree kernels are bound by the L2 RED stream, not by latency)
-constexpr int kAffineCPT = 1;
-
 template <int FORM, int DIM, int ND>
 __global__ void __launch_bounds__(128)
 affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) {
   constexpr int NM = et_nmats<FORM, DIM>();
-  CellGather<DIM, ND, kAffineCPT> g;
-  gather_cells<DIM, ND, kAffineCPT>(p.mesh, p.u, p.start, p.end, g);
+  constexpr int NV = DIM + 1;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  int dof[ND];
 #pragma unroll
-  for (int k = 0; k < kAffineCPT; ++k) {
-    double cm[NM];
-    et_coeffs<FORM, DIM, NM>(g.X[k], cm);
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
 #pragma unroll
-    for (int i = 0; i < ND; ++i) {
-      double yi = 0.0;
+  for (int v = 0; v < NV; ++v) {
+    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+  }
+  double w[ND];
 #pragma unroll
-      for (int m = 0; m < NM; ++m) {
-        double t = 0.0;
+  for (int i = 0; i < ND; ++i) w[i] = __ldg(p.u + dof[i]);
+  double cm[NM];
+  et_coeffs<FORM, DIM, NM>(X, cm);
 #pragma unroll
-        for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], g.w[k][j], t);
-        yi = fma(cm[m], t, yi);
-      }
-      if (g.ok[k]) scatter_add(p.y, g.dof[k][i], yi);
+  for (int i = 0; i < ND; ++i) {
+    double yi = 0.0;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], w[j], t);
+      yi = fma(cm[m], t, yi);
     }
+    scatter_add(p.y, dof[i], yi);
   }
 }
 
@@ -155,22 +124,24 @@ struct SplitParams {
 };
 
 template <int FORM, int DIM, int ND, int NQS>
-FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[ND],
-                          const double (&X)[DIM + 1][DIM], const double (&w)[ND], bool ok);
-
-template <int FORM, int DIM, int ND, int NQS>
 __global__ void __launch_bounds__(128)
 affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
-  CellGather<DIM, ND, kAffineCPT> gc;
-  gather_cells<DIM, ND, kAffineCPT>(p.mesh, p.u, p.start, p.end, gc);
+  constexpr int NV = DIM + 1;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  int dof[ND];
 #pragma unroll
-  for (int k = 0; k < kAffineCPT; ++k)
-    split_cell<FORM, DIM, ND, NQS>(p, gc.dof[k], gc.X[k], gc.w[k], gc.ok[k]);
-}
-
-template <int FORM, int DIM, int ND, int NQS>
-FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[ND],
-                          const double (&X)[DIM + 1][DIM], const double (&w)[ND], bool ok) {
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+  }
+  double w[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) w[i] = __ldg(p.u + dof[i]);
   // geometry: K = |det J| J^-1 J^-T (symmetric)
   double J[DIM][DIM], Ji[DIM][DIM];
 #pragma unroll
@@ -223,7 +194,6 @@ FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, const int (&dof)[N
 #pragma unroll
       for (int a = 0; a < DIM; ++a) yv[j] = fma(p.dphi[q][j][a], f[a], yv[j]);
   }
-  if (!ok) return;
 #pragma unroll
   for (int i = 0; i < ND; ++i) scatter_add(p.y, dof[i], yv[i]);
 }

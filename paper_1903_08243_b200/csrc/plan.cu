@@ -266,8 +266,7 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->start = start;
   hp->end = end;
   int n = end - start;
-  constexpr int per_cta = 128 * kAffineCPT;
-  affine_et_kernel<FORM, DIM, ND><<<(n + per_cta - 1) / per_cta, 128, 0, s>>>(*hp);
+  affine_et_kernel<FORM, DIM, ND><<<(n + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -340,8 +339,7 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   hp->start = start;
   hp->end = end;
   const int n = end - start;
-  constexpr int per_cta = 128 * kAffineCPT;
-  affine_split_kernel<FORM, DIM, ND, NQS><<<(n + per_cta - 1) / per_cta, 128, 0, s>>>(*hp);
+  affine_split_kernel<FORM, DIM, ND, NQS><<<(n + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
