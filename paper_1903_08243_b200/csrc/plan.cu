@@ -93,8 +93,11 @@ struct fe_plan {
   uint32_t b_flags = 0;
   // host-entry staging
   cudaStream_t hstream = nullptr;
+  cudaStream_t hstream2 = nullptr;
+  cudaEvent_t ev_u = nullptr, ev_y0 = nullptr;
   double* d_u = nullptr;
   double* d_y = nullptr;
+  double* d_y0 = nullptr;
   double* d_c0 = nullptr;
   double* d_c1 = nullptr;
   size_t cap_u = 0, cap_c = 0;
@@ -642,6 +645,12 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rm, const int32_t* __
   out[t] = rm[c * nd + perm[l]];
 }
 
+__global__ void k_add(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
+
 __global__ void k_pad_coords(const double* __restrict__ x, double* __restrict__ out, int nv, int dim,
                              int cstride) {
   int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -965,9 +974,11 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   if (p->cap_u < n) {
     cudaFree(p->d_u);
     cudaFree(p->d_y);
-    p->d_u = p->d_y = nullptr;
+    cudaFree(p->d_y0);
+    p->d_u = p->d_y = p->d_y0 = nullptr;
     CUDA_TRY(cudaMalloc(&p->d_u, n * sizeof(double)));
     CUDA_TRY(cudaMalloc(&p->d_y, n * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&p->d_y0, n * sizeof(double)));
     p->cap_u = n;
   }
   const double* c0 = nullptr;
@@ -985,10 +996,24 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
     c0 = p->d_c0;
     c1 = p->d_c1;
   }
+  // u first; then the operator runs (into a zeroed buffer) while the caller's
+  // dat0 uploads on a second stream behind it; the accumulate dat0 + A(u)
+  // is one axpy before the download.
+  if (!p->hstream2) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream2, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0, cudaEventDisableTiming));
+  }
   CUDA_TRY(cudaMemcpyAsync(p->d_u, dat2, n * sizeof(double), cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(p->d_y, dat0, n * sizeof(double), cudaMemcpyHostToDevice, s));
-  int rc = fe_apply(p, start, end, p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
+  CUDA_TRY(cudaEventRecord(p->ev_u, s));
+  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_u, 0));
+  CUDA_TRY(cudaMemcpyAsync(p->d_y0, dat0, n * sizeof(double), cudaMemcpyHostToDevice, p->hstream2));
+  CUDA_TRY(cudaEventRecord(p->ev_y0, p->hstream2));
+  int rc = fe_apply(p, start, end, p->d_y, p->d_u, c0, c1, FE_APPLY_OVERWRITE, s);
   if (rc) return rc;
+  CUDA_TRY(cudaStreamWaitEvent(s, p->ev_y0, 0));
+  k_add<<<std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(p->d_y, p->d_y0, (int64_t)n);
+  CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(dat0, p->d_y, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return FE_OK;
@@ -1013,9 +1038,13 @@ void fe_plan_destroy(fe_plan* p) {
   cudaFree(p->d_lex);
   cudaFree(p->d_u);
   cudaFree(p->d_y);
+  cudaFree(p->d_y0);
   cudaFree(p->d_c0);
   cudaFree(p->d_c1);
   if (p->hstream) cudaStreamDestroy(p->hstream);
+  if (p->hstream2) cudaStreamDestroy(p->hstream2);
+  if (p->ev_u) cudaEventDestroy(p->ev_u);
+  if (p->ev_y0) cudaEventDestroy(p->ev_y0);
   ::operator delete(p->host_params);
   delete p;
 }
