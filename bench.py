@@ -171,7 +171,10 @@ def build_ops(names, seed, device, rank, world):
                   F=fe.flops_per_cell(prob.spec, prob.rule),
                   B=fe.bytes_per_cell(prob.spec, m, dm))
         local = (lambda h, coef: lambda uu, yy: h.apply(uu, yy, coef=coef, overwrite=True))(h, coef)
-        op["dist"] = DistributedOperator(prob, local, rank, world) if (slab and world > 1) else None
+        rng = (lambda h, coef: lambda uu, yy, a, b, ow: h.apply(uu, yy, a, b, coef=coef,
+                                                                 overwrite=ow))(h, coef)
+        op["dist"] = (DistributedOperator(prob, local, rank, world, range_apply=rng)
+                      if (slab and world > 1) else None)
         op["run"] = op["dist"].apply if op["dist"] else local
         ops.append(op)
     return ops

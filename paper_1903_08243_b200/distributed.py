@@ -139,16 +139,28 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
 
 class DistributedOperator:
     """y = A u on this rank's slab, interface planes summed with the
-    neighbouring ranks.  ``local_apply(u, y)`` computes the slab-local
-    action (overwrite); ``torch.distributed`` must be initialised (NCCL for
-    CUDA tensors, gloo for CPU tensors)."""
+    neighbouring ranks; ``torch.distributed`` must be initialised (NCCL for
+    CUDA tensors, gloo for CPU tensors).
 
-    def __init__(self, slab: Slab, local_apply, rank: int, world: int):
+    ``local_apply(u, y)`` computes the slab-local action (overwrite).  With
+    ``range_apply(u, y, start, end, overwrite)`` (the plan's fe_apply on a
+    cell range) the exchange OVERLAPS the interior: cells are ordered cube
+    layer by cube layer (z slowest), so the boundary layers -- the only cells
+    touching an interface plane -- are two contiguous ranges.  They are
+    applied first, the interface planes go out on NCCL (its stream waits for
+    them, not for the interior), the interior layers run on the compute
+    stream meanwhile, and the received partial sums are added after both."""
+
+    def __init__(self, slab: Slab, local_apply, rank: int, world: int, range_apply=None):
         self.slab = slab
         self.local_apply = local_apply
+        self.range_apply = range_apply
         self.rank = rank
         self.world = world
         self.n_if = slab.plane * slab.spec.element.value_size
+        nx, ny, nzl = slab.mesh.grid
+        self.layer_cells = slab.mesh.ncells // nzl
+        self.nlayers = nzl
         self._bufs = None
 
     def _buffers(self, y):
@@ -158,29 +170,45 @@ class DistributedOperator:
                           torch.empty(self.n_if, dtype=y.dtype, device=y.device))
         return self._bufs
 
-    def exchange(self, y):
-        """Sum the interface planes with the neighbours (in place)."""
+    def _start_exchange(self, y):
         import torch.distributed as dist
         n = self.n_if
         below, above = self._buffers(y)
         ops = []
         if self.slab.has_below:
-            ops.append(dist.P2POp(dist.isend, y[:n].contiguous(), self.rank - 1))
+            ops.append(dist.P2POp(dist.isend, y[:n], self.rank - 1))
             ops.append(dist.P2POp(dist.irecv, below, self.rank - 1))
         if self.slab.has_above:
-            ops.append(dist.P2POp(dist.isend, y[-n:].contiguous(), self.rank + 1))
+            ops.append(dist.P2POp(dist.isend, y[-n:], self.rank + 1))
             ops.append(dist.P2POp(dist.irecv, above, self.rank + 1))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def _finish_exchange(self, y, works):
+        for w in works:
+            w.wait()
+        n = self.n_if
+        below, above = self._bufs if self._bufs else (None, None)
         if self.slab.has_below:
             y[:n] += below
         if self.slab.has_above:
             y[-n:] += above
 
+    def exchange(self, y):
+        """Sum the interface planes with the neighbours (in place)."""
+        self._finish_exchange(y, self._start_exchange(y))
+
     def apply(self, u, y):
-        self.local_apply(u, y)
-        self.exchange(y)
+        nc, lc = self.slab.mesh.ncells, self.layer_cells
+        if self.range_apply is None or self.world == 1 or self.nlayers < 3:
+            self.local_apply(u, y)
+            self.exchange(y)
+            return y
+        # boundary layers first (the only cells touching an interface plane)
+        self.range_apply(u, y, 0, lc, True)           # zero-fills y, then layer 0
+        self.range_apply(u, y, nc - lc, nc, False)
+        works = self._start_exchange(y)                 # NCCL waits for the boundary cells
+        self.range_apply(u, y, lc, nc - lc, False)      # interior overlaps the exchange
+        self._finish_exchange(y, works)
         return y
 
 

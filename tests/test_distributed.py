@@ -27,7 +27,16 @@ def _oracle_apply(slab):
     def apply(u, y):
         y.copy_(torch.from_numpy(fo.assemble(P, slab.mesh.coords, slab.mesh.cell2vert,
                                              slab.dofmap.cell2dof, u.numpy(), slab.mu, slab.lam)))
-    return apply
+
+    def range_apply(u, y, start, end, overwrite):
+        part = torch.from_numpy(fo.assemble(P, slab.mesh.coords, slab.mesh.cell2vert,
+                                            slab.dofmap.cell2dof, u.numpy(), slab.mu, slab.lam,
+                                            start, end))
+        if overwrite:
+            y.copy_(part)
+        else:
+            y += part
+    return apply, range_apply
 
 
 def _free_port():
@@ -38,14 +47,15 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, name, nz, q):
+def _worker(rank, world, port, name, nz, q, overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = C.get_config(name, (3, 2, nz))
     z0, z1, nzg = slab_range(rank, world, nz)
     slab = build_slab(cfg, 11, z0, z1, nzg)
-    op = DistributedOperator(slab, _oracle_apply(slab), rank, world)
+    apply, range_apply = _oracle_apply(slab)
+    op = DistributedOperator(slab, apply, rank, world, range_apply if overlap else None)
     u = torch.from_numpy(slab.u.copy())
     y = torch.zeros_like(u)
     op.apply(u, y)
@@ -54,13 +64,16 @@ def _worker(rank, world, port, name, nz, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("C2-P2", 2), ("C5", 2), ("C3-Q2", 3), ("C4-hex-Q1", 2)])
-def test_distributed_equals_single_domain(name, world):
-    nz = 2
+@pytest.mark.parametrize("name,world,nz,overlap", [
+    ("C2-P2", 2, 2, False), ("C5", 2, 2, False), ("C3-Q2", 3, 2, False), ("C4-hex-Q1", 2, 2, False),
+    # boundary layers first, exchange overlapping the interior layers
+    ("C2-P2", 3, 3, True), ("C4-hex-Q1", 2, 4, True)])
+def test_distributed_equals_single_domain(name, world, nz, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, nz, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, nz, q, overlap))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])

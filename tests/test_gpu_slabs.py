@@ -14,11 +14,13 @@ from oracle import fe_oracle as fo
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,world", [("C2-P2", 2), ("C2-P4", 3), ("C3-Q3", 2), ("C4-hex-Q2", 2),
-                                        ("C5", 4)])
-def test_slabs_on_gpu_equal_single_domain(name, world):
+@pytest.mark.parametrize("name,world,nz,split", [
+    ("C2-P2", 2, 2, False), ("C2-P4", 3, 2, False), ("C3-Q3", 2, 2, False), ("C4-hex-Q2", 2, 2, False),
+    ("C5", 4, 2, False),
+    # the overlapped order of DistributedOperator: boundary layers, then interior
+    ("C2-P3", 3, 3, True), ("C3-Q2", 2, 4, True), ("C4-hex-Q1", 2, 3, True)])
+def test_slabs_on_gpu_equal_single_domain(name, world, nz, split):
     import torch
-    nz = 2
     cfg = C.get_config(name, (3, 2, nz))
     dev = torch.device("cuda")
     ys, slabs = [], []
@@ -33,7 +35,14 @@ def test_slabs_on_gpu_equal_single_domain(name, world):
         u = torch.tensor(s.u, device=dev)
         y = torch.zeros_like(u)
         coef = None if s.mu is None else (torch.tensor(s.mu, device=dev), torch.tensor(s.lam, device=dev))
-        h.apply(u, y, coef=coef, overwrite=True)
+        if split:
+            nc = s.mesh.ncells
+            lc = nc // nz
+            h.apply(u, y, 0, lc, coef=coef, overwrite=True)
+            h.apply(u, y, nc - lc, nc, coef=coef)
+            h.apply(u, y, lc, nc - lc, coef=coef)
+        else:
+            h.apply(u, y, coef=coef, overwrite=True)
         ys.append(y)
         slabs.append(s)
     exchange_loopback(ys, slabs[0].plane * slabs[0].spec.element.value_size)
