@@ -255,7 +255,7 @@ struct QuadConstParams {
   double phi[VALUES ? NQ : 1][ND];
   double dphi[NQ][ND][DIM];
   double gphi[NQ][NV];
-  double gdphi[AFFINE ? 1 : NQ][NV][DIM];
+  double px[AFFINE ? 1 : NQ][DIM];  // reference coordinates of the points (tensor cells)
 };
 
 template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
@@ -289,12 +289,34 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
     }
   }
   double J[DIM][DIM], Ji[DIM][DIM], absdet = 0.0;
+  // multilinear map x = a0 + a1 xi + a2 eta (+ a3 zeta) + a4 xi eta (+ a5 xi zeta
+  // + a6 eta zeta + a7 xi eta zeta): J at a point costs 3 FMAs per entry
+  // (2D: 1) instead of a sum over all 2^d vertex-basis gradients
+  double cf[DIM == 3 ? 7 : 3][DIM];
   if constexpr (AFFINE) {
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
       for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
     absdet = fabs(det_inv<DIM>(J, Ji));
+  } else if constexpr (DIM == 3) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      cf[0][d] = X[1][d] - X[0][d];                                   // xi
+      cf[1][d] = X[2][d] - X[0][d];                                   // eta
+      cf[2][d] = X[4][d] - X[0][d];                                   // zeta
+      cf[3][d] = (X[3][d] - X[2][d]) - cf[0][d];                      // xi eta
+      cf[4][d] = (X[5][d] - X[4][d]) - cf[0][d];                      // xi zeta
+      cf[5][d] = (X[6][d] - X[4][d]) - cf[1][d];                      // eta zeta
+      cf[6][d] = ((X[7][d] - X[6][d]) - (X[5][d] - X[4][d])) - (X[3][d] - X[2][d]) + cf[0][d];
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      cf[0][d] = X[1][d] - X[0][d];
+      cf[1][d] = X[2][d] - X[0][d];
+      cf[2][d] = (X[3][d] - X[2][d]) - cf[0][d];
+    }
   }
   double A[ND][VS];
 #pragma unroll
@@ -304,15 +326,23 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
 #pragma unroll 1
   for (int q = 0; q < NQ; ++q) {
     if constexpr (!AFFINE) {
+      if constexpr (DIM == 3) {
+        const double xi = p.px[q][0], eta = p.px[q][1], zeta = p.px[q][2];
+        const double ez = eta * zeta, xz = xi * zeta, xe = xi * eta;
 #pragma unroll
-      for (int a = 0; a < DIM; ++a)
-#pragma unroll
-        for (int b = 0; b < DIM; ++b) {
-          double s = 0.0;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) s = fma(X[v][a], p.gdphi[q][v][b], s);
-          J[a][b] = s;
+        for (int d = 0; d < 3; ++d) {
+          J[d][0] = fma(cf[6][d], ez, fma(cf[4][d], zeta, fma(cf[3][d], eta, cf[0][d])));
+          J[d][1] = fma(cf[6][d], xz, fma(cf[5][d], zeta, fma(cf[3][d], xi, cf[1][d])));
+          J[d][2] = fma(cf[6][d], xe, fma(cf[5][d], eta, fma(cf[4][d], xi, cf[2][d])));
         }
+      } else {
+        const double xi = p.px[q][0], eta = p.px[q][1];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          J[d][0] = fma(cf[2][d], eta, cf[0][d]);
+          J[d][1] = fma(cf[2][d], xi, cf[1][d]);
+        }
+      }
       absdet = fabs(det_inv<DIM>(J, Ji));
     }
     const double tw = p.qw[q] * absdet;

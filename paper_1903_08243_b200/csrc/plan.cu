@@ -186,8 +186,16 @@ int qc_prepare(fe_plan* p) {
     }
     for (int v = 0; v < NV; ++v) {
       hp->gphi[q][v] = p->gphi[q * NV + v];
-      if constexpr (!AFF)
-        for (int b = 0; b < DIM; ++b) hp->gdphi[q][v][b] = p->gdphi[((size_t)q * NV + v) * DIM + b];
+    }
+    if constexpr (!AFF) {
+      // tensor rule, x slowest (elements.py:193-198): q = (ix * Q + iy) * Q + iz
+      const int Q1 = p->q1d;
+      if (Q1 <= 0) return fail(FE_EINVAL, "tensor quad_const plan needs the 1D rule");
+      int rem = q;
+      for (int b = DIM - 1; b >= 0; --b) {
+        hp->px[q][b] = p->x1d[rem % Q1];
+        rem /= Q1;
+      }
     }
   }
   p->host_params = hp;
