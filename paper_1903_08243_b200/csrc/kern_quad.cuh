@@ -258,8 +258,10 @@ struct QuadConstParams {
   double px[AFFINE ? 1 : NQ][DIM];  // reference coordinates of the points (tensor cells)
 };
 
-template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
-__global__ void __launch_bounds__(128)
+// MINB: CTAs of 128 threads per SM the register allocation must allow
+// (chosen per variant from measurements)
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB)
 quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFFINE> p) {
   constexpr int VS = form_vs(FORM, DIM);
   const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;

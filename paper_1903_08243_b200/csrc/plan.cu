@@ -172,7 +172,7 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // quadrature kernel with tables in the parameter block (affine simplices)
 // ---------------------------------------------------------------------------
 
-template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1>
 int qc_prepare(fe_plan* p) {
   using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
   static_assert(sizeof(P) <= 32000, "parameter block too large");
@@ -203,7 +203,7 @@ int qc_prepare(fe_plan* p) {
   return FE_OK;
 }
 
-template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1>
 int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
               const double* c0, const double* c1, cudaStream_t s) {
   using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
@@ -218,7 +218,7 @@ int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB><<<(n + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -540,9 +540,9 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 #define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
   {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true>,    \
    qc_launch<FORM, DIM, DIM + 1, ND, NQ, true>}
-#define QCT(FORM, CELL, DIM, NV, K, ND, NQ)                                                  \
-  {FORM, CELL, K, NQ, 25, "quad_const_tensor", 128, qc_prepare<FORM, DIM, NV, ND, NQ, false>, \
-   qc_launch<FORM, DIM, NV, ND, NQ, false>}
+#define QCT(FORM, CELL, DIM, NV, K, ND, NQ, MINB)                                            \
+  {FORM, CELL, K, NQ, 25, "quad_const_tensor", 128,                                          \
+   qc_prepare<FORM, DIM, NV, ND, NQ, false, MINB>, qc_launch<FORM, DIM, NV, ND, NQ, false, MINB>}
 #define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
   {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
    split_launch<FORM, DIM, ND, NQS>}
@@ -622,12 +622,12 @@ static const Variant kVariants[] = {
     SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
-    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8),
-    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16),
-    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 6),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 4),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 3),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 6),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16, 4),
+    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 2),
     FE_TENSOR_VARIANTS
     FE_DMMA_VARIANTS
 };
