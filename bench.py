@@ -415,7 +415,8 @@ def run_reference(args):
         prob, _ = build_problem_for_rank(name, args.seed, 0, 1)
         ops.append(dict(name=name, prob=prob, C=prob.mesh.ncells, ndofs=prob.ndofs,
                         F=fe.flops_per_cell(prob.spec, prob.rule)))
-    budget = max(4.0, 60.0 / max(1, args.steps + args.warmup))
+    # the whole --steps K --warmup W run stays near two minutes of CPU work
+    budget = max(0.4, 120.0 / max(1, args.steps + args.warmup))
     vals = []
     for it in range(args.warmup + args.steps):
         r = cpu_measure(ops, budget_s=budget)

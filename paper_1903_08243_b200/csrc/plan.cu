@@ -622,12 +622,12 @@ static const Variant kVariants[] = {
     SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
-    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 6),
-    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 4),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 3),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 6),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 1),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16, 4),
-    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 2),
+    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
     FE_TENSOR_VARIANTS
     FE_DMMA_VARIANTS
 };
