@@ -77,8 +77,12 @@ def test_full_size_constants(name):
     if prob.spec.form == "laplacian_scalar":
         ref = float(torch.linalg.norm(A(torch.tensor(prob.u, device=dev))))
         assert float(torch.linalg.norm(y)) <= 1e-12 * ref
-    else:   # helmholtz: grad 1 = 0 leaves the mass term; sum = volume of the unit cube
-        assert abs(float(y.sum()) - 1.0) <= 1e-12
+    else:
+        # helmholtz: grad 1 = 0 leaves the mass term; sum = volume of the unit
+        # cube.  The stiffness term cancels only to round-off of the (shared)
+        # reference matrices' row sums, a SYSTEMATIC ~1e-15 |S| per cell that
+        # adds up over 1.6M cells weighted by |K| ~ h: tolerance 1e-9.
+        assert abs(float(y.sum()) - 1.0) <= 1e-9
 
 
 def test_full_size_neohookean_translation_invariance_and_parity():
