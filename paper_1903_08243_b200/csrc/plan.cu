@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "kern_affine.cuh"
+#include "kern_plane.cuh"
 #include "kern_quad.cuh"
 #include "kern_tensor.cuh"
 #include "kern_dmma.cuh"
@@ -442,13 +443,10 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // sum-factorised tensor-cell kernel
 // ---------------------------------------------------------------------------
 
-template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
-int tensor_prepare(fe_plan* p) {
-  using TP = TensorParams<Q, P>;
-  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT, tensor_block<MINB>()>;
-  static_assert(sizeof(TP) <= 32000, "parameter block too large");
+// 1D factors of a tensor-cell plan -> the kernel parameter block
+template <int Q, int P>
+int fill_tensor_tables(const fe_plan* p, TensorParams<Q, P>* hp) {
   if (p->q1d != Q || p->degree + 1 != P) return fail(FE_EINVAL, "tensor factors do not match the kernel");
-  TP* hp = new TP();
   for (int a = 0; a < Q; ++a) {
     for (int i = 0; i < P; ++i) {
       hp->B[a][i] = p->B1d[a * P + i];
@@ -456,8 +454,6 @@ int tensor_prepare(fe_plan* p) {
     }
     hp->w[a] = p->w1d[a];
   }
-  const int stride = DIM == 3 ? Q * Q : Q;
-  (void)stride;
   for (int a = 0; a < Q; ++a) hp->x[a] = p->x1d[a];
   // collocation derivative at the Gauss points: Dc[a][e] = l_e'(x_a) for the
   // Lagrange basis l_e on the Gauss points (barycentric formula)
@@ -476,6 +472,19 @@ int tensor_prepare(fe_plan* p) {
       diag -= hp->Dc[a][e];
     }
     hp->Dc[a][a] = diag;
+  }
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
+int tensor_prepare(fe_plan* p) {
+  using TP = TensorParams<Q, P>;
+  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT, tensor_block<MINB>()>;
+  static_assert(sizeof(TP) <= 32000, "parameter block too large");
+  TP* hp = new TP();
+  if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
+    delete hp;
+    return rc;
   }
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
@@ -518,6 +527,53 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   return FE_OK;
 }
 
+// plane-per-thread scalar Laplacian on hexahedra (kern_plane.cuh)
+template <int P, int Q, int WARPS, int MINB>
+int plane_prepare(fe_plan* p) {
+  using TP = TensorParams<Q, P>;
+  using L = PlaneLayout<P, Q>;
+  TP* hp = new TP();
+  if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
+    delete hp;
+    return rc;
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(TP);
+  p->tables_bytes = (size_t)WARPS * L::WARP_DOUBLES * sizeof(double);
+  CUDA_TRY(cudaFuncSetAttribute(plane_kernel<P, Q, WARPS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->tables_bytes));
+  p->cells_per_block = WARPS * L::TPW;
+  int dev = 0, sms = 0, per_sm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plane_kernel<P, Q, WARPS, MINB>, WARPS * 32,
+                                                         p->tables_bytes));
+  p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  return FE_OK;
+}
+
+template <int P, int Q, int WARPS, int MINB>
+int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                 const double*, const double*, cudaStream_t s) {
+  using TP = TensorParams<Q, P>;
+  TP* hp = static_cast<TP*>(p->host_params);
+  if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
+  hp->mesh = mesh_view(p);
+  hp->maplex = p->d_map_lex;
+  hp->u = u;
+  hp->y = y;
+  hp->mu = hp->lam = nullptr;
+  hp->start = start;
+  hp->end = end;
+  const int n = end - start;
+  const int cpb = p->cells_per_block;
+  const int nbatch = (n + cpb - 1) / cpb;
+  const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
+  plane_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
 // ---------------------------------------------------------------------------
 // registry
 // ---------------------------------------------------------------------------
@@ -534,6 +590,9 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 #define TVD(FORM, CELL, DIM, K, P, Q, MINB)                                                  \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised_direct", 256,          \
    tensor_prepare<FORM, DIM, P, Q, MINB, true>, tensor_launch<FORM, DIM, P, Q, MINB, true>}
+#define PLV(K, P, Q, WARPS, MINB)                                                            \
+  {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 22, "sum_factorised_plane",   \
+   WARPS * 32, plane_prepare<P, Q, WARPS, MINB>, plane_launch<P, Q, WARPS, MINB>}
 #define ETPV(FORM, CELL, DIM, K, ND)                                                         \
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
@@ -629,6 +688,7 @@ static const Variant kVariants[] = {
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16, 4),
     QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
     FE_TENSOR_VARIANTS
+    FE_PLANE_VARIANTS
     FE_DMMA_VARIANTS
 };
 
@@ -715,6 +775,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
     if (v.priority == 12 && (p->qw_aux.empty() || getenv("FE_NO_SPLIT"))) continue;  // split needs the aux rule
     if (v.priority == 25 && getenv("FE_NO_QCT")) continue;  // experiments: team kernel instead
+    if (v.priority == 22 && getenv("FE_NO_PLANE")) continue;  // experiments: pencil team kernel
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;
