@@ -1,37 +1,39 @@
-// Plane-per-thread sum-factorised kernel: scalar Laplacian on hexahedra (C3).
+// Plane-per-thread, column-streamed sum-factorised kernel: scalar Laplacian
+// on hexahedra (C3).
 //
-// Same mathematics as tensor_kernel's collocation path (kern_tensor.cuh,
-// SURVEY.md Appendix B), different GPU mapping.  tensor_kernel gives each
-// thread one 1D pencil per stage, so every contraction stage passes its whole
-// field through shared memory: P+Q shared accesses per P*Q FMAs, which with a
-// 2-stage warp pipeline and 16 warps/SM left the FP64 pipe at ~53%
-// (profiles/r01/prof5_C3-Q3.ncu-rep: short-scoreboard and wait stalls).
-// Here a TEAM of Q threads owns a cell and each thread owns a whole 2D PLANE:
+// Same mathematics as tensor_kernel's direct path (kern_tensor.cuh, SURVEY.md
+// Appendix B), different GPU mapping.  tensor_kernel gives each thread one 1D
+// pencil per stage, so every contraction stage passes its whole field through
+// shared memory (P+Q shared accesses per P*Q FMAs); with 16 warps/SM that left
+// the FP64 pipe at ~53% (profiles/r01/prof5_C3-Q3.ncu-rep).  Here a TEAM of Q
+// threads owns a cell and the work is streamed over the z points c:
 //
-//   phase 1  thread j holds the dof plane u[i, j, k] (i = x, k = z):
-//            z- and x-contractions stay in registers
-//              Z  = B_z u          V0 = B_x Z          V1 = D_x Z
-//   transpose V0, V1 through shared memory (plane j -> plane a)
-//   phase 2  thread a holds V0[j, c], V1[j, c] for its x point a and walks the
-//            y rows b: u, d/dxi, d/deta at (a, b, c) by y-contractions,
-//            d/dzeta by the collocation derivative Dc along the row, the
-//            Laplacian flux, and the transposed y-contractions accumulated
-//            into W0, W1 (registers)
-//   transpose W0, W1 back (plane a -> plane j)
-//   phase 1' Zb = B_x^T W0 + D_x^T W1,  y = B_z^T Zb,  scatter (FP64 RED)
+//   phase 1  thread j < P holds the dof plane u[i, j, k] (i = x, k = z) in
+//            registers; for point column c it forms the z-contractions
+//            z0 = B_z u, z1 = D_z u (P values each) and the x-contractions
+//            V0 = B_x z0, V1 = D_x z0, V2 = B_x z1 (Q values each), written to
+//            a small shared column buffer T[field][a][j]
+//   phase 2  thread a < Q reads V*[a][j] and walks the y points b:
+//            d/dxi = B_y V1, d/deta = D_y V0, d/dzeta = B_y V2, the Laplacian
+//            flux at (a, b, c), and the transposed y-contractions back into
+//            W*[a][j] (written in place over its own V* slots)
+//   phase 1' thread j reads W*[a][j]: zb0 = B_x^T W0 + D_x^T W1,
+//            zb1 = B_x^T W2, and accumulates y[i][k] += B_z[c][k] zb0[i] +
+//            D_z[c][k] zb1[i] in registers; after the last column: scatter.
 //
-// Only the two transposes touch shared memory: 8 P Q^2 accesses per cell
-// against ~14 Q^4 FMAs.  The flux uses the adjugate form
-//   f = (w / |det J|) adj(J) adj(J)^T g_ref      (= |det J| w J^-1 J^-T g_ref)
-// with the trilinear Jacobian built per point from per-thread / per-row
-// factors (its columns are bilinear or linear in the point coordinates).
+// Nothing bigger than a column (3 P Q values per cell) ever sits in shared
+// memory and no thread holds more than a dof plane and its output plane, so
+// the kernel runs at low register pressure with many warps per SM.  The flux
+// uses the adjugate form
+//   f = (w / |det J|) adj(J) adj(J)^T g_ref      (= w |det J| J^-1 J^-T g_ref)
+// with the trilinear Jacobian built per point from per-column factors (its
+// columns are linear in eta along a y line).
 //
 // Teams are packed into warps (32 / Q cells per warp) and every warp runs its
 // own persistent loop over warp batches -- there are no CTA barriers.  The
 // gather is asynchronous (cp.async, LDGSTS): the map row and vertex ids of
 // batch n+2 and the u values and vertex coordinates of batch n+1 are copied
-// into shared memory while batch n computes, so the indirect gather never
-// occupies registers or stalls the arithmetic.
+// into shared memory while batch n computes.
 #pragma once
 #include "common.cuh"
 #include "kern_tensor.cuh"
@@ -67,27 +69,29 @@ constexpr int plane_conflict(int cs, int s, int nt, int tpw, int q) {
   }
   return worst;
 }
-struct PlanePick { int su, sa, cs; };
-// u plane  e = j*SU + k*P + i   (phase 1 reads: lanes vary j)
-// transpose e = a*SA + j*Q + c  (phase 1 writes / reads: lanes vary j; phase 2: a)
-// team stride CS.  Minimise the summed conflict degree, then the footprint.
+struct PlanePick { int s, cs; };
+// u plane e = j*SU + k*P + i, team stride CU (phase-1 reads: lanes vary j)
 template <int P, int Q>
-constexpr PlanePick plane_pick() {
-  constexpr int tpw = 32 / Q;
-  PlanePick best{P * P, P * Q, 0};
-  int bc = 1 << 30, bsz = 1 << 30;
+constexpr PlanePick plane_pick_u() {
+  PlanePick best{P * P, P * P * P};
+  int bc = 1 << 30;
   for (int su = P * P; su < P * P + 8; ++su)
-    for (int sa = P * Q; sa < P * Q + 8; ++sa) {
-      const int nb = P * su > Q * sa ? P * su : Q * sa;
-      for (int cs = nb; cs < nb + 16; ++cs) {
-        const int c = plane_conflict(cs, su, P, tpw, Q) + plane_conflict(cs, Q, P, tpw, Q) +
-                      plane_conflict(cs, sa, Q, tpw, Q);
-        if (c < bc || (c == bc && cs < bsz)) {
-          bc = c;
-          bsz = cs;
-          best = PlanePick{su, sa, cs};
-        }
-      }
+    for (int cs = P * su; cs < P * su + 16; ++cs) {
+      const int c = plane_conflict(cs, su, P, 32 / Q, Q);
+      if (c < bc) { bc = c; best = PlanePick{su, cs}; }
+    }
+  return best;
+}
+// column buffer e = f*Q*SA + a*SA + j, team stride CT (writes: lanes vary j
+// with stride 1; reads: lanes vary a with stride SA)
+template <int P, int Q>
+constexpr PlanePick plane_pick_t() {
+  PlanePick best{P, 3 * Q * P};
+  int bc = 1 << 30;
+  for (int sa = P; sa < P + 8; ++sa)
+    for (int cs = 3 * Q * sa; cs < 3 * Q * sa + 16; ++cs) {
+      const int c = plane_conflict(cs, 1, P, 32 / Q, Q) + plane_conflict(cs, sa, Q, 32 / Q, Q);
+      if (c < bc) { bc = c; best = PlanePick{sa, cs}; }
     }
   return best;
 }
@@ -96,14 +100,17 @@ template <int P, int Q>
 struct PlaneLayout {
   static constexpr int TPW = 32 / Q;  // cells (teams) per warp
   static constexpr int ND = P * P * P;
-  static constexpr PlanePick pick = plane_pick<P, Q>();
-  static constexpr int SU = pick.su, SA = pick.sa, CS = pick.cs, SJ = Q;
-  static constexpr int XS = 32;                     // 8 vertices x (x, y, z, pad)
+  static constexpr PlanePick pu = plane_pick_u<P, Q>(), pt = plane_pick_t<P, Q>();
+  static constexpr int SU = pu.s, CU = pu.cs, SA = pt.s, CT = pt.cs;
+  // 8 vertices x (x, y, z, pad); the cell stride is 2 (mod 16) words so the
+  // teams of a warp reading the same vertex of their own cells hit distinct banks
+  static constexpr int XS = 34;
   static constexpr int MS = ((ND + 8) + 3) / 4 * 4;  // map row + 8 vertex ids (int32)
-  // per warp: X[2][TPW][XS] doubles | U[2][TPW][CS] doubles | M[3][TPW][MS] int32
+  // per warp (doubles): X[2][TPW][XS] | U[TPW][CU] | T[2][TPW][CT] | M[3][TPW][MS] int32
   static constexpr int X0 = 0;
   static constexpr int U0 = X0 + 2 * TPW * XS;
-  static constexpr int M0 = U0 + 2 * TPW * CS;          // in doubles
+  static constexpr int T0 = U0 + ((TPW * CU + 1) & ~1);
+  static constexpr int M0 = T0 + ((2 * TPW * CT + 1) & ~1);
   static constexpr int WARP_DOUBLES = M0 + (3 * TPW * MS + 3) / 4 * 2;  // keeps 16-byte alignment
 };
 
@@ -111,8 +118,8 @@ template <int P, int Q, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   using L = PlaneLayout<P, Q>;
-  constexpr int TPW = L::TPW, ND = L::ND, CS = L::CS, SU = L::SU, SA = L::SA, SJ = L::SJ;
-  constexpr int MS = L::MS, XS = L::XS;
+  constexpr int TPW = L::TPW, ND = L::ND, SU = L::SU, CU = L::CU, SA = L::SA, CT = L::CT;
+  constexpr int MS = L::MS, XS = L::XS, SF = Q * SA;
   extern __shared__ double smem_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int T = lane / Q, t = lane % Q;
@@ -120,7 +127,8 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   const int Tc = in_team ? T : 0;
   double* wbase = smem_all + warp * L::WARP_DOUBLES;
   double* sX0 = wbase + L::X0;
-  double* sU0 = wbase + L::U0;
+  double* sU = wbase + L::U0 + Tc * CU;
+  double* sT0 = wbase + L::T0 + Tc * CT;
   int32_t* sM0 = reinterpret_cast<int32_t*>(wbase + L::M0);
 
   const int64_t ncs = p.mesh.nc_stride;
@@ -154,20 +162,19 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       if (v < 8) cp_async4(m + ND + v, p.mesh.vmap + v * ncs + c);
     }
   };
-  // u values and vertex coordinates of warp batch wb (its map in mslot) -> buffer buf
-  auto issue_data = [&](int wb, int mslot, int buf) {
+  // u values and vertex coordinates of warp batch wb (its map in mslot)
+  auto issue_data = [&](int wb, int mslot, int xbuf) {
     if (!valid(wb)) return;
     const int32_t* m = sM0 + (mslot * TPW + T) * MS;
-    double* su = sU0 + (buf * TPW + T) * CS;
 #pragma unroll
     for (int r = 0; r < (ND + Q - 1) / Q; ++r) {
       const int e = t + r * Q;
       if (e < ND) {
         const int i = e % P, j = (e / P) % P, k = e / (P * P);
-        cp_async8(su + j * SU + k * P + i, p.u + m[e]);
+        cp_async8(sU + j * SU + k * P + i, p.u + m[e]);
       }
     }
-    double* sx = sX0 + (buf * TPW + T) * XS;
+    double* sx = sX0 + (xbuf * TPW + T) * XS;
 #pragma unroll
     for (int r = 0; r < (16 + Q - 1) / Q; ++r) {
       const int e = t + r * Q;
@@ -188,134 +195,106 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     const int cur = it & 1;
     cp_wait_all();
     __syncwarp();
-    // next batch's gather and the map of the one after, in flight while this batch computes
-    issue_data(wb + GW, (it + 1) % 3, cur ^ 1);
-    issue_map(wb + 2 * GW, (it + 2) % 3);
-    cp_commit();
-
     const bool active = valid(wb);
-    double* sU = sU0 + (cur * TPW + Tc) * CS;
-    const double* sX = sX0 + (cur * TPW + Tc) * XS;
-    const int32_t* sM = sM0 + ((it % 3) * TPW + Tc) * MS;
+    const bool jt = active && t < P;  // phase-1 role (dof plane j = t)
 
-    // ---- phase 1: thread j = t < P holds the dof plane u[i, j, k] --------
-    double Z[P][Q];  // Z[i][c] = sum_k B[c][k] u[i][j][k]
-    if (active && t < P) {
-      double pu[P][P];
+    // dof plane u[i, j = t, k] -> registers; then the buffer takes the next batch
+    double pu[P][P];  // [k][i]
+    if (jt) {
 #pragma unroll
       for (int k = 0; k < P; ++k)
 #pragma unroll
         for (int i = 0; i < P; ++i) pu[k][i] = sU[t * SU + k * P + i];
-#pragma unroll
-      for (int i = 0; i < P; ++i)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < P; ++k) s = fma(p.B[c][k], pu[k][i], s);
-          Z[i][c] = s;
-        }
     }
     __syncwarp();
-    // V0 = B_x Z  -> transpose
-    if (active && t < P) {
-#pragma unroll
-      for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int i = 0; i < P; ++i) s = fma(p.B[a][i], Z[i][c], s);
-          sU[a * SA + t * SJ + c] = s;
-        }
-    }
-    __syncwarp();
-    double V0[P][Q], V1[P][Q];
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < P; ++j)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) V0[j][c] = sU[t * SA + j * SJ + c];
-    }
-    __syncwarp();
-    // V1 = D_x Z  -> transpose
-    if (active && t < P) {
-#pragma unroll
-      for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int i = 0; i < P; ++i) s = fma(p.D[a][i], Z[i][c], s);
-          sU[a * SA + t * SJ + c] = s;
-        }
-    }
-    __syncwarp();
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < P; ++j)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) V1[j][c] = sU[t * SA + j * SJ + c];
-    }
+    issue_data(wb + GW, (it + 1) % 3, cur ^ 1);
+    issue_map(wb + 2 * GW, (it + 2) % 3);
+    cp_commit();
 
-    // ---- phase 2: thread a = t, rows b, points c ---------------------------
-    double W0[P][Q], W1[P][Q];
+    const double* sX = sX0 + (cur * TPW + Tc) * XS;
+    auto X = [&](int vx, int vy, int vz, int d) { return sX[(vx + 2 * vy + 4 * vz) * 4 + d]; };
+    double yp[P][P];  // output plane y[i, j = t, k], [k][i]
 #pragma unroll
-    for (int j = 0; j < P; ++j)
+    for (int k = 0; k < P; ++k)
 #pragma unroll
-      for (int c = 0; c < Q; ++c) W0[j][c] = W1[j][c] = 0.0;
-    if (active) {
-      const double xi = p.x[t], wa = p.w[t];
-      auto X = [&](int vx, int vy, int vz, int d) { return sX[(vx + 2 * vy + 4 * vz) * 4 + d]; };
-      // d/deta column: linear in zeta; d/dzeta column: linear in eta (xi fixed)
-      double e0[3], de[3], f0[3], df[3];
+      for (int i = 0; i < P; ++i) yp[k][i] = 0.0;
+
+#pragma unroll 1
+    for (int c = 0; c < Q; ++c) {
+      double* sT = sT0 + (c & 1) * TPW * CT;
+      // ---- phase 1: column c of V0, V1, V2 from the dof plane ---------------
+      if (jt) {
+        double z0[P], z1[P];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double s0 = (X(0, 1, 0, d) - X(0, 0, 0, d)) * (1.0 - xi) + (X(1, 1, 0, d) - X(1, 0, 0, d)) * xi;
-        const double s1 = (X(0, 1, 1, d) - X(0, 0, 1, d)) * (1.0 - xi) + (X(1, 1, 1, d) - X(1, 0, 1, d)) * xi;
-        const double g0 = (X(0, 0, 1, d) - X(0, 0, 0, d)) * (1.0 - xi) + (X(1, 0, 1, d) - X(1, 0, 0, d)) * xi;
-        const double g1 = (X(0, 1, 1, d) - X(0, 1, 0, d)) * (1.0 - xi) + (X(1, 1, 1, d) - X(1, 1, 0, d)) * xi;
-        e0[d] = s0; de[d] = s1 - s0;
-        f0[d] = g0; df[d] = g1 - g0;
+        for (int i = 0; i < P; ++i) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            s0 = fma(p.B[c][k], pu[k][i], s0);
+            s1 = fma(p.D[c][k], pu[k][i], s1);
+          }
+          z0[i] = s0;
+          z1[i] = s1;
+        }
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            v0 = fma(p.B[a][i], z0[i], v0);
+            v1 = fma(p.D[a][i], z0[i], v1);
+            v2 = fma(p.B[a][i], z1[i], v2);
+          }
+          sT[a * SA + t] = v0;
+          sT[SF + a * SA + t] = v1;
+          sT[2 * SF + a * SA + t] = v2;
+        }
       }
+      __syncwarp();
+      // ---- phase 2: thread a = t, points (a, b, c) ----------------------------
+      if (active) {
+        double V0[P], V1[P], V2[P];
 #pragma unroll
-      for (int b = 0; b < Q; ++b) {
-        const double eta = p.x[b], wab = wa * p.w[b];
-        // d/dxi column: bilinear in (eta, zeta) -> linear in zeta along the row
-        double r0[3], dr[3], J2[3];
+        for (int j = 0; j < P; ++j) {
+          V0[j] = sT[t * SA + j];
+          V1[j] = sT[SF + t * SA + j];
+          V2[j] = sT[2 * SF + t * SA + j];
+        }
+        const double xi = p.x[t], zeta = p.x[c], wac = p.w[t] * p.w[c];
+        const double lx0 = 1.0 - xi, lz0 = 1.0 - zeta;
+        // d/dxi column: linear in eta; d/deta: constant on the line; d/dzeta: linear in eta
+        double g0[3], dg[3], J1[3], h0[3], dh[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const double q0 = (X(1, 0, 0, d) - X(0, 0, 0, d)) * (1.0 - eta) + (X(1, 1, 0, d) - X(0, 1, 0, d)) * eta;
-          const double q1 = (X(1, 0, 1, d) - X(0, 0, 1, d)) * (1.0 - eta) + (X(1, 1, 1, d) - X(0, 1, 1, d)) * eta;
-          r0[d] = q0; dr[d] = q1 - q0;
-          J2[d] = fma(eta, df[d], f0[d]);
+          const double q0 = (X(1, 0, 0, d) - X(0, 0, 0, d)) * lz0 + (X(1, 0, 1, d) - X(0, 0, 1, d)) * zeta;
+          const double q1 = (X(1, 1, 0, d) - X(0, 1, 0, d)) * lz0 + (X(1, 1, 1, d) - X(0, 1, 1, d)) * zeta;
+          g0[d] = q0; dg[d] = q1 - q0;
+          const double e0 = (X(0, 1, 0, d) - X(0, 0, 0, d)) * lx0 + (X(1, 1, 0, d) - X(1, 0, 0, d)) * xi;
+          const double e1 = (X(0, 1, 1, d) - X(0, 0, 1, d)) * lx0 + (X(1, 1, 1, d) - X(1, 0, 1, d)) * xi;
+          J1[d] = e0 * lz0 + e1 * zeta;
+          const double f0 = (X(0, 0, 1, d) - X(0, 0, 0, d)) * lx0 + (X(1, 0, 1, d) - X(1, 0, 0, d)) * xi;
+          const double f1 = (X(0, 1, 1, d) - X(0, 1, 0, d)) * lx0 + (X(1, 1, 1, d) - X(1, 1, 0, d)) * xi;
+          h0[d] = f0; dh[d] = f1 - f0;
         }
-        double uq[Q];
+        double W0[P], W1[P], W2[P];
 #pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double s = 0.0;
+        for (int j = 0; j < P; ++j) W0[j] = W1[j] = W2[j] = 0.0;
 #pragma unroll
-          for (int j = 0; j < P; ++j) s = fma(p.B[b][j], V0[j][c], s);
-          uq[c] = s;
-        }
-        double fz[Q];
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
+        for (int b = 0; b < Q; ++b) {
+          const double eta = p.x[b];
           double gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            gx = fma(p.B[b][j], V1[j][c], gx);
-            gy = fma(p.D[b][j], V0[j][c], gy);
+            gx = fma(p.B[b][j], V1[j], gx);
+            gy = fma(p.D[b][j], V0[j], gy);
+            gz = fma(p.B[b][j], V2[j], gz);
           }
-#pragma unroll
-          for (int e = 0; e < Q; ++e) gz = fma(p.Dc[c][e], uq[e], gz);
-          const double zeta = p.x[c];
           double J[3][3];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            J[d][0] = fma(zeta, dr[d], r0[d]);
-            J[d][1] = fma(zeta, de[d], e0[d]);
-            J[d][2] = J2[d];
+            J[d][0] = fma(eta, dg[d], g0[d]);
+            J[d][1] = J1[d];
+            J[d][2] = fma(eta, dh[d], h0[d]);
           }
           // adjugate (J^-1 = adj / det, rows = reference directions)
           const double a00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
@@ -328,83 +307,57 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wab * p.w[c]) / fabs(det);
-          // v = adj^T g (physical gradient * det), f = s adj v
+          const double s = (wac * p.w[b]) / fabs(det);
+          // v = adj^T g (= det * physical gradient), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;
           const double v2 = a02 * gx + a12 * gy + a22 * gz;
           const double fx = s * (a00 * v0 + a01 * v1 + a02 * v2);
           const double fy = s * (a10 * v0 + a11 * v1 + a12 * v2);
-          fz[c] = s * (a20 * v0 + a21 * v1 + a22 * v2);
+          const double fz = s * (a20 * v0 + a21 * v1 + a22 * v2);
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            W1[j][c] = fma(p.B[b][j], fx, W1[j][c]);
-            W0[j][c] = fma(p.D[b][j], fy, W0[j][c]);
+            W1[j] = fma(p.B[b][j], fx, W1[j]);
+            W0[j] = fma(p.D[b][j], fy, W0[j]);
+            W2[j] = fma(p.B[b][j], fz, W2[j]);
           }
         }
-        // Dc^T along the row for the zeta flux, then B_y^T
 #pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          double tz = 0.0;
-#pragma unroll
-          for (int e = 0; e < Q; ++e) tz = fma(p.Dc[e][c], fz[e], tz);
-#pragma unroll
-          for (int j = 0; j < P; ++j) W0[j][c] = fma(p.B[b][j], tz, W0[j][c]);
+        for (int j = 0; j < P; ++j) {  // in place over this thread's V slots
+          sT[t * SA + j] = W0[j];
+          sT[SF + t * SA + j] = W1[j];
+          sT[2 * SF + t * SA + j] = W2[j];
         }
       }
-    }
-    __syncwarp();  // V1 reads done: the buffer takes W0
-    if (active) {
+      __syncwarp();
+      // ---- phase 1': x^T then z^T into the output plane -----------------------
+      if (jt) {
+        double zb0[P], zb1[P];
 #pragma unroll
-      for (int j = 0; j < P; ++j)
+        for (int i = 0; i < P; ++i) zb0[i] = zb1[i] = 0.0;
 #pragma unroll
-        for (int c = 0; c < Q; ++c) sU[t * SA + j * SJ + c] = W0[j][c];
-    }
-    __syncwarp();
-    double Zb[P][Q];
-    if (active && t < P) {
+        for (int a = 0; a < Q; ++a) {
+          const double w0 = sT[a * SA + t], w1 = sT[SF + a * SA + t], w2 = sT[2 * SF + a * SA + t];
 #pragma unroll
-      for (int i = 0; i < P; ++i)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) Zb[i][c] = 0.0;
-#pragma unroll
-      for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          const double w = sU[a * SA + t * SJ + c];
-#pragma unroll
-          for (int i = 0; i < P; ++i) Zb[i][c] = fma(p.B[a][i], w, Zb[i][c]);
+          for (int i = 0; i < P; ++i) {
+            zb0[i] = fma(p.B[a][i], w0, zb0[i]);
+            zb0[i] = fma(p.D[a][i], w1, zb0[i]);
+            zb1[i] = fma(p.B[a][i], w2, zb1[i]);
+          }
         }
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+          for (int i = 0; i < P; ++i) yp[k][i] = fma(p.B[c][k], zb0[i], fma(p.D[c][k], zb1[i], yp[k][i]));
+      }
     }
-    __syncwarp();
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < P; ++j)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) sU[t * SA + j * SJ + c] = W1[j][c];
-    }
-    __syncwarp();
-    if (active && t < P) {
-#pragma unroll
-      for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int c = 0; c < Q; ++c) {
-          const double w = sU[a * SA + t * SJ + c];
-#pragma unroll
-          for (int i = 0; i < P; ++i) Zb[i][c] = fma(p.D[a][i], w, Zb[i][c]);
-        }
-      // y[i, j, k] = sum_c B[c][k] Zb[i][c]; scatter
+    if (jt) {
+      const int32_t* sM = sM0 + ((it % 3) * TPW + T) * MS;
 #pragma unroll
       for (int k = 0; k < P; ++k)
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int c = 0; c < Q; ++c) s = fma(p.B[c][k], Zb[i][c], s);
-          scatter_add(p.y, sM[i + P * t + P * P * k], s);
-        }
+        for (int i = 0; i < P; ++i) scatter_add(p.y, sM[i + P * t + P * P * k], yp[k][i]);
     }
-    __syncwarp();  // buffers of this batch free for the batch after next
   }
   cp_wait_all();
 }
@@ -412,5 +365,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 }  // namespace fe
 
 // registry hook (plan.cu): PLV(degree, P, Q, WARPS, MINB)
-#define FE_PLANE_VARIANTS                                                                  \
-  PLV(1, 2, 2, 4, 1), PLV(2, 3, 3, 4, 1), PLV(3, 4, 4, 4, 1),
+// C3-Q3 (P = Q = 4) and C3-Q4 (P = Q = 5); Q2 uses the whole-plane-transpose
+// variant (kern_plane1.cuh), Q1 the thread-per-cell quad_const_tensor kernel,
+// Q5/Q6 the pencil team kernel (profiles/r01/sweep_plane.txt)
+#define FE_PLANE_VARIANTS PLV(3, 4, 4, 4, 1), PLV(4, 5, 5, 4, 1),

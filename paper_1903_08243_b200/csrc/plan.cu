@@ -12,10 +12,12 @@
 #include <string>
 #include <algorithm>
 #include <vector>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kern_affine.cuh"
 #include "kern_plane.cuh"
+#include "kern_plane1.cuh"
 #include "kern_quad.cuh"
 #include "kern_tensor.cuh"
 #include "kern_dmma.cuh"
@@ -528,10 +530,15 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 }
 
 // plane-per-thread scalar Laplacian on hexahedra (kern_plane.cuh)
-template <int P, int Q, int WARPS, int MINB>
+template <int P, int Q, int WARPS, int MINB, bool V1>
 int plane_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
-  using L = PlaneLayout<P, Q>;
+  using L = std::conditional_t<V1, Plane1Layout<P, Q>, PlaneLayout<P, Q>>;
+  const void* kfn;
+  if constexpr (V1)
+    kfn = (const void*)plane1_kernel<P, Q, WARPS, MINB>;
+  else
+    kfn = (const void*)plane_kernel<P, Q, WARPS, MINB>;
   TP* hp = new TP();
   if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
     delete hp;
@@ -540,19 +547,17 @@ int plane_prepare(fe_plan* p) {
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
   p->tables_bytes = (size_t)WARPS * L::WARP_DOUBLES * sizeof(double);
-  CUDA_TRY(cudaFuncSetAttribute(plane_kernel<P, Q, WARPS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)p->tables_bytes));
+  CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
   p->cells_per_block = WARPS * L::TPW;
   int dev = 0, sms = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plane_kernel<P, Q, WARPS, MINB>, WARPS * 32,
-                                                         p->tables_bytes));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, WARPS * 32, p->tables_bytes));
   p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
   return FE_OK;
 }
 
-template <int P, int Q, int WARPS, int MINB>
+template <int P, int Q, int WARPS, int MINB, bool V1>
 int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                  const double*, const double*, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
@@ -569,7 +574,10 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   const int cpb = p->cells_per_block;
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
-  plane_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
+  if constexpr (V1)
+    plane1_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
+  else
+    plane_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -592,7 +600,10 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
    tensor_prepare<FORM, DIM, P, Q, MINB, true>, tensor_launch<FORM, DIM, P, Q, MINB, true>}
 #define PLV(K, P, Q, WARPS, MINB)                                                            \
   {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 22, "sum_factorised_plane",   \
-   WARPS * 32, plane_prepare<P, Q, WARPS, MINB>, plane_launch<P, Q, WARPS, MINB>}
+   WARPS * 32, plane_prepare<P, Q, WARPS, MINB, false>, plane_launch<P, Q, WARPS, MINB, false>}
+#define PL1V(K, P, Q, WARPS, MINB)                                                           \
+  {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 23, "sum_factorised_plane_t",  \
+   WARPS * 32, plane_prepare<P, Q, WARPS, MINB, true>, plane_launch<P, Q, WARPS, MINB, true>}
 #define ETPV(FORM, CELL, DIM, K, ND)                                                         \
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
@@ -689,6 +700,7 @@ static const Variant kVariants[] = {
     QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
     FE_TENSOR_VARIANTS
     FE_PLANE_VARIANTS
+    FE_PLANE1_VARIANTS
     FE_DMMA_VARIANTS
 };
 
@@ -776,6 +788,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 12 && (p->qw_aux.empty() || getenv("FE_NO_SPLIT"))) continue;  // split needs the aux rule
     if (v.priority == 25 && getenv("FE_NO_QCT")) continue;  // experiments: team kernel instead
     if (v.priority == 22 && getenv("FE_NO_PLANE")) continue;  // experiments: pencil team kernel
+    if (v.priority == 23 && getenv("FE_NO_PLANE1")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;

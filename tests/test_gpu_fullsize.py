@@ -52,7 +52,7 @@ def _subrange_parity(prob, h, dev, coef, ncheck=2048):
     return fo.rel_l2(y.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("name", ["C2-P4", "C3-Q6", "C4-quad-Q4", "C4-hex-Q3"])
+@pytest.mark.parametrize("name", ["C2-P4", "C3-Q3", "C3-Q6", "C4-quad-Q4", "C4-hex-Q3"])
 def test_full_size_symmetry_linearity_and_parity(name):
     import torch
     prob, h, A, dev, coef = _setup(name)
