@@ -65,17 +65,60 @@ FE_DEVICE void et_coeffs(const double (&X)[DIM + 1][DIM], double (&cm)[NM]) {
   }
 }
 
+// One thread's G consecutive cells are scattered together: contributions of
+// the group to the same dof are summed in registers first and one RED is
+// issued per distinct dof.  Consecutive cells of the structured meshes share
+// vertices, edges and faces (the 6 Kuhn tets of a cube touch 8 vertices
+// through 24 cell-vertex pairs), and at low degree the RED stream -- ~1.3
+// LSU cycles per lane on the issuing SM -- rivals the arithmetic.  The
+// duplicate search compares dof ids at run time (no mesh assumption); cells
+// past `end` carry unique negative ids and are never scattered.
+template <int G, int ND>
+FE_DEVICE void group_scatter(double* __restrict__ y, const int (&dof)[G][ND], double (&yv)[G][ND]) {
+  bool dup[G][ND];
+#pragma unroll
+  for (int r = 0; r < G; ++r)
+#pragma unroll
+    for (int i = 0; i < ND; ++i) dup[r][i] = false;
+#pragma unroll
+  for (int r = 1; r < G; ++r)
+#pragma unroll
+    for (int i = 0; i < ND; ++i)
+#pragma unroll
+      for (int r2 = 0; r2 < r; ++r2)
+#pragma unroll
+        for (int i2 = 0; i2 < ND; ++i2)
+          if (!dup[r2][i2] && dof[r][i] == dof[r2][i2]) {  // at most one live match
+            yv[r2][i2] += yv[r][i];
+            dup[r][i] = true;
+          }
+#pragma unroll
+  for (int r = 0; r < G; ++r)
+#pragma unroll
+    for (int i = 0; i < ND; ++i)
+      if (!dup[r][i] && dof[r][i] >= 0) scatter_add(y, dof[r][i], yv[r][i]);
+}
+
+// dof ids of a thread's G consecutive cells (lane l of a warp owns cells
+// base + l*G + r); cells past `end` get unique negative ids.  (Staging the
+// map columns through shared memory for coalescing measured slower.)
+template <int G, int ND>
+FE_DEVICE void group_dofs(const int32_t* __restrict__ map, int64_t cs, int base, int end, int lane,
+                          int (&dof)[G][ND]) {
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+    const int c = base + lane * G + r;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) dof[r][i] = c < end ? __ldg(map + i * cs + c) : -1 - (r * ND + i);
+  }
+}
+
 template <int FORM, int DIM, int ND>
-__global__ void __launch_bounds__(128)
-affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) {
+FE_DEVICE void et_cell(const ETParams<et_nmats<FORM, DIM>(), ND>& p, int cell, const int (&dof)[ND],
+                       double (&yv)[ND]) {
   constexpr int NM = et_nmats<FORM, DIM>();
   constexpr int NV = DIM + 1;
-  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
-  if (cell >= p.end) return;
   const int64_t cs = p.mesh.nc_stride;
-  int dof[ND];
-#pragma unroll
-  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
   double X[NV][DIM];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -97,8 +140,29 @@ affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) 
       for (int j = 0; j < ND; ++j) t = fma(p.S[m][i][j], w[j], t);
       yi = fma(cm[m], t, yi);
     }
-    scatter_add(p.y, dof[i], yi);
+    yv[i] = yi;
   }
+}
+
+template <int FORM, int DIM, int ND, int G>
+__global__ void __launch_bounds__(128)
+affine_et_kernel(const __grid_constant__ ETParams<et_nmats<FORM, DIM>(), ND> p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int base = p.start + (blockIdx.x * blockDim.x + warp * 32) * G;
+  if (base >= p.end) return;  // warp-uniform
+  int dof[G][ND];
+  group_dofs<G, ND>(p.mesh.map, p.mesh.nc_stride, base, p.end, lane, dof);
+  double yv[G][ND];
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+    if (dof[r][0] >= 0) {
+      et_cell<FORM, DIM, ND>(p, base + lane * G + r, dof[r], yv[r]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < ND; ++i) yv[r][i] = 0.0;
+    }
+  }
+  group_scatter<G, ND>(p.y, dof, yv);
 }
 
 // ---------------------------------------------------------------------------
@@ -124,15 +188,10 @@ struct SplitParams {
 };
 
 template <int FORM, int DIM, int ND, int NQS>
-__global__ void __launch_bounds__(128)
-affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
+FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, int cell, const int (&dof)[ND],
+                           double (&yv)[ND]) {
   constexpr int NV = DIM + 1;
-  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
-  if (cell >= p.end) return;
   const int64_t cs = p.mesh.nc_stride;
-  int dof[ND];
-#pragma unroll
-  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
   double X[NV][DIM];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -159,7 +218,6 @@ affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
       for (int c = 0; c < DIM; ++c) s = fma(Ji[a][c], Ji[b][c], s);
       K[a][b] = K[b][a] = ad * s;
     }
-  double yv[ND];
   // mass term
 #pragma unroll
   for (int i = 0; i < ND; ++i) {
@@ -194,8 +252,27 @@ affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
 #pragma unroll
       for (int a = 0; a < DIM; ++a) yv[j] = fma(p.dphi[q][j][a], f[a], yv[j]);
   }
+}
+
+template <int FORM, int DIM, int ND, int NQS, int G>
+__global__ void __launch_bounds__(128)
+affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int base = p.start + (blockIdx.x * blockDim.x + warp * 32) * G;
+  if (base >= p.end) return;  // warp-uniform
+  int dof[G][ND];
+  group_dofs<G, ND>(p.mesh.map, p.mesh.nc_stride, base, p.end, lane, dof);
+  double yv[G][ND];
 #pragma unroll
-  for (int i = 0; i < ND; ++i) scatter_add(p.y, dof[i], yv[i]);
+  for (int r = 0; r < G; ++r) {
+    if (dof[r][0] >= 0) {
+      split_cell<FORM, DIM, ND, NQS>(p, base + lane * G + r, dof[r], yv[r]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < ND; ++i) yv[r][i] = 0.0;
+    }
+  }
+  group_scatter<G, ND>(p.y, dof, yv);
 }
 
 // ---------------------------------------------------------------------------

@@ -253,6 +253,23 @@ static void element_matrices(const fe_plan* p, bool mass, bool grads, std::vecto
   }
 }
 
+// cells per thread of the affine kernels (group_scatter, kern_affine.cuh),
+// per measurement (profiles/r01/sweep_group.txt: C2-P1 40 -> 34 us at G = 2;
+// larger groups and every P2 grouping are slower -- registers and latency)
+#ifndef FE_GROUP_TET_P1
+#define FE_GROUP_TET_P1 2
+#endif
+#ifndef FE_GROUP_TET_P2
+#define FE_GROUP_TET_P2 1
+#endif
+#ifndef FE_GROUP_TRI_P2
+#define FE_GROUP_TRI_P2 1
+#endif
+constexpr int affine_group(int dim, int nd) {
+  return dim == 3 ? (nd == 4 ? FE_GROUP_TET_P1 : nd == 10 ? FE_GROUP_TET_P2 : 1)
+                  : (nd == 6 ? FE_GROUP_TRI_P2 : 1);
+}
+
 template <int FORM, int DIM, int ND>
 int et_prepare(fe_plan* p) {
   constexpr int NM = et_nmats<FORM, DIM>();
@@ -280,7 +297,9 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->start = start;
   hp->end = end;
   int n = end - start;
-  affine_et_kernel<FORM, DIM, ND><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  constexpr int G = affine_group(DIM, ND);
+  const int nt = (n + G - 1) / G;
+  affine_et_kernel<FORM, DIM, ND, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -353,7 +372,9 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   hp->start = start;
   hp->end = end;
   const int n = end - start;
-  affine_split_kernel<FORM, DIM, ND, NQS><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  constexpr int G = affine_group(DIM, ND);
+  const int nt = (n + G - 1) / G;
+  affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }

@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_all.log 2>&1; tail -1 gpurun_out/pytest_all.log
-tools/sweep_subset.sh C3-Q1 C3-Q2 C3-Q3 C3-Q4 C3-Q5 C3-Q6 > gpurun_out/sweep_c3.txt
+for lib in libfeb200 libfeb200_g3; do
+ export FE_LIB_PATH=$PWD/paper_1903_08243_b200/$lib.so
+ echo "== $lib"
+ python -m pytest tests/test_gpu_parity.py tests/test_gpu_slabs.py -m gpu -x -q 2>&1 | tail -1
+ tools/sweep_subset.sh C2-P1 C2-P1 C1
+done > gpurun_out/sweep_group2.txt 2>&1
