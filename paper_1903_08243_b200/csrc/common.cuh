@@ -39,12 +39,33 @@ FE_DEVICE void load_vertex(const double* __restrict__ coords, int v, double* x) 
   }
 }
 
+// 1/x without the IEEE division's slow-path subroutine: MUFU.RCP64H seed and
+// two Newton steps (relative error ~1 ulp for the normal, non-tiny |det J|
+// values it is used on).  The compiled 1.0/x is a BSSY/CALL region per use,
+// which fences instruction scheduling across the unrolled quadrature points
+// of a kernel.  Whether that helps is kernel-specific (it also frees ptxas to
+// hoist more work and raise register pressure), so every caller picks per
+// kernel variant from measurement (profiles/r01/sweep_rcp.txt).
+FE_DEVICE double rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+template <bool FAST>
+FE_DEVICE double recip(double x) {
+  if constexpr (FAST) return rcp(x);
+  else return 1.0 / x;
+}
+
 // determinant and inverse of a DIM x DIM matrix stored row-major J[a][b]
-template <int DIM>
+template <int DIM, bool FAST = false>
 FE_DEVICE double det_inv(const double (&J)[DIM][DIM], double (&Ji)[DIM][DIM]) {
   if constexpr (DIM == 2) {
     double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-    double r = 1.0 / det;
+    double r = recip<FAST>(det);
     Ji[0][0] = J[1][1] * r;  Ji[0][1] = -J[0][1] * r;
     Ji[1][0] = -J[1][0] * r; Ji[1][1] = J[0][0] * r;
     return det;
@@ -59,7 +80,7 @@ FE_DEVICE double det_inv(const double (&J)[DIM][DIM], double (&Ji)[DIM][DIM]) {
     double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
     double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
     double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-    double r = 1.0 / det;
+    double r = recip<FAST>(det);
     Ji[0][0] = a00 * r; Ji[0][1] = a01 * r; Ji[0][2] = a02 * r;
     Ji[1][0] = a10 * r; Ji[1][1] = a11 * r; Ji[1][2] = a12 * r;
     Ji[2][0] = a20 * r; Ji[2][1] = a21 * r; Ji[2][2] = a22 * r;

@@ -1,0 +1,148 @@
+// Component-pair kernel: 2D elasticity on quadrilaterals (C4-quad), sum
+// factorised in registers.
+//
+// Two lanes per cell, lane c owning displacement component c.  Each lane
+// holds its component's dof plane u_c[j][i] and output plane y_c[j][i] in
+// registers and streams over the point rows b:
+//   Y0 = B_y u_c, Y1 = D_y u_c                  (row b, P values each)
+//   per point a:  du_c/dxi = D_x Y0, du_c/deta = B_x Y1
+//                 gradient row (g_ref adj J)[c][:] (= det * physical); the
+//                 partner lane's row arrives by one shuffle pair, giving the
+//                 strain, the trace and the Lame stress row sigma[c][:]
+//                 flux row (w/|det|) sigma[c][:] adj^T -> Z0 += D_x^T f0,
+//                 Z1 += B_x^T f1
+//   y_c += B_y^T Z0 + D_y^T Z1
+// and finally scatters its P^2 values (FP64 RED).  No shared memory and no
+// barriers: the team-of-threads kernel (kern_tensor.cuh) kept only 4-5 of
+// every 6 lanes busy in its pencil stages and stalled on its shared-memory
+// round trips (profiles/r01/prof9_C4-quad-Q3.ncu-rep: FP64 pipe 50%).
+// The bilinear Jacobian's d/dxi column is constant along a point row, its
+// d/deta column linear in xi; mu and lambda are bilinear vertex fields.
+#pragma once
+#include "common.cuh"
+#include "kern_tensor.cuh"
+
+namespace fe {
+
+template <int FORM, int P, int Q, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
+  static_assert(FORM == FE_FORM_ELASTICITY_LAME || FORM == FE_FORM_ELASTICITY, "2D elasticity forms");
+  constexpr int NDS = P * P;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = gt & 1;
+  const int cell = p.start + (gt >> 1);
+  const unsigned live = __ballot_sync(0xffffffffu, cell < p.end);  // pairs live or die together
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+
+  const int32_t* mrow = p.maplex + (int64_t)cell * NDS;
+  int dof[NDS];
+#pragma unroll
+  for (int e = 0; e < NDS; ++e) dof[e] = __ldg(mrow + e);
+  double u[P][P];
+#pragma unroll
+  for (int j = 0; j < P; ++j)
+#pragma unroll
+    for (int i = 0; i < P; ++i) u[j][i] = __ldg(p.u + 2 * (int64_t)dof[j * P + i] + c);
+  double X[4][2], mv[4], lv[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int vid = __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<2>(p.mesh.coords, vid, X[v]);
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+      mv[v] = __ldg(p.mu + vid);
+      lv[v] = __ldg(p.lam + vid);
+    } else {
+      mv[v] = 0.5;
+      lv[v] = 0.0;
+    }
+  }
+  // d/deta column of J: linear in xi
+  double j1[2], d1[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    j1[d] = X[2][d] - X[0][d];
+    d1[d] = (X[3][d] - X[1][d]) - j1[d];
+  }
+  double y[P][P];
+#pragma unroll
+  for (int j = 0; j < P; ++j)
+#pragma unroll
+    for (int i = 0; i < P; ++i) y[j][i] = 0.0;
+
+#pragma unroll
+  for (int b = 0; b < Q; ++b) {
+    const double eta = p.x[b], le = 1.0 - eta, wb = p.w[b];
+    double Y0[P], Y1[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        s0 = fma(p.B[b][j], u[j][i], s0);
+        s1 = fma(p.D[b][j], u[j][i], s1);
+      }
+      Y0[i] = s0;
+      Y1[i] = s1;
+    }
+    // d/dxi column of J on this row; mu, lambda on the row: m0 + xi dm
+    double J0[2];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) J0[d] = (X[1][d] - X[0][d]) * le + (X[3][d] - X[2][d]) * eta;
+    const double det0 = J0[0] * j1[1] - j1[0] * J0[1], ddet = J0[0] * d1[1] - d1[0] * J0[1];
+    const double m0 = mv[0] * le + mv[2] * eta, dm = mv[1] * le + mv[3] * eta - m0;
+    const double l0 = lv[0] * le + lv[2] * eta, dl = lv[1] * le + lv[3] * eta - l0;
+    double Z0[P], Z1[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) Z0[i] = Z1[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      const double xi = p.x[a];
+      double gx = 0.0, gy = 0.0;  // du_c/dxi, du_c/deta
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        gx = fma(p.D[a][i], Y0[i], gx);
+        gy = fma(p.B[a][i], Y1[i], gy);
+      }
+      // adjugate form: with adj = det J^-1 = [[J11, -J01], [-J10, J00]] the
+      // flux tw sigma(G) J^-T equals (w / |det|) sigma(g adj) adj^T, so no
+      // inverse is formed; det is linear in xi along the row
+      const double J01 = fma(xi, d1[0], j1[0]), J11 = fma(xi, d1[1], j1[1]);
+      const double det = fma(xi, ddet, det0);
+      const double sc = (p.w[a] * wb) * recip<(P <= 4)>(fabs(det));  // fast at Q3, IEEE at Q4 (measured)
+      const double mu = sc * fma(xi, dm, m0), lam = sc * fma(xi, dl, l0);
+      // own row of g adj, the partner's by shuffle
+      const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
+      const double o0 = __shfl_xor_sync(live, g0, 1), o1 = __shfl_xor_sync(live, g1, 1);
+      const double tr = c ? (g1 + o0) : (g0 + o1);
+      // (G + G^T)[c][:] and the Lame stress row (the scale folded into mu, lambda)
+      const double s0 = g0 + (c ? o1 : g0), s1 = g1 + (c ? g1 : o0);
+      const double t0 = fma(mu, s0, c ? 0.0 : lam * tr), t1 = fma(mu, s1, c ? lam * tr : 0.0);
+      const double f0 = t0 * J11 - t1 * J01, f1 = t1 * J0[0] - t0 * J0[1];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        Z0[i] = fma(p.D[a][i], f0, Z0[i]);
+        Z1[i] = fma(p.B[a][i], f1, Z1[i]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+      for (int i = 0; i < P; ++i) y[j][i] = fma(p.B[b][j], Z0[i], fma(p.D[b][j], Z1[i], y[j][i]));
+  }
+#pragma unroll
+  for (int j = 0; j < P; ++j)
+#pragma unroll
+    for (int i = 0; i < P; ++i) scatter_add(p.y, 2 * (int64_t)dof[j * P + i] + c, y[j][i]);
+}
+
+}  // namespace fe
+
+// registry hook (plan.cu): PRV(form, degree, P, Q, MINB); C4-quad-Q3/Q4 (Q1/Q2:
+// the thread-per-cell quad_const_tensor kernel measured faster)
+#ifndef FE_PAIR_MINB
+#define FE_PAIR_MINB 1
+#endif
+#define FE_PAIR_VARIANTS                                                                     \
+  PRV(FE_FORM_ELASTICITY_LAME, 3, 4, 5, FE_PAIR_MINB), PRV(FE_FORM_ELASTICITY_LAME, 4, 5, 6, FE_PAIR_MINB),

@@ -368,4 +368,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 // C3-Q3 (P = Q = 4) and C3-Q4 (P = Q = 5); Q2 uses the whole-plane-transpose
 // variant (kern_plane1.cuh), Q1 the thread-per-cell quad_const_tensor kernel,
 // Q5/Q6 the pencil team kernel (profiles/r01/sweep_plane.txt)
-#define FE_PLANE_VARIANTS PLV(3, 4, 4, 4, 1), PLV(4, 5, 5, 4, 1),
+#ifndef FE_PLANE_MINB
+#define FE_PLANE_MINB 1
+#endif
+#define FE_PLANE_VARIANTS PLV(3, 4, 4, 4, FE_PLANE_MINB), PLV(4, 5, 5, 4, FE_PLANE_MINB),

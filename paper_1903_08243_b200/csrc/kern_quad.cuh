@@ -39,7 +39,7 @@ struct QuadTables {
 // reference gradients g[c][b] of u.  Outputs: cv[c] multiplies phi_j and
 // cg[c][b] multiplies dphi_j/dxi_b in the accumulation A[j][c] += ...
 // (kernels.py:202-252 for the reference forms).
-template <int FORM, int DIM, int VS>
+template <int FORM, int DIM, int VS, bool FAST = false>
 FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (&uq)[VS],
                          const double (&g)[VS][DIM], double mu, double lam,
                          double (&cv)[VS], double (&cg)[VS][DIM]) {
@@ -85,7 +85,7 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
       for (int c = 0; c < DIM; ++c)
 #pragma unroll
         for (int a = 0; a < DIM; ++a) F[c][a] = G[c][a] + (c == a ? 1.0 : 0.0);
-      double Jf = det_inv<DIM>(F, Fi);
+      double Jf = det_inv<DIM, FAST>(F, Fi);
       double ll = lam * log(Jf);
 #pragma unroll
       for (int c = 0; c < DIM; ++c)
@@ -300,7 +300,7 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
       for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
-    absdet = fabs(det_inv<DIM>(J, Ji));
+    absdet = fabs(det_inv<DIM, true>(J, Ji));
   } else if constexpr (DIM == 3) {
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -345,7 +345,7 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
           J[d][1] = fma(cf[2][d], xi, cf[1][d]);
         }
       }
-      absdet = fabs(det_inv<DIM>(J, Ji));
+      absdet = fabs(det_inv<DIM, true>(J, Ji));
     }
     const double tw = p.qw[q] * absdet;
     double uq[VS], g[VS][DIM];
@@ -377,7 +377,7 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
       }
     }
     double cv[VS], cg[VS][DIM];
-    pointwise<FORM, DIM, VS>(Ji, tw, uq, g, mu, lam, cv, cg);
+    pointwise<FORM, DIM, VS, true>(Ji, tw, uq, g, mu, lam, cv, cg);
 #pragma unroll
     for (int j = 0; j < ND; ++j)
 #pragma unroll

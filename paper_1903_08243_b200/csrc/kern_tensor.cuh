@@ -478,7 +478,9 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           J[d][1] = fma(xi, d1[d], j1[d]);
           if constexpr (DIM == 3) J[d][2] = fma(xi, d2[d], j2[d]);
         }
-        const double det = det_inv<DIM>(J, Ji);
+        // fast reciprocal except in the DIRECT (Q5/Q6) variants: measured
+        // (profiles/r01/sweep_rcp.txt)
+        const double det = det_inv<DIM, !DIRECT>(J, Ji);
         const double tw = (p.w[a] * wbc) * fabs(det);
         double mu = p.p0, lam = p.p1;
         if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
@@ -492,7 +494,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
           for (int d = 0; d < DIM; ++d) gq[comp][d] = g[comp][d][a];
         }
-        pointwise<FORM, DIM, VS>(Ji, tw, uq, gq, mu, lam, cv, cg);
+        pointwise<FORM, DIM, VS, !DIRECT>(Ji, tw, uq, gq, mu, lam, cv, cg);
 #pragma unroll
         for (int comp = 0; comp < VS; ++comp)
 #pragma unroll

@@ -18,6 +18,7 @@
 #include "kern_affine.cuh"
 #include "kern_plane.cuh"
 #include "kern_plane1.cuh"
+#include "kern_pair.cuh"
 #include "kern_quad.cuh"
 #include "kern_tensor.cuh"
 #include "kern_dmma.cuh"
@@ -603,6 +604,40 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   return FE_OK;
 }
 
+// component-pair 2D elasticity kernel (kern_pair.cuh)
+template <int FORM, int P, int Q, int MINB>
+int pair_prepare(fe_plan* p) {
+  using TP = TensorParams<Q, P>;
+  TP* hp = new TP();
+  if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
+    delete hp;
+    return rc;
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(TP);
+  return FE_OK;
+}
+
+template <int FORM, int P, int Q, int MINB>
+int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                const double* c0, const double* c1, cudaStream_t s) {
+  using TP = TensorParams<Q, P>;
+  TP* hp = static_cast<TP*>(p->host_params);
+  if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
+  hp->mesh = mesh_view(p);
+  hp->maplex = p->d_map_lex;
+  hp->u = u;
+  hp->y = y;
+  hp->mu = c0;
+  hp->lam = c1;
+  hp->start = start;
+  hp->end = end;
+  const int64_t nt = 2 * (int64_t)(end - start);
+  pair_kernel<FORM, P, Q, MINB><<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
 // ---------------------------------------------------------------------------
 // registry
 // ---------------------------------------------------------------------------
@@ -625,6 +660,9 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
 #define PL1V(K, P, Q, WARPS, MINB)                                                           \
   {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 23, "sum_factorised_plane_t",  \
    WARPS * 32, plane_prepare<P, Q, WARPS, MINB, true>, plane_launch<P, Q, WARPS, MINB, true>}
+#define PRV(FORM, K, P, Q, MINB)                                                             \
+  {FORM, FE_CELL_QUADRILATERAL, K, Q * Q, 26, "component_pair", 128, pair_prepare<FORM, P, Q, MINB>, \
+   pair_launch<FORM, P, Q, MINB>}
 #define ETPV(FORM, CELL, DIM, K, ND)                                                         \
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
@@ -722,6 +760,7 @@ static const Variant kVariants[] = {
     FE_TENSOR_VARIANTS
     FE_PLANE_VARIANTS
     FE_PLANE1_VARIANTS
+    FE_PAIR_VARIANTS
     FE_DMMA_VARIANTS
 };
 
@@ -810,6 +849,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 25 && getenv("FE_NO_QCT")) continue;  // experiments: team kernel instead
     if (v.priority == 22 && getenv("FE_NO_PLANE")) continue;  // experiments: pencil team kernel
     if (v.priority == 23 && getenv("FE_NO_PLANE1")) continue;
+    if (v.priority == 26 && getenv("FE_NO_PAIR")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;
