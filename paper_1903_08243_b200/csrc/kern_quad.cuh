@@ -260,7 +260,9 @@ struct QuadConstParams {
 
 // MINB: CTAs of 128 threads per SM the register allocation must allow
 // (chosen per variant from measurements)
-template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE, int MINB = 1>
+// UNR: quadrature-loop unroll (table entries become immediate constant-bank
+// operands instead of LDC loads; larger unrolls raise register pressure)
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE, int MINB = 1, int UNR = 1>
 __global__ void __launch_bounds__(128, MINB)
 quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFFINE> p) {
   constexpr int VS = form_vs(FORM, DIM);
@@ -325,7 +327,7 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
   for (int i = 0; i < ND; ++i)
 #pragma unroll
     for (int c = 0; c < VS; ++c) A[i][c] = 0.0;
-#pragma unroll 1
+#pragma unroll UNR
   for (int q = 0; q < NQ; ++q) {
     if constexpr (!AFFINE) {
       if constexpr (DIM == 3) {

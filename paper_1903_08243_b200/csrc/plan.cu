@@ -176,7 +176,7 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // quadrature kernel with tables in the parameter block (affine simplices)
 // ---------------------------------------------------------------------------
 
-template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1, int UNR = 1>
 int qc_prepare(fe_plan* p) {
   using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
   static_assert(sizeof(P) <= 32000, "parameter block too large");
@@ -207,7 +207,7 @@ int qc_prepare(fe_plan* p) {
   return FE_OK;
 }
 
-template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1>
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1, int UNR = 1>
 int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
               const double* c0, const double* c1, cudaStream_t s) {
   using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
@@ -222,7 +222,7 @@ int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -667,11 +667,11 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   {FORM, CELL, K, -1, 15, "element_tensor_patch", kPatchCells, etp_prepare<FORM, DIM, ND>,   \
    etp_launch<FORM, DIM, ND>}
 #define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
-  {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true>,    \
-   qc_launch<FORM, DIM, DIM + 1, ND, NQ, true>}
-#define QCT(FORM, CELL, DIM, NV, K, ND, NQ, MINB)                                            \
+  {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true, 1, 3>, \
+   qc_launch<FORM, DIM, DIM + 1, ND, NQ, true, 1, 3>}
+#define QCT(FORM, CELL, DIM, NV, K, ND, NQ, MINB, UNR)                                       \
   {FORM, CELL, K, NQ, 25, "quad_const_tensor", 128,                                          \
-   qc_prepare<FORM, DIM, NV, ND, NQ, false, MINB>, qc_launch<FORM, DIM, NV, ND, NQ, false, MINB>}
+   qc_prepare<FORM, DIM, NV, ND, NQ, false, MINB, UNR>, qc_launch<FORM, DIM, NV, ND, NQ, false, MINB, UNR>}
 #define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
   {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
    split_launch<FORM, DIM, ND, NQS>}
@@ -751,12 +751,13 @@ static const Variant kVariants[] = {
     SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
-    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1),
-    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 1),
-    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16, 4),
-    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1),
+    // (..., MINB, quadrature-loop unroll): per measurement, profiles/r01/sweep_unroll*.txt
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1, 8),
+    QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 1, 1),
+    QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 2, 9, 16, 4, 4),
+    QCT(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     FE_TENSOR_VARIANTS
     FE_PLANE_VARIANTS
     FE_PLANE1_VARIANTS
