@@ -287,7 +287,7 @@ def run_e2e(ops, steps):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_1903_08243_b200.harness import L2Flusher
+    from paper_1903_08243_b200.harness import L2Flusher, gpu_busy_wait
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -318,6 +318,7 @@ def run_ours(args):
             flush()
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in ops]
+            gpu_busy_wait()              # host submission latency stays outside the events
             for (e0, e1), op in zip(ev, ops):
                 e0.record(stream)
                 op["run"](op["u"], op["y"])

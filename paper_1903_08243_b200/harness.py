@@ -239,9 +239,20 @@ class L2Flusher:
         self.buf.fill_(1)
 
 
-def time_device(fn, trials=20, warmup=3, flush=True, stream=None):
+def gpu_busy_wait(seconds=50e-6):
+    """Queue a short spin kernel so the GPU is still busy while the host
+    enqueues the next event pair and launches: the events then bracket GPU
+    execution only, not host submission latency (~tens of us of Python and
+    driver time, which would otherwise dominate small configs such as C1)."""
+    import torch
+    torch.cuda._sleep(int(seconds * 2.0e9))
+
+
+def time_device(fn, trials=20, warmup=3, flush=True, stream=None, setup=None):
     """CUDA-event timing of ``fn()`` on ``stream`` with an optional L2 flush
-    outside each event pair.  Returns a list of seconds."""
+    outside each event pair; ``setup()`` (e.g. zeroing the output, as the
+    reference's bench.py:197-198 does outside its timer) runs before the
+    flush, untimed.  Returns a list of seconds."""
     import torch
     stream = stream or torch.cuda.current_stream()
     fl = L2Flusher() if flush else None
@@ -250,10 +261,13 @@ def time_device(fn, trials=20, warmup=3, flush=True, stream=None):
     torch.cuda.synchronize()
     times = []
     for _ in range(trials):
+        if setup:
+            setup()
         if fl:
             fl()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        gpu_busy_wait()
         e0.record(stream)
         fn()
         e1.record(stream)

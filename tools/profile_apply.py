@@ -43,12 +43,19 @@ def main():
         coef = (torch.as_tensor(prob.mu, device=dev), torch.as_tensor(prob.lam, device=dev))
     fn = lambda: h.apply(u, y, coef=coef, overwrite=True)
     if args.time:
-        ts = time_device(fn, trials=max(args.reps, 10), warmup=3)
+        # the reference's protocol (bench.py:196-200): accumulate into an
+        # output zeroed outside the timer; the overwrite path (zero-fill
+        # inside the timed call) is reported next to it
+        ts = time_device(lambda: h.apply(u, y, coef=coef), trials=max(args.reps, 10), warmup=3,
+                         setup=lambda: y.zero_())
+        tw = time_device(fn, trials=max(args.reps, 10), warmup=3)
         F = fe.flops_per_cell(prob.spec, prob.rule) * m.ncells
         troof = roofline_time(prob.spec, m, dm, prob.rule)
         print(json.dumps({"config": args.config, "kernel": h.info["kernel"], "ncells": m.ncells,
                           "best_ms": min(ts) * 1e3, "median_ms": float(np.median(ts)) * 1e3,
-                          "gflops": F / min(ts) / 1e9, "roofline_frac": troof / min(ts)}))
+                          "gflops": F / min(ts) / 1e9, "roofline_frac": troof / min(ts),
+                          "best_ms_with_zero_fill": min(tw) * 1e3,
+                          "roofline_frac_with_zero_fill": troof / min(tw)}))
     else:
         for _ in range(args.reps):
             fn()
