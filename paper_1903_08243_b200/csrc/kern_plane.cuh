@@ -114,7 +114,8 @@ struct PlaneLayout {
   static constexpr int WARP_DOUBLES = M0 + (3 * TPW * MS + 3) / 4 * 2;  // keeps 16-byte alignment
 };
 
-template <int P, int Q, int WARPS, int MINB>
+// CU: point-column loop unroll (per measurement: 2 at P = 4, 1 at P = 5)
+template <int P, int Q, int WARPS, int MINB, int CU>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   using L = PlaneLayout<P, Q>;
@@ -219,7 +220,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
       for (int i = 0; i < P; ++i) yp[k][i] = 0.0;
 
-#pragma unroll 1
+#pragma unroll CU
     for (int c = 0; c < Q; ++c) {
       double* sT = sT0 + (c & 1) * TPW * CT;
       // ---- phase 1: column c of V0, V1, V2 from the dof plane ---------------
@@ -364,11 +365,11 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
 }  // namespace fe
 
-// registry hook (plan.cu): PLV(degree, P, Q, WARPS, MINB)
+// registry hook (plan.cu): PLV(degree, P, Q, WARPS, MINB, CU)
 // C3-Q3 (P = Q = 4) and C3-Q4 (P = Q = 5); Q2 uses the whole-plane-transpose
 // variant (kern_plane1.cuh), Q1 the thread-per-cell quad_const_tensor kernel,
 // Q5/Q6 the pencil team kernel (profiles/r01/sweep_plane.txt)
 #ifndef FE_PLANE_MINB
 #define FE_PLANE_MINB 1
 #endif
-#define FE_PLANE_VARIANTS PLV(3, 4, 4, 4, FE_PLANE_MINB), PLV(4, 5, 5, 4, FE_PLANE_MINB),
+#define FE_PLANE_VARIANTS PLV(3, 4, 4, 4, FE_PLANE_MINB, 2), PLV(4, 5, 5, 4, FE_PLANE_MINB, 1),

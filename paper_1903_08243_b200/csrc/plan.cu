@@ -552,7 +552,7 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
 }
 
 // plane-per-thread scalar Laplacian on hexahedra (kern_plane.cuh)
-template <int P, int Q, int WARPS, int MINB, bool V1>
+template <int P, int Q, int WARPS, int MINB, bool V1, int CU = 1>
 int plane_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
   using L = std::conditional_t<V1, Plane1Layout<P, Q>, PlaneLayout<P, Q>>;
@@ -560,7 +560,7 @@ int plane_prepare(fe_plan* p) {
   if constexpr (V1)
     kfn = (const void*)plane1_kernel<P, Q, WARPS, MINB>;
   else
-    kfn = (const void*)plane_kernel<P, Q, WARPS, MINB>;
+    kfn = (const void*)plane_kernel<P, Q, WARPS, MINB, CU>;
   TP* hp = new TP();
   if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
     delete hp;
@@ -579,7 +579,7 @@ int plane_prepare(fe_plan* p) {
   return FE_OK;
 }
 
-template <int P, int Q, int WARPS, int MINB, bool V1>
+template <int P, int Q, int WARPS, int MINB, bool V1, int CU = 1>
 int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                  const double*, const double*, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
@@ -599,7 +599,7 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   if constexpr (V1)
     plane1_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
   else
-    plane_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
+    plane_kernel<P, Q, WARPS, MINB, CU><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -654,9 +654,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define TVD(FORM, CELL, DIM, K, P, Q, MINB)                                                  \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised_direct", 256,          \
    tensor_prepare<FORM, DIM, P, Q, MINB, true>, tensor_launch<FORM, DIM, P, Q, MINB, true>}
-#define PLV(K, P, Q, WARPS, MINB)                                                            \
+#define PLV(K, P, Q, WARPS, MINB, CU)                                                        \
   {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 22, "sum_factorised_plane",   \
-   WARPS * 32, plane_prepare<P, Q, WARPS, MINB, false>, plane_launch<P, Q, WARPS, MINB, false>}
+   WARPS * 32, plane_prepare<P, Q, WARPS, MINB, false, CU>, plane_launch<P, Q, WARPS, MINB, false, CU>}
 #define PL1V(K, P, Q, WARPS, MINB)                                                           \
   {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 23, "sum_factorised_plane_t",  \
    WARPS * 32, plane_prepare<P, Q, WARPS, MINB, true>, plane_launch<P, Q, WARPS, MINB, true>}

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-tools/sweep.sh > gpurun_out/sweep_v9.txt 2>&1
-python bench.py > gpurun_out/bench_v9.log 2>&1; tail -1 gpurun_out/bench_v9.log | cut -c1-600
+tools/sweep.sh > gpurun_out/sweep_v10.txt 2>&1
+for v in cu2 cu5; do echo "== $v"; FE_LIB_PATH=$PWD/paper_1903_08243_b200/libfeb200_$v.so tools/sweep_subset.sh C3-Q3 C3-Q4; done >> gpurun_out/sweep_v10.txt 2>&1
