@@ -114,8 +114,8 @@ struct PlaneLayout {
   static constexpr int WARP_DOUBLES = M0 + (3 * TPW * MS + 3) / 4 * 2;  // keeps 16-byte alignment
 };
 
-// CU: point-column loop unroll (per measurement: 2 at P = 4, 1 at P = 5)
-template <int P, int Q, int WARPS, int MINB, int CU>
+// COLU: point-column loop unroll (per measurement: 2 at P = 4, 1 at P = 5)
+template <int P, int Q, int WARPS, int MINB, int COLU>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
 plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   using L = PlaneLayout<P, Q>;
@@ -220,7 +220,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
       for (int i = 0; i < P; ++i) yp[k][i] = 0.0;
 
-#pragma unroll CU
+#pragma unroll COLU
     for (int c = 0; c < Q; ++c) {
       double* sT = sT0 + (c & 1) * TPW * CT;
       // ---- phase 1: column c of V0, V1, V2 from the dof plane ---------------
