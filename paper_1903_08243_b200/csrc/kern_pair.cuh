@@ -24,8 +24,13 @@
 
 namespace fe {
 
+#ifndef FE_PAIR_BLOCK
+#define FE_PAIR_BLOCK 32  // one warp per CTA: measured best (profiles/r01/sweep_warps.txt)
+#endif
+constexpr int kPairBlock = FE_PAIR_BLOCK;
+
 template <int FORM, int P, int Q, int MINB>
-__global__ void __launch_bounds__(128, MINB)
+__global__ void __launch_bounds__(kPairBlock, MINB)
 pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(FORM == FE_FORM_ELASTICITY_LAME || FORM == FE_FORM_ELASTICITY, "2D elasticity forms");
   constexpr int NDS = P * P;

@@ -372,4 +372,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #ifndef FE_PLANE_MINB
 #define FE_PLANE_MINB 1
 #endif
-#define FE_PLANE_VARIANTS PLV(3, 4, 4, 4, FE_PLANE_MINB, 2), PLV(4, 5, 5, 4, FE_PLANE_MINB, 1),
+#ifndef FE_PLANE_WARPS
+#define FE_PLANE_WARPS 4
+#endif
+#define FE_PLANE_VARIANTS PLV(3, 4, 4, FE_PLANE_WARPS, FE_PLANE_MINB, 2), PLV(4, 5, 5, FE_PLANE_WARPS, FE_PLANE_MINB, 1),

@@ -633,7 +633,7 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   hp->start = start;
   hp->end = end;
   const int64_t nt = 2 * (int64_t)(end - start);
-  pair_kernel<FORM, P, Q, MINB><<<(unsigned)((nt + 127) / 128), 128, 0, s>>>(*hp);
+  pair_kernel<FORM, P, Q, MINB><<<(unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s>>>(*hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
