@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-for v in w1 w2 w3; do echo "== $v"; FE_LIB_PATH=$PWD/paper_1903_08243_b200/libfeb200_$v.so tools/sweep_subset.sh C3-Q3 C3-Q4 C4-quad-Q3 C4-quad-Q4; done > gpurun_out/sweep_warps.txt 2>&1
-echo "== default" >> gpurun_out/sweep_warps.txt; tools/sweep_subset.sh C3-Q3 C3-Q4 C4-quad-Q3 C4-quad-Q4 >> gpurun_out/sweep_warps.txt 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v11.log 2>&1; tail -1 gpurun_out/pytest_v11.log
+tools/sweep.sh > gpurun_out/sweep_v11.txt 2>&1
+python bench.py > gpurun_out/bench_v11.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_v11.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_bench_v11.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v11.log 2>&1; tail -3 gpurun_out/smoke_v11.log
