@@ -106,9 +106,12 @@ typedef struct fe_element_desc {
   const double* x1d;       /* [q1d] 1D Gauss points on [0,1] */
   const int32_t* lex;      /* [(degree+1)^dim] local node index of tensor node (x fastest) */
   double params[4];        /* neohookean: mu, lambda */
-  /* optional auxiliary rule (else nq_aux = 0): the element's reference
-   * gradients on a lower-order rule exact for the stiffness integrand of an
-   * affine cell (degree 2k-2), used by the split Helmholtz/Laplacian kernel */
+  /* optional stiffness factorisation (else nq_aux = 0): weights w and
+   * reference gradients G such that int dphi_i/dxi_a dphi_j/dxi_b =
+   * sum_r w_r G[r][i][a] G[r][j][b] on the reference simplex -- a rule exact
+   * for degree 2k-2, or its minimal-rank form (m = dim P_{k-1} modes,
+   * elements.stiffness_modes).  Used by the split and modal DMMA
+   * Helmholtz/Laplacian kernels of affine simplices. */
   int32_t nq_aux;
   const double* qw_aux;    /* [nq_aux] */
   const double* dphi_aux;  /* [nq_aux][ndof][dim] */

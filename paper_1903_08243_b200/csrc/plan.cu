@@ -5,6 +5,7 @@
 // (form, cell, degree, rule) -- here chosen from a registry of sm_100a
 // template instantiations instead of generated C -- plus the bound mesh in
 // the GPU layout (element-batched SoA maps, padded coordinates).
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -463,6 +464,103 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   }
 }
 
+// modal two-stage DMMA kernel (kern_dmma.cuh): fragment-ordered G (stage 1,
+// B operand) and [G^T | Mhat] (stage 2, A operand) from the plan's stiffness
+// modes (qw_aux / dphi_aux, elements.stiffness_modes) and mass matrix.
+template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB>
+int dmma_modal_setup(fe_plan* p) {
+  auto kfn = dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB>;
+  CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
+  int dev = 0, sms = 0, per_sm = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kDmmaBlock, p->tables_bytes));
+  p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND, int NMODE>
+int dmma_modal_prepare(fe_plan* p) {
+  constexpr bool MASS = FORM == FE_FORM_HELMHOLTZ;
+  constexpr int KT = DmmaShape<ND>::KT, MT = DmmaShape<ND>::MT;
+  using MS = ModalShape<DIM, NMODE>;
+  constexpr int NJ = MS::NJ, TPL = MS::TPL, NSTEP = MS::NSTEP;
+  constexpr int S2 = NSTEP + (MASS ? KT : 0);
+  if ((int)p->qw_aux.size() != NMODE) return fail(FE_EUNSUPPORTED, "modal kernel needs %d stiffness modes", NMODE);
+  for (double w : p->qw_aux)
+    if (!(w >= 0.0)) return fail(FE_EINVAL, "stiffness modes need non-negative weights");
+  // G[r][i][a] = sqrt(w_r) dphi_aux[r][i][a]; column (lane-group c, slot li)
+  // holds mode r = c * TPL + li / DIM, direction a = li % DIM
+  auto G = [&](int c, int li, int dof) -> double {
+    const int r = c * TPL + li / DIM, a = li % DIM;
+    if (li >= DIM * TPL || r >= NMODE || dof >= ND) return 0.0;
+    return std::sqrt(p->qw_aux[r]) * p->dphi_aux[((size_t)r * ND + dof) * DIM + a];
+  };
+  std::vector<double> S;
+  if (MASS) element_matrices(p, true, false, S);
+  std::vector<double> T((size_t)(NJ * KT + S2 * MT) * 32, 0.0);
+  for (int j = 0; j < NJ; ++j)
+    for (int t = 0; t < KT; ++t)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int n = lane >> 2, k = 4 * t + (lane & 3);  // B[k][n], column 8j + n
+        T[((size_t)j * KT + t) * 32 + lane] = G(n >> 1, 2 * j + (n & 1), k);
+      }
+  double* A2 = T.data() + (size_t)NJ * KT * 32;
+  for (int s = 0; s < S2; ++s)
+    for (int mt = 0; mt < MT; ++mt)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int row = 8 * mt + (lane >> 2), c = lane & 3;  // A[row][k = c]
+        double v = 0.0;
+        if (s < NSTEP) {
+          v = G(c, s, row);
+        } else {
+          const int col = 4 * (s - NSTEP) + c;
+          if (row < ND && col < ND) v = S[(size_t)row * ND + col];
+        }
+        A2[((size_t)s * MT + mt) * 32 + lane] = v;
+      }
+  p->tables_bytes = T.size() * sizeof(double);
+  CUDA_TRY(cudaMalloc(&p->d_tables, p->tables_bytes));
+  CUDA_TRY(cudaMemcpy(p->d_tables, T.data(), p->tables_bytes, cudaMemcpyHostToDevice));
+  const char* env = getenv("FE_DMMA_CFG");
+  p->dmma_cfg = env ? atoi(env) : 1;
+  if (p->dmma_cfg < 0 || p->dmma_cfg > 3) p->dmma_cfg = 0;
+  switch (p->dmma_cfg) {
+    case 1: return dmma_modal_setup<FORM, DIM, ND, NMODE, 1, 2>(p);
+    case 2: return dmma_modal_setup<FORM, DIM, ND, NMODE, 2, 2>(p);
+    case 3: return dmma_modal_setup<FORM, DIM, ND, NMODE, 1, 1>(p);
+    default: return dmma_modal_setup<FORM, DIM, ND, NMODE, 2, 1>(p);
+  }
+}
+
+template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB>
+int dmma_modal_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_t s) {
+  const int ngroups = (n + 8 * NT - 1) / (8 * NT);
+  const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
+  const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
+  dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int ND, int NMODE>
+int dmma_modal_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                      const double*, const double*, cudaStream_t s) {
+  DmmaParams k;
+  k.mesh = mesh_view(p);
+  k.u = u;
+  k.y = y;
+  k.afrag = p->d_tables;
+  k.start = start;
+  k.end = end;
+  switch (p->dmma_cfg) {
+    case 1: return dmma_modal_run<FORM, DIM, ND, NMODE, 1, 2>(p, k, end - start, s);
+    case 2: return dmma_modal_run<FORM, DIM, ND, NMODE, 2, 2>(p, k, end - start, s);
+    case 3: return dmma_modal_run<FORM, DIM, ND, NMODE, 1, 1>(p, k, end - start, s);
+    default: return dmma_modal_run<FORM, DIM, ND, NMODE, 2, 1>(p, k, end - start, s);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // sum-factorised tensor-cell kernel
 // ---------------------------------------------------------------------------
@@ -648,6 +746,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define DMV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 20, "dmma_element_tensor", kDmmaBlock, dmma_prepare<FORM, DIM, ND>,    \
    dmma_launch<FORM, DIM, ND>}
+#define DMMV(FORM, CELL, DIM, K, ND, NMODE)                                                  \
+  {FORM, CELL, K, -1, 21, "dmma_modal", kDmmaBlock, dmma_modal_prepare<FORM, DIM, ND, NMODE>,  \
+   dmma_modal_launch<FORM, DIM, ND, NMODE>}
 #define TV(FORM, CELL, DIM, K, P, Q, MINB)                                                   \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised", 256,                 \
    tensor_prepare<FORM, DIM, P, Q, MINB, false>, tensor_launch<FORM, DIM, P, Q, MINB, false>}
@@ -748,9 +849,10 @@ static const Variant kVariants[] = {
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 1, 3, 4),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 2, 6, 9),
     SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
-    SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
+    SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 2, 10, 4),
+    SPV(FE_FORM_HELMHOLTZ, FE_CELL_TETRAHEDRON, 3, 3, 20, 10),
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 1, 4, 1),
-    SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 8),
+    SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 4),
     // (..., MINB, quadrature-loop unroll): per measurement, profiles/r01/sweep_unroll*.txt
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1, 8),
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
@@ -846,7 +948,12 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.cell == FE_CELL_HEXAHEDRON || v.cell == FE_CELL_QUADRILATERAL)
       if (v.priority >= 20 && p->q1d == 0) continue;  // tensor kernels need 1D factors
     if ((flags & 1u) && v.priority > 0) continue;                // FE_PLAN_GENERIC: quad kernel only
-    if (v.priority == 12 && (p->qw_aux.empty() || getenv("FE_NO_SPLIT"))) continue;  // split needs the aux rule
+    if (v.priority == 12 && (p->qw_aux.empty() || getenv("FE_NO_SPLIT"))) continue;  // split needs the modes
+    // modal DMMA likewise; at P1/P2 it measured 2.7x / 1.8x slower than the
+    // thread-per-cell split kernel (profiles/r01/sweep_modal2.txt), so only
+    // P3/P4 are registered
+    if (v.priority == 21 && (p->qw_aux.empty() || getenv("FE_NO_MODAL"))) continue;
+    if (v.priority == 20 && getenv("FE_NO_DMMA") && v.cell == FE_CELL_TETRAHEDRON) continue;  // experiments
     if (v.priority == 25 && getenv("FE_NO_QCT")) continue;  // experiments: team kernel instead
     if (v.priority == 22 && getenv("FE_NO_PLANE")) continue;  // experiments: pencil team kernel
     if (v.priority == 23 && getenv("FE_NO_PLANE1")) continue;

@@ -61,6 +61,7 @@ __all__ = [
     "operator_spec",
     "integrand_degree",
     "tensor_factors",
+    "stiffness_modes",
     "MAX_QUADRATURE_DEGREE",
 ]
 
@@ -479,6 +480,36 @@ def tensor_factors(element: ReferenceElement, rule: QuadratureRule) -> TensorFac
     lex = np.empty(p ** d, dtype=np.int32)
     lex[lin] = np.arange(len(lin), dtype=np.int32)
     return TensorFactors(B, D, wg / 2.0, x01, lex)
+
+
+def stiffness_modes(element: ReferenceElement, cell=None):
+    """Minimal-rank factorisation of the reference stiffness tensor of a
+    simplex element: tables (w, G) with m = dim P_{k-1} "modes" such that
+
+        S_ab[i][j] = int dphi_i/dxi_a dphi_j/dxi_b = sum_r w_r G[r,i,a] G[r,j,b]
+
+    (w = 1).  The reference gradients of P_k lie in P_{k-1}; G[:, :, a] are
+    their coefficients in an L2-orthonormal basis of P_{k-1}, obtained as the
+    rank-m SVD factor of the square-root-weighted gradient table on the rule
+    exact for degree 2k-2.  This is the reference's quadrature with the
+    smallest possible number of points (m instead of k^d: 4 vs 8 for P2
+    tetrahedra, 20 vs 64 for P4); the kernels that consume it treat the modes
+    exactly like quadrature points.  Exact on affine cells."""
+    cell = element.cell
+    if not cell.simplex:
+        raise ValueError("stiffness modes are defined for simplices")
+    k, d, nd = element.degree, cell.dim, element.ndof_scalar
+    rule = quadrature_rule(cell, max(2 * k - 2, 0))
+    grads = tabulate(element, rule).grads                     # [nq][nd][d]
+    Q = np.sqrt(rule.weights)[:, None] * grads.transpose(0, 2, 1).reshape(rule.npoints, d * nd)
+    _, sig, vt = np.linalg.svd(Q, full_matrices=False)
+    m = 1
+    for j in range(k - 1):
+        m = m * (d + k - 1 - j) // (j + 1)                    # C(k-1+d, d)
+    if len(sig) < m or (len(sig) > m and sig[m] > 1e-12 * sig[0]):
+        raise ValueError("stiffness tensor rank differs from dim P_{k-1}")
+    G = (sig[:m, None] * vt[:m]).reshape(m, d, nd).transpose(0, 2, 1)
+    return np.ones(m), np.ascontiguousarray(G)
 
 
 # ---------------------------------------------------------------------------

@@ -143,7 +143,14 @@ def flops_per_cell(spec: OperatorSpec, rule=None) -> int:
         et = 14 * nd * nd + 13 * nd + 80
         quad = 16 * nd * nq + 20 * nq + 80
         split = 12 * nd * k ** 3 + 15 * k ** 3 + 2 * nd * nd + 2 * nd + 80
-        return min(et, quad, split)
+        # "modal split" (added to the menu in round 1, lowering F as SURVEY
+        # App. B allows): the split algorithm on the m = dim P_{k-1} =
+        # k(k+1)(k+2)/6 stiffness modes of elements.stiffness_modes instead
+        # of the k^3 points -- 183 / 840 / 3,470 / 11,300 for k = 1..4
+        # (the frozen SURVEY values were 183 / 1,380 / 5,940 / 17,685)
+        m = k * (k + 1) * (k + 2) // 6
+        modal = 12 * nd * m + 15 * m + 2 * nd * nd + 2 * nd + 80
+        return min(et, quad, split, modal)
     if cell.kind == "hexahedron" and form == "laplacian_scalar":
         p, q = k + 1, rule.npoints_1d
         return 2 * _interp_sumfact(3, p, q) + 148 * q ** 3 + 36

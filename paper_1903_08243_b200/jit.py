@@ -37,7 +37,7 @@ import numpy as np
 
 from . import _lib
 from .elements import (OperatorSpec, QuadratureRule, integrand_degree, quadrature_rule,
-                       tabulate, tensor_factors)
+                       stiffness_modes, tabulate, tensor_factors)
 
 __all__ = ["Target", "PlanUnit", "emit_for", "compile_and_load", "GpuKernelHandle",
            "ToolchainError", "KernelError"]
@@ -146,12 +146,11 @@ class GpuKernelHandle:
         for i, v in enumerate(spec.params[:4]):
             d.params[i] = v
         d.nq_aux = 0
-        if cell.simplex and spec.form in ("helmholtz", "laplacian_scalar") and el.degree <= 2:
-            # stiffness integrand of an affine cell has degree 2k-2
-            aux = quadrature_rule(cell, 2 * el.degree - 2)
-            keep["qw_aux"] = np.ascontiguousarray(aux.weights, dtype=np.float64)
-            keep["dphi_aux"] = np.ascontiguousarray(tabulate(el, aux).grads, dtype=np.float64)
-            d.nq_aux = aux.npoints
+        if cell.simplex and spec.form in ("helmholtz", "laplacian_scalar"):
+            qw_aux, dphi_aux = stiffness_modes(el, cell)
+            keep["qw_aux"] = qw_aux
+            keep["dphi_aux"] = dphi_aux
+            d.nq_aux = qw_aux.shape[0]
             d.qw_aux = _dptr(keep["qw_aux"])
             d.dphi_aux = _dptr(keep["dphi_aux"])
         plan = ctypes.c_void_p()

@@ -62,3 +62,27 @@ def test_bench_configs_are_all_supported():
     for name, cfg in C.CONFIGS.items():
         spec = fe.operator_spec(cfg.form, cfg.cell, cfg.degree)
         fe.compile_and_load(fe.emit_for(spec, fe.Target(), fe.quadrature_rule(cfg.cell, cfg.qdegree)))
+
+
+# Kernel families that measured slower and are kept reachable for experiments
+# through the plan's environment switches (read at plan creation): each must
+# still match the oracle.
+ALTERNATIVES = [
+    ("helmholtz", "tetrahedron", 3, {"FE_NO_MODAL": "1"}, "dmma_element_tensor"),
+    ("helmholtz", "tetrahedron", 4, {"FE_NO_MODAL": "1"}, "dmma_element_tensor"),
+    ("helmholtz", "tetrahedron", 3, {"FE_NO_MODAL": "1", "FE_NO_DMMA": "1"}, "element_split"),
+    ("laplacian_scalar", "tetrahedron", 4, {"FE_NO_MODAL": "1"}, "dmma_element_tensor"),
+    ("helmholtz", "tetrahedron", 2, {"FE_NO_SPLIT": "1"}, "element_tensor"),
+    ("helmholtz", "tetrahedron", 4, {"FE_DMMA_CFG": "0"}, "dmma_modal"),
+    ("helmholtz", "tetrahedron", 3, {"FE_DMMA_CFG": "2"}, "dmma_modal"),
+    ("laplacian_scalar", "tetrahedron", 3, {"FE_DMMA_CFG": "3"}, "dmma_modal"),
+]
+
+
+@pytest.mark.parametrize("form,cell,k,env,kernel", ALTERNATIVES)
+def test_alternative_kernel_families_match_oracle(monkeypatch, form, cell, k, env, kernel):
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    got, err = _run(form, cell, k, False)
+    assert got == kernel
+    assert err <= 1e-12, (got, err)

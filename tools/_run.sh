@@ -1,5 +1,9 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v11.log 2>&1; tail -1 gpurun_out/pytest_v11.log
-tools/sweep.sh > gpurun_out/sweep_v11.txt 2>&1
-python bench.py > gpurun_out/bench_v11.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_v11.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_bench_v11.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v11.log 2>&1; tail -3 gpurun_out/smoke_v11.log
+for c in C2-P1 C2-P2; do
+  for cfg in 0 1 2 3; do
+    echo "dmma cfg=$cfg $(FE_NO_SPLIT=1 FE_DMMA_CFG=$cfg python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+  done
+  echo "split $(python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+  echo "split-g2 $(FE_LIB_PATH=paper_1903_08243_b200/libfeb200_g2.so python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+done > gpurun_out/sweep_modal2.txt 2>&1
+cut -c1-200 gpurun_out/sweep_modal2.txt
