@@ -88,6 +88,26 @@ FE_DEVICE double det_inv(const double (&J)[DIM][DIM], double (&Ji)[DIM][DIM]) {
   }
 }
 
+FE_DEVICE uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+FE_DEVICE void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+FE_DEVICE void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+FE_DEVICE void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+FE_DEVICE void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+FE_DEVICE void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// 8-byte copy that zero-fills the destination when !valid (src-size 0)
+FE_DEVICE void cp_async8_zfill(void* s, const void* g, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(s)), "l"(g),
+               "r"(valid ? 8 : 0) : "memory");
+}
+template <int N>
+FE_DEVICE void cp_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // y[idx] += v.  The global scatter P_e^T: FP64 RED at L2 (REDG.E.ADD.F64).
 FE_DEVICE void scatter_add(double* y, int64_t idx, double v) { atomicAdd(y + idx, v); }
 

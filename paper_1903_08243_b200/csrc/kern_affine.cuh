@@ -188,19 +188,8 @@ struct SplitParams {
 };
 
 template <int FORM, int DIM, int ND, int NQS>
-FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, int cell, const int (&dof)[ND],
-                           double (&yv)[ND]) {
-  constexpr int NV = DIM + 1;
-  const int64_t cs = p.mesh.nc_stride;
-  double X[NV][DIM];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
-    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
-  }
-  double w[ND];
-#pragma unroll
-  for (int i = 0; i < ND; ++i) w[i] = __ldg(p.u + dof[i]);
+FE_DEVICE void split_compute(const SplitParams<NQS, ND, DIM>& p, const double (&X)[DIM + 1][DIM],
+                             const double (&w)[ND], double (&yv)[ND]) {
   // geometry: K = |det J| J^-1 J^-T (symmetric)
   double J[DIM][DIM], Ji[DIM][DIM];
 #pragma unroll
@@ -229,7 +218,7 @@ FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, int cell, const in
     }
     yv[i] = s;
   }
-  // stiffness term on the low-order rule
+  // stiffness term on the modes / low-order rule
 #pragma unroll
   for (int q = 0; q < NQS; ++q) {
     double g[DIM];
@@ -254,6 +243,23 @@ FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, int cell, const in
   }
 }
 
+template <int FORM, int DIM, int ND, int NQS>
+FE_DEVICE void split_cell(const SplitParams<NQS, ND, DIM>& p, int cell, const int (&dof)[ND],
+                          double (&yv)[ND]) {
+  constexpr int NV = DIM + 1;
+  const int64_t cs = p.mesh.nc_stride;
+  double X[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    int vid = (p.mesh.vmap == p.mesh.map) ? dof[v] : __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid, X[v]);
+  }
+  double w[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) w[i] = __ldg(p.u + dof[i]);
+  split_compute<FORM, DIM, ND, NQS>(p, X, w, yv);
+}
+
 template <int FORM, int DIM, int ND, int NQS, int G>
 __global__ void __launch_bounds__(128)
 affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
@@ -273,6 +279,66 @@ affine_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p) {
     }
   }
   group_scatter<G, ND>(p.y, dof, yv);
+}
+
+// ---------------------------------------------------------------------------
+// Macro-cell variant (C2-P1).  At P1 the operator is bound by the global
+// gathers and the FP64 RED stream (4 REDs per tet), not by arithmetic.  When
+// the bound mesh consists of macro-cells -- MC consecutive cells whose dofs
+// follow one fixed local pattern over NU distinct dofs, e.g. the 6 Kuhn
+// tetrahedra of a cube over its 8 corners -- one thread takes a whole
+// macro-cell: it gathers the NU dofs and coordinates once, runs the MC cells
+// with compile-time local indices (all in registers, shared dofs summed in
+// registers) and issues NU REDs instead of MC*ND (8 instead of 24 per cube).
+// The pattern is verified for every macro-cell at bind time
+// (fe_plan_bind_mesh); meshes that do not follow it, and the ragged ends of
+// unaligned [start, end) ranges, run the per-cell kernel.
+// ---------------------------------------------------------------------------
+
+// the 6 Kuhn tetrahedra of a cube (mesh.kuhn_tets(): corner bit masks,
+// positively oriented) as a local pattern over the cube's 8 corners
+struct KuhnTetP1 {
+  static constexpr int MC = 6, NU = 8, ND = 4;
+  // rows {0,1,3,7} {0,1,7,5} {0,2,7,3} {0,2,6,7} {0,4,5,7} {0,4,7,6}, one nibble per entry
+  __host__ __device__ static constexpr int at(int t, int i) {
+    constexpr unsigned rows[6] = {0x7310u, 0x5710u, 0x3720u, 0x7620u, 0x7540u, 0x6740u};
+    return (int)((rows[t] >> (4 * i)) & 15u);
+  }
+};
+
+template <int FORM, int DIM, int ND, int NQS, class PAT>
+__global__ void __launch_bounds__(128)
+macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const int32_t* __restrict__ corner,
+                   int64_t mstride, int32_t m0, int32_t m1) {
+  static_assert(PAT::ND == ND && ND == DIM + 1, "macro pattern covers vertex dofs only");
+  constexpr int NU = PAT::NU, MC = PAT::MC;
+  const int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= m1) return;
+  int dof[NU];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) dof[k] = __ldg(corner + k * mstride + m);
+  double X[NU][DIM], w[NU], yl[NU];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    load_vertex<DIM>(p.mesh.coords, dof[k], X[k]);
+    w[k] = __ldg(p.u + dof[k]);
+    yl[k] = 0.0;
+  }
+#pragma unroll
+  for (int t = 0; t < MC; ++t) {
+    double Xt[DIM + 1][DIM], wt[ND], yt[ND];
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) Xt[i][a] = X[PAT::at(t, i)][a];
+      wt[i] = w[PAT::at(t, i)];
+    }
+    split_compute<FORM, DIM, ND, NQS>(p, Xt, wt, yt);
+#pragma unroll
+    for (int i = 0; i < ND; ++i) yl[PAT::at(t, i)] += yt[i];
+  }
+#pragma unroll
+  for (int k = 0; k < NU; ++k) scatter_add(p.y, dof[k], yl[k]);
 }
 
 // ---------------------------------------------------------------------------

@@ -40,18 +40,6 @@
 
 namespace fe {
 
-FE_DEVICE uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-FE_DEVICE void cp_async4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-FE_DEVICE void cp_async8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-FE_DEVICE void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-FE_DEVICE void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-FE_DEVICE void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ---- compile-time layout ------------------------------------------------------
 // Lanes are team-major (lane = T * Q + t).  Worst count of 8-byte words on one

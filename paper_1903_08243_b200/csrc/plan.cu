@@ -91,6 +91,12 @@ struct fe_plan {
   int32_t* d_patch_dofs = nullptr;
   uint16_t* d_pidx = nullptr;
   int patch_maxu = 0;
+  // macro-cells (kern_affine.cuh macro_split_kernel): pattern requested by
+  // the kernel family, SoA [NU][macro_stride] dofs of the verified mesh
+  std::vector<int32_t> macro_pat;  // [MC][ND] local macro-dof of each cell dof
+  int macro_mc = 0, macro_nu = 0;
+  int32_t* d_macro = nullptr;
+  int64_t macro_stride = 0;
   double* d_coords = nullptr;   // padded [nverts][cstride]
   const void* b_coords = nullptr;
   const void* b_map0 = nullptr;
@@ -360,6 +366,14 @@ int split_prepare(fe_plan* p) {
   std::memcpy(hp->M, S.data(), sizeof(hp->M));
   p->host_params = hp;
   p->host_params_bytes = sizeof(P);
+  if (DIM == 3 && ND == 4 && !getenv("FE_NO_MACRO")) {
+    using PAT = KuhnTetP1;
+    p->macro_mc = PAT::MC;
+    p->macro_nu = PAT::NU;
+    p->macro_pat.clear();
+    for (int t = 0; t < PAT::MC; ++t)
+      for (int i = 0; i < PAT::ND; ++i) p->macro_pat.push_back(PAT::at(t, i));
+  }
   return FE_OK;
 }
 
@@ -373,10 +387,30 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   hp->y = y;
   hp->start = start;
   hp->end = end;
-  const int n = end - start;
   constexpr int G = affine_group(DIM, ND);
-  const int nt = (n + G - 1) / G;
-  affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
+  auto per_cell = [&](int32_t a, int32_t b) {
+    if (a >= b) return;
+    hp->start = a;
+    hp->end = b;
+    const int nt = (b - a + G - 1) / G;
+    affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
+  };
+  if constexpr (DIM == 3 && ND == 4) {
+    if (p->d_macro) {
+      // whole macro-cells inside [start, end) on the macro kernel, ragged ends per cell
+      const int mc = KuhnTetP1::MC;
+      const int32_t m0 = (start + mc - 1) / mc, m1 = end / mc;
+      if (m0 < m1) {
+        macro_split_kernel<FORM, DIM, ND, NQS, KuhnTetP1>
+            <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+        per_cell(start, m0 * mc);
+        per_cell(m1 * mc, end);
+        CUDA_TRY(cudaGetLastError());
+        return FE_OK;
+      }
+    }
+  }
+  per_cell(start, end);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -922,6 +956,24 @@ __global__ void k_check_vertex_cols(const int32_t* __restrict__ map0, int nc, in
   if (v < 0 || v >= nverts) *flag = 1;
 }
 
+// macro-cell detection: corner dofs of macro-cell m from the first
+// occurrence of each local macro-dof, then every cell dof of the macro-cell
+// checked against the pattern (flag = 1 on any mismatch)
+__global__ void k_macro_detect(const int32_t* __restrict__ rm, int nd, int64_t nmacro, int mc, int nu,
+                               int npv, const int32_t* __restrict__ pat, const int32_t* __restrict__ first,
+                               int32_t* __restrict__ corner, int64_t mstride, int* flag) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= nmacro) return;
+  const int32_t* c = rm + m * mc * nd;
+  for (int k = 0; k < nu; ++k) {
+    const int f = first[k];
+    corner[k * mstride + m] = c[(f / npv) * nd + f % npv];
+  }
+  for (int t = 0; t < mc; ++t)
+    for (int i = 0; i < npv; ++i)
+      if (c[t * nd + i] != corner[pat[t * npv + i] * mstride + m]) *flag = 1;
+}
+
 namespace {
 
 void free_mesh(fe_plan* p) {
@@ -934,6 +986,8 @@ void free_mesh(fe_plan* p) {
   cudaFree(p->d_patch_off);
   cudaFree(p->d_patch_dofs);
   cudaFree(p->d_pidx);
+  cudaFree(p->d_macro);
+  p->d_macro = nullptr;
   p->d_patch_off = p->d_patch_dofs = nullptr;
   p->d_pidx = nullptr;
   p->d_coords = nullptr;
@@ -967,6 +1021,38 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
 }
 
 }  // namespace
+
+// Verify the macro-cell pattern of the plan's kernel family on the bound
+// mesh (every macro-cell) and keep the SoA corner dofs if it holds.
+static int build_macro(fe_plan* p, cudaStream_t s) {
+  const int mc = p->macro_mc, nu = p->macro_nu, npv = (int)p->macro_pat.size() / mc;
+  const int64_t nmacro = p->ncells / mc;
+  std::vector<int32_t> first(nu, -1);
+  for (int f = 0; f < mc * npv; ++f)
+    if (first[p->macro_pat[f]] < 0) first[p->macro_pat[f]] = f;
+  std::vector<int32_t> tab(p->macro_pat);
+  tab.insert(tab.end(), first.begin(), first.end());
+  int32_t* d_tab = nullptr;
+  int* d_flag = nullptr;
+  p->macro_stride = (nmacro + 31) / 32 * 32;
+  CUDA_TRY(cudaMalloc(&p->d_macro, (size_t)nu * p->macro_stride * sizeof(int32_t)));
+  CUDA_TRY(cudaMalloc(&d_tab, tab.size() * sizeof(int32_t)));
+  CUDA_TRY(cudaMalloc(&d_flag, sizeof(int)));
+  CUDA_TRY(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+  k_macro_detect<<<(unsigned)((nmacro + 255) / 256), 256, 0, s>>>(
+      p->d_map_rm, p->nd, nmacro, mc, nu, npv, d_tab, d_tab + mc * npv, p->d_macro, p->macro_stride, d_flag);
+  int h_flag = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(d_tab);
+  cudaFree(d_flag);
+  if (h_flag) {  // not a macro-cell mesh: the per-cell kernel runs
+    cudaFree(p->d_macro);
+    p->d_macro = nullptr;
+  }
+  return FE_OK;
+}
 
 // Patches of kPatchCells consecutive cells: sorted distinct dofs and the
 // patch-local index of every cell dof (host side, once per bound mesh).
@@ -1167,6 +1253,13 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     CUDA_TRY(cudaStreamSynchronize(s));
   }
   cudaFree(d_m1);
+  if (p->macro_mc > 0 && p->d_vmap == p->d_map && ncells >= p->macro_mc) {
+    int rc = build_macro(p, s);
+    if (rc) {
+      free_mesh(p);
+      return rc;
+    }
+  }
   if (p->wants_patch && ncells > 0) {
     int rc = build_patches(p, map0, dev, s);
     if (rc) {
@@ -1273,7 +1366,7 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
 int fe_plan_get_info(const fe_plan* p, fe_plan_info* info) {
   if (!p || !info) return fail(FE_EINVAL, "null argument");
   std::memset(info, 0, sizeof *info);
-  std::snprintf(info->kernel, sizeof info->kernel, "%s", p->var->name);
+  std::snprintf(info->kernel, sizeof info->kernel, "%s%s", p->var->name, p->d_macro ? "_macro" : "");
   info->threads_per_cell = 1;
   info->block = p->var->block;
   info->launches_per_apply = 1;

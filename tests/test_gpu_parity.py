@@ -76,14 +76,15 @@ def test_gpu_matches_oracle_on_config(name, n):
     assert fe.harness.rel_l2(out, ref) <= TOL, (name, h.info, fe.harness.rel_l2(out, ref))
 
 
-@pytest.mark.parametrize("name", ["C1", "C2-P2", "C2-P3", "C3-Q3", "C5"])
+@pytest.mark.parametrize("name", ["C1", "C2-P1", "C2-P2", "C2-P3", "C3-Q3", "C5"])
 def test_arbitrary_cell_ranges(name):
     """Any [start, end) must be honoured (the reference's batched targets get
     unaligned start wrong)."""
     prob = C.build_problem(C.get_config(name, 3 if name != "C1" else 8), seed=2)
     h = handle_for(prob.spec, prob.rule)
     nc = prob.mesh.ncells
-    for start, end in [(1, nc), (0, 1), (7, 7), (3, nc - 5), (nc - 1, nc)]:
+    for start, end in [(1, nc), (0, 1), (7, 7), (3, nc - 5), (nc - 1, nc), (6, 12), (5, 13),
+                       (12, nc)]:
         ref = oracle_fn(prob.spec, prob.mesh, prob.dofmap, prob.rule, prob.u, prob.mu, prob.lam,
                         start, end)
         out = np.zeros(prob.ndofs)
@@ -92,6 +93,39 @@ def test_arbitrary_cell_ranges(name):
             assert not out.any()
         else:
             assert fe.harness.rel_l2(out, ref) <= TOL, (start, end)
+
+
+def _macro_problem(seed):
+    prob = C.build_problem(C.get_config("C2-P1", 3), seed=seed)
+    h = handle_for(prob.spec, prob.rule)
+    return prob, h
+
+
+def test_macro_cell_path_is_detected_and_matches_oracle():
+    """The Kuhn-cube macro-cell kernel (C2-P1) is selected on the structured
+    tet mesh and agrees with the oracle."""
+    prob, h = _macro_problem(7)
+    out = np.zeros(prob.ndofs)
+    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out))
+    assert h.info["kernel"] == "element_split_macro"
+    ref = oracle_fn(prob.spec, prob.mesh, prob.dofmap, prob.rule, prob.u)
+    assert fe.harness.rel_l2(out, ref) <= TOL
+
+
+def test_macro_cell_path_falls_back_on_other_cell_orders():
+    """Cells that do not follow the macro pattern (here: a cell permutation)
+    must run the per-cell kernel, with the same result."""
+    prob, h = _macro_problem(8)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(prob.mesh.ncells)
+    mesh = fe.Mesh(prob.mesh.coords, np.ascontiguousarray(prob.mesh.cell2vert[perm]), prob.mesh.cell)
+    dm = fe.DofMap(np.ascontiguousarray(prob.dofmap.cell2dof[perm]), prob.dofmap.ndofs_global,
+                   prob.dofmap.element)
+    out = np.zeros(prob.ndofs)
+    h(0, mesh.ncells, fe.make_bindings(mesh, dm, prob.u, out))
+    assert h.info["kernel"] == "element_split"
+    ref = oracle_fn(prob.spec, mesh, dm, prob.rule, prob.u)
+    assert fe.harness.rel_l2(out, ref) <= TOL
 
 
 def test_accumulate_semantics():
