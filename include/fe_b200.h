@@ -57,7 +57,11 @@ enum {
   FE_FORM_ELASTICITY = 3,        /* eps(u):grad v, value_size = dim (reference) */
   FE_FORM_LAPLACIAN_SCALAR = 4,  /* grad u . grad v */
   FE_FORM_ELASTICITY_LAME = 5,   /* 2 mu eps(u):eps(v) + lambda div u div v */
-  FE_FORM_NEOHOOKEAN = 6         /* P(F) : grad v, P = mu(F - F^-T) + lambda ln J F^-T */
+  FE_FORM_NEOHOOKEAN = 6,        /* P(F) : grad v, P = mu(F - F^-T) + lambda ln J F^-T */
+  FE_FORM_NEOHOOKEAN_TANGENT = 7 /* dP(F)[grad du] : grad v at the state u (coef0, same
+                                    layout as u): mu dF + (mu - lambda ln J) F^-T dF^T F^-T
+                                    + lambda tr(F^-1 dF) F^-T, the Newton-step operator of
+                                    FE_FORM_NEOHOOKEAN */
 };
 
 enum {
@@ -142,7 +146,9 @@ int fe_plan_bind_mesh(fe_plan* plan, int32_t ncells, int32_t nverts, int64_t ngl
                       uint32_t ptr_flags, void* stream);
 
 /* Device apply on the bound mesh: dat0 (+)= sum over cells in [start,end).
- * coef0/coef1: device vertex fields mu/lambda for elasticity_lame, else NULL.
+ * coef0/coef1: device vertex fields mu/lambda for elasticity_lame; for
+ * neohookean_tangent coef0 is the state u (vs*nglobal doubles, the layout of
+ * dat2) and coef1 is NULL; else both NULL.
  * stream: a cudaStream_t (NULL = legacy default stream). */
 int fe_apply(const fe_plan* plan, int32_t start, int32_t end, double* dat0,
              const double* dat2, const double* coef0, const double* coef1,

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("FE_LIB_PATH") or os.path.join(HERE, "libfeb200.so")
 
 FORMS = {
     "mass": 0, "helmholtz": 1, "laplacian": 2, "elasticity": 3,
-    "laplacian_scalar": 4, "elasticity_lame": 5, "neohookean": 6,
+    "laplacian_scalar": 4, "elasticity_lame": 5, "neohookean": 6, "neohookean_tangent": 7,
 }
 CELLS = {"triangle": 0, "quadrilateral": 1, "tetrahedron": 2, "hexahedron": 3}
 

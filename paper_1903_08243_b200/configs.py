@@ -1,11 +1,13 @@
-"""BASELINE.json configurations C1..C5 and their seeded synthetic inputs.
+"""BASELINE.json configurations C1..C5 (+ C6, the SURVEY 8(f).1 tangent of
+C5) and their seeded synthetic inputs.
 
 Seeds: ``SeedSequence(seed).spawn(4)`` -> independent
 ``default_rng`` streams in the fixed order [jitter, u, mu, lambda];
 jitter moves interior vertices by U(-0.1h, 0.1h) per coordinate; u ~
 U(-1, 1) per dof (C5: 0.01 h U(-1, 1): the
 literal 0.05 U(-1,1) makes det F <= 0 at about half the quadrature points);
-mu, lambda ~ U(0.5, 2) per vertex (C4).
+mu, lambda ~ U(0.5, 2) per vertex (C4); a fifth stream draws the state u0 =
+0.01 h U(-1, 1) of the linearised C6 (spawn keeps the first four streams).
 
 The configs themselves are the BASELINE.json ``configs`` list; BASELINE has
 no public dataset, so seeded synthetic inputs with the stated shapes stand in.
@@ -62,6 +64,10 @@ def _configs():
                           (64, 64, 64), 2 * k + 2))
     out.append(Config("C5", "C5", "neohookean", "tetrahedron", 2, (128, 128, 128), 4,
                       jitter=False, u_scale="h", partitioned=True))
+    # the Newton-step companion of C5 -- the tangent action
+    # dF(u0; du) on the C5 mesh, state u0 = 0.01 h U(-1,1), du ~ U(-1,1)
+    out.append(Config("C6", "C6", "neohookean_tangent", "tetrahedron", 2, (128, 128, 128), 4,
+                      jitter=False, u_scale="unit", partitioned=True))
     return {c.name: c for c in out}
 
 
@@ -90,6 +96,15 @@ class Problem:
     u: np.ndarray
     mu: np.ndarray = None
     lam: np.ndarray = None
+    state: np.ndarray = None   # u0 of a linearised form (neohookean_tangent)
+
+    def coef(self):
+        """(coef0, coef1) host arrays for fe_apply, or None."""
+        if self.mu is not None:
+            return (self.mu, self.lam)
+        if self.state is not None:
+            return (self.state, None)
+        return None
 
     @property
     def nglobal(self) -> int:
@@ -105,8 +120,8 @@ def build_problem(cfg: Config, seed: int = 0) -> Problem:
     if cfg.qdegree < 2 * cfg.degree:
         raise ValueError("quadrature below the integrand's polynomial degree")
     rule = quadrature_rule(cfg.cell, cfg.qdegree)
-    r_jit, r_u, r_mu, r_lam = [np.random.default_rng(s)
-                               for s in np.random.SeedSequence(seed).spawn(4)]
+    r_jit, r_u, r_mu, r_lam, r_state = [np.random.default_rng(s)
+                                        for s in np.random.SeedSequence(seed).spawn(5)]
     mesh = build_mesh(cfg.cell, *cfg.n)
     if cfg.jitter:
         mesh = jitter_mesh(mesh, r_jit, 0.1)
@@ -115,11 +130,13 @@ def build_problem(cfg: Config, seed: int = 0) -> Problem:
     u = r_u.uniform(-1.0, 1.0, n)
     if cfg.u_scale == "h":
         u *= 0.01 / max(cfg.n)
-    mu = lam = None
+    mu = lam = state = None
     if spec.coefficient_fields:
         mu = r_mu.uniform(0.5, 2.0, mesh.nvertices)
         lam = r_lam.uniform(0.5, 2.0, mesh.nvertices)
-    return Problem(cfg, spec, rule, mesh, dm, u, mu, lam)
+    if spec.has_state:
+        state = r_state.uniform(-1.0, 1.0, n) * (0.01 / max(cfg.n))
+    return Problem(cfg, spec, rule, mesh, dm, u, mu, lam, state)
 
 
 def default_rule(spec):

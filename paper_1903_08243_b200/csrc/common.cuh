@@ -10,12 +10,15 @@ namespace fe {
 
 constexpr int form_vs(int form, int dim) {
   return (form == FE_FORM_LAPLACIAN || form == FE_FORM_ELASTICITY ||
-          form == FE_FORM_ELASTICITY_LAME || form == FE_FORM_NEOHOOKEAN) ? dim : 1;
+          form == FE_FORM_ELASTICITY_LAME || form == FE_FORM_NEOHOOKEAN ||
+          form == FE_FORM_NEOHOOKEAN_TANGENT) ? dim : 1;
 }
 constexpr bool form_needs_values(int form) {
   return form == FE_FORM_MASS || form == FE_FORM_HELMHOLTZ;
 }
 constexpr bool form_needs_grads(int form) { return form != FE_FORM_MASS; }
+// forms linearised at a state u0 (coef0): its reference gradient is interpolated too
+constexpr bool form_has_state(int form) { return form == FE_FORM_NEOHOOKEAN_TANGENT; }
 
 // Device-side view of a bound mesh, in the plan's internal layout.
 struct MeshView {

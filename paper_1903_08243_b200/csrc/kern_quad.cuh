@@ -36,13 +36,15 @@ struct QuadTables {
 
 // Pointwise flux at one quadrature point.  Inputs: inverse Jacobian Ji
 // (Ji[b][a] = dxi_b/dx_a), weight tw = w_q |det J|, values uq[c] and
-// reference gradients g[c][b] of u.  Outputs: cv[c] multiplies phi_j and
-// cg[c][b] multiplies dphi_j/dxi_b in the accumulation A[j][c] += ...
-// (kernels.py:202-252 for the reference forms).
+// reference gradients g[c][b] of u (and g0 of the state u0 for the
+// linearised forms).  Outputs: cv[c] multiplies phi_j and cg[c][b] multiplies
+// dphi_j/dxi_b in the accumulation A[j][c] += ... (kernels.py:202-252 for the
+// reference forms).
 template <int FORM, int DIM, int VS, bool FAST = false>
 FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (&uq)[VS],
                          const double (&g)[VS][DIM], double mu, double lam,
-                         double (&cv)[VS], double (&cg)[VS][DIM]) {
+                         double (&cv)[VS], double (&cg)[VS][DIM],
+                         const double (&g0)[VS][DIM] = {}) {
   if constexpr (form_needs_values(FORM)) {
 #pragma unroll
     for (int c = 0; c < VS; ++c) cv[c] = tw * uq[c];
@@ -94,6 +96,45 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
           double fit = Fi[a][c];  // F^{-T}[c][a]
           T[c][a] = mu * (F[c][a] - fit) + ll * fit;
         }
+    } else if constexpr (FORM == FE_FORM_NEOHOOKEAN_TANGENT) {
+      // dP = mu dF + (mu - lambda ln J) F^-T dF^T F^-T + lambda tr(F^-1 dF) F^-T
+      // with F = I + grad u0 (state), dF = grad du = G; F^-T dF^T F^-T = (M F^-1)^T
+      // for M = F^-1 dF
+      static_assert(VS == DIM, "vector form");
+      double F[DIM][DIM], Fi[DIM][DIM];
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double s = 0.0;
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) s += Ji[b][a] * g0[c][b];
+          F[c][a] = s + (c == a ? 1.0 : 0.0);
+        }
+      double Jf = det_inv<DIM, FAST>(F, Fi);
+      const double cc = mu - lam * log(Jf);
+      double M[DIM][DIM];
+      double tr = 0.0;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) s += Fi[a][c] * G[c][b];
+          M[a][b] = s;
+          if (a == b) tr += s;
+        }
+      const double lt = lam * tr;
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double s = 0.0;  // (M F^-1)[a][c] = (F^-T dF^T F^-T)[c][a]
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) s += M[a][b] * Fi[b][c];
+          T[c][a] = mu * G[c][a] + cc * s + lt * Fi[a][c];
+        }
     }
 #pragma unroll
     for (int c = 0; c < VS; ++c)
@@ -138,6 +179,13 @@ __global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
   for (int i = 0; i < ND; ++i)
 #pragma unroll
     for (int c = 0; c < VS; ++c) w[i][c] = __ldg(p.u + (int64_t)VS * dof[i] + c);
+  double w0[form_has_state(FORM) ? ND : 1][VS];
+  if constexpr (form_has_state(FORM)) {
+#pragma unroll
+    for (int i = 0; i < ND; ++i)
+#pragma unroll
+      for (int c = 0; c < VS; ++c) w0[i][c] = __ldg(p.mu + (int64_t)VS * dof[i] + c);
+  }
   double muv[NV], lamv[NV];
   if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
 #pragma unroll
@@ -207,8 +255,23 @@ __global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
         lam += gv * lamv[v];
       }
     }
+    double g0[VS][DIM];
+    if constexpr (form_has_state(FORM)) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) g0[c][b] = 0.0;
+#pragma unroll
+      for (int i = 0; i < ND; ++i)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+          double d = s_dphi[(q * ND + i) * DIM + b];
+#pragma unroll
+          for (int c = 0; c < VS; ++c) g0[c][b] += d * w0[i][c];
+        }
+    }
     double cv[VS], cg[VS][DIM];
-    pointwise<FORM, DIM, VS>(Ji, tw, uq, g, mu, lam, cv, cg);
+    pointwise<FORM, DIM, VS>(Ji, tw, uq, g, mu, lam, cv, cg, g0);
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
 #pragma unroll
@@ -284,6 +347,13 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
   for (int i = 0; i < ND; ++i)
 #pragma unroll
     for (int c = 0; c < VS; ++c) w[i][c] = __ldg(p.u + (int64_t)VS * dof[i] + c);
+  double w0[form_has_state(FORM) ? ND : 1][VS];
+  if constexpr (form_has_state(FORM)) {
+#pragma unroll
+    for (int i = 0; i < ND; ++i)
+#pragma unroll
+      for (int c = 0; c < VS; ++c) w0[i][c] = __ldg(p.mu + (int64_t)VS * dof[i] + c);
+  }
   double muv[NV], lamv[NV];
   if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
 #pragma unroll
@@ -378,8 +448,21 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
         lam = fma(p.gphi[q][v], lamv[v], lam);
       }
     }
+    double g0[VS][DIM];
+    if constexpr (form_has_state(FORM)) {
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) g0[c][b] = 0.0;
+#pragma unroll
+      for (int i = 0; i < ND; ++i)
+#pragma unroll
+        for (int c = 0; c < VS; ++c)
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) g0[c][b] = fma(p.dphi[q][i][b], w0[i][c], g0[c][b]);
+    }
     double cv[VS], cg[VS][DIM];
-    pointwise<FORM, DIM, VS, true>(Ji, tw, uq, g, mu, lam, cv, cg);
+    pointwise<FORM, DIM, VS, true>(Ji, tw, uq, g, mu, lam, cv, cg, g0);
 #pragma unroll
     for (int j = 0; j < ND; ++j)
 #pragma unroll

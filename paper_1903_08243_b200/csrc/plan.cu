@@ -804,6 +804,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
   {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true, 1, 3>, \
    qc_launch<FORM, DIM, DIM + 1, ND, NQ, true, 1, 3>}
+#define QCVU(FORM, CELL, DIM, K, ND, NQ, UNR)                                                \
+  {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true, 1, UNR>, \
+   qc_launch<FORM, DIM, DIM + 1, ND, NQ, true, 1, UNR>}
 #define QCT(FORM, CELL, DIM, NV, K, ND, NQ, MINB, UNR)                                       \
   {FORM, CELL, K, NQ, 25, "quad_const_tensor", 128,                                          \
    qc_prepare<FORM, DIM, NV, ND, NQ, false, MINB, UNR>, qc_launch<FORM, DIM, NV, ND, NQ, false, MINB, UNR>}
@@ -828,6 +831,7 @@ static const Variant kVariants[] = {
     TRI_FORM(FE_FORM_MASS), TRI_FORM(FE_FORM_HELMHOLTZ), TRI_FORM(FE_FORM_LAPLACIAN),
     TRI_FORM(FE_FORM_ELASTICITY), TRI_FORM(FE_FORM_LAPLACIAN_SCALAR),
     TRI_FORM(FE_FORM_ELASTICITY_LAME), TRI_FORM(FE_FORM_NEOHOOKEAN),
+    TRI_FORM(FE_FORM_NEOHOOKEAN_TANGENT),
     QUAD_FORM(FE_FORM_MASS), QUAD_FORM(FE_FORM_HELMHOLTZ), QUAD_FORM(FE_FORM_LAPLACIAN),
     QUAD_FORM(FE_FORM_ELASTICITY), QUAD_FORM(FE_FORM_LAPLACIAN_SCALAR),
     QUAD_FORM(FE_FORM_ELASTICITY_LAME),
@@ -844,6 +848,8 @@ static const Variant kVariants[] = {
     QV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
     QV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
     QV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
+    QV(FE_FORM_NEOHOOKEAN_TANGENT, FE_CELL_TETRAHEDRON, 3, 4, 1, 4, 8, true),
+    QV(FE_FORM_NEOHOOKEAN_TANGENT, FE_CELL_TETRAHEDRON, 3, 4, 2, 10, 27, true),
     // hexahedra: default rule nq = (k+2)^3, BASELINE C3 rule nq = (k+1)^3
     QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, false),
     QV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, false),
@@ -878,6 +884,10 @@ static const Variant kVariants[] = {
     ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 3, 20),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 2, 10, 27),
+    QCV(FE_FORM_NEOHOOKEAN_TANGENT, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
+    // tangent P2: state + increment + output (90 doubles) in registers; the
+    // point loop is not unrolled (UNR 3 spills)
+    QCVU(FE_FORM_NEOHOOKEAN_TANGENT, FE_CELL_TETRAHEDRON, 3, 2, 10, 27, 1),
     QCV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
     QCV(FE_FORM_ELASTICITY_LAME, FE_CELL_TETRAHEDRON, 3, 2, 10, 27),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TRIANGLE, 2, 1, 3, 4),
@@ -1112,7 +1122,7 @@ int fe_plan_create(fe_plan** out, const fe_element_desc* d, uint32_t flags) {
   if (!out || !d) return fail(FE_EINVAL, "null argument");
   *out = nullptr;
   if (d->cell < 0 || d->cell > 3) return fail(FE_EINVAL, "bad cell %d", d->cell);
-  if (d->form < 0 || d->form > 6) return fail(FE_EINVAL, "bad form %d", d->form);
+  if (d->form < 0 || d->form > FE_FORM_NEOHOOKEAN_TANGENT) return fail(FE_EINVAL, "bad form %d", d->form);
   fe_plan* p = new fe_plan();
   p->form = d->form;
   p->cell = d->cell;
@@ -1283,6 +1293,8 @@ int fe_apply(const fe_plan* p, int32_t start, int32_t end, double* y, const doub
   if (!y || !u) return fail(FE_EINVAL, "null dat0/dat2");
   if (p->form == FE_FORM_ELASTICITY_LAME && (!c0 || !c1))
     return fail(FE_EINVAL, "elasticity_lame needs the mu and lambda vertex fields");
+  if (p->form == FE_FORM_NEOHOOKEAN_TANGENT && !c0)
+    return fail(FE_EINVAL, "neohookean_tangent needs the state u (coef0)");
   cudaStream_t s = (cudaStream_t)stream;
   if (apply_flags & FE_APPLY_OVERWRITE)
     CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)p->vs * p->nglobal * sizeof(double), s));
@@ -1327,18 +1339,25 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   }
   const double* c0 = nullptr;
   const double* c1 = nullptr;
-  if (dat3 && dat4) {
-    if (p->cap_c < (size_t)p->nverts) {
+  // coefficient fields: mu/lambda vertex fields, or the state u of a
+  // linearised form (a dof field with the layout of dat2)
+  const bool state = p->form == FE_FORM_NEOHOOKEAN_TANGENT;
+  if (state ? dat3 != nullptr : (dat3 && dat4)) {
+    const size_t nc = state ? n : (size_t)p->nverts;
+    if (p->cap_c < nc) {
       cudaFree(p->d_c0);
       cudaFree(p->d_c1);
-      CUDA_TRY(cudaMalloc(&p->d_c0, p->nverts * sizeof(double)));
-      CUDA_TRY(cudaMalloc(&p->d_c1, p->nverts * sizeof(double)));
-      p->cap_c = p->nverts;
+      p->d_c0 = p->d_c1 = nullptr;
+      CUDA_TRY(cudaMalloc(&p->d_c0, nc * sizeof(double)));
+      CUDA_TRY(cudaMalloc(&p->d_c1, nc * sizeof(double)));
+      p->cap_c = nc;
     }
-    CUDA_TRY(cudaMemcpyAsync(p->d_c0, dat3, p->nverts * sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(p->d_c1, dat4, p->nverts * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(p->d_c0, dat3, nc * sizeof(double), cudaMemcpyHostToDevice, s));
     c0 = p->d_c0;
-    c1 = p->d_c1;
+    if (!state) {
+      CUDA_TRY(cudaMemcpyAsync(p->d_c1, dat4, nc * sizeof(double), cudaMemcpyHostToDevice, s));
+      c1 = p->d_c1;
+    }
   }
   // u first; then the operator runs (into a zeroed buffer) while the caller's
   // dat0 uploads on a second stream behind it; the accumulate dat0 + A(u)

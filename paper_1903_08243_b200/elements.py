@@ -78,6 +78,7 @@ OPERATOR_FORMS = (
     "laplacian_scalar",
     "elasticity_lame",
     "neohookean",
+    "neohookean_tangent",
 )
 
 
@@ -518,7 +519,7 @@ def stiffness_modes(element: ReferenceElement, cell=None):
 
 
 def form_value_size(form: str, dim: int) -> int:
-    if form in ("laplacian", "elasticity", "elasticity_lame", "neohookean"):
+    if form in ("laplacian", "elasticity", "elasticity_lame", "neohookean", "neohookean_tangent"):
         return dim
     return 1
 
@@ -557,6 +558,12 @@ class OperatorSpec:
         """Number of vertex-valued coefficient fields the form reads."""
         return 2 if self.form == "elasticity_lame" else 0
 
+    @property
+    def has_state(self) -> bool:
+        """Linearised form: reads the state u0 (a dof field with the layout
+        of u, binding ``dat3``) at which the residual is linearised."""
+        return self.form == "neohookean_tangent"
+
 
 NEOHOOKEAN_DEFAULT = (1.0, 10.0)  # mu, lambda (BASELINE.json configs[4])
 
@@ -568,7 +575,7 @@ def operator_spec(form: str, cell, degree: int, params=None) -> OperatorSpec:
     elem = reference_element(cell, degree, vs)
     geo = reference_element(cell, 1, cell.dim)
     if params is None:
-        params = NEOHOOKEAN_DEFAULT if form == "neohookean" else ()
+        params = NEOHOOKEAN_DEFAULT if form in ("neohookean", "neohookean_tangent") else ()
     return OperatorSpec(form, elem, geo, tuple(float(p) for p in params))
 
 

@@ -88,9 +88,10 @@ class BenchmarkRecord:
         return [getattr(self, c) for c in CSV_COLUMNS]
 
 
-def make_bindings(mesh: Mesh, dofmap: DofMap, u, out, mu=None, lam=None) -> dict:
+def make_bindings(mesh: Mesh, dofmap: DofMap, u, out, mu=None, lam=None, state=None) -> dict:
     """Binding names -> buffers (reference bench.py:94-101); dat3/dat4 carry
-    the mu/lambda vertex fields of elasticity_lame."""
+    the mu/lambda vertex fields of elasticity_lame, dat3 the state u0 of a
+    linearised form (neohookean_tangent)."""
     b = {
         "dat0": out,
         "dat1": np.ascontiguousarray(mesh.coords, dtype=np.float64).ravel(),
@@ -101,6 +102,8 @@ def make_bindings(mesh: Mesh, dofmap: DofMap, u, out, mu=None, lam=None) -> dict
     if mu is not None:
         b["dat3"] = np.ascontiguousarray(mu, dtype=np.float64)
         b["dat4"] = np.ascontiguousarray(lam, dtype=np.float64)
+    if state is not None:
+        b["dat3"] = np.ascontiguousarray(state, dtype=np.float64)
     return b
 
 
@@ -162,6 +165,12 @@ def flops_per_cell(spec: OperatorSpec, rule=None) -> int:
         return min(sf, dense)
     if cell.kind == "tetrahedron" and form == "neohookean" and k == 2:
         return nq * 543 + 52
+    if cell.kind == "tetrahedron" and form == "neohookean_tangent" and k == 2:
+        # per point: interpolate grad u0 and grad du (2 x 180), both to
+        # physical (2 x 45), F 3, cofactor + det 32, 1/J 1, F^-1 9, ln J 1,
+        # M = F^-1 dF 45, tr 2, M F^-1 45, dP 54, w|det| 10, dP J^-T 45,
+        # integrate 180; per cell geometry 52
+        return nq * 832 + 52
     # generic quadrature algorithm: interpolation and integration of values
     # (2 nd per component) and reference gradients (2 nd d per component)
     per_q = 0

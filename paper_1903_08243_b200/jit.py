@@ -75,6 +75,8 @@ def _wrapper_args(spec: OperatorSpec) -> tuple:
             ("dat2", "real64", "read")]
     if spec.coefficient_fields:
         args += [("dat3", "real64", "read"), ("dat4", "real64", "read")]
+    elif spec.has_state:
+        args += [("dat3", "real64", "read")]
     args += [("map0", "int32", "read"), ("map1", "int32", "read")]
     return tuple(args)
 

@@ -21,7 +21,7 @@ CELLS = {"triangle": (1, 2, 3, 4), "quadrilateral": (1, 2, 3, 4),
 N = {"triangle": (5, 4), "quadrilateral": (5, 4), "tetrahedron": (3, 2, 2), "hexahedron": (2, 2, 2)}
 
 CASES = [(f, c, k) for f in FORMS for c, ks in CELLS.items() for k in ks
-         if not (f == "neohookean" and k > 2)]
+         if not (f.startswith("neohookean") and k > 2)]
 
 
 def _run(form, cell, k, generic):
@@ -31,10 +31,11 @@ def _run(form, cell, k, generic):
     prob = build_problem(cfg, seed=k)
     h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(generic=generic), prob.rule))
     out = np.zeros(prob.ndofs)
-    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam))
+    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam,
+                                            state=prob.state))
     P = fo.Problem(form, cell, k, prob.rule.exactness_degree, prob.spec.params)
     ref = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
-                      prob.mu, prob.lam)
+                      prob.mu, prob.lam, state=prob.state)
     return h.info["kernel"], fo.rel_l2(out, ref)
 
 

@@ -30,8 +30,8 @@ def _setup(name):
            torch.tensor(np.asarray(prob.mesh.cell2vert, np.int32).ravel(), device=dev),
            nglobal=prob.dofmap.ndofs_global)
     coef = None
-    if prob.mu is not None:
-        coef = (torch.tensor(prob.mu, device=dev), torch.tensor(prob.lam, device=dev))
+    if prob.coef() is not None:
+        coef = tuple(None if c is None else torch.tensor(c, device=dev) for c in prob.coef())
 
     def A(u):
         y = torch.zeros_like(u)
@@ -48,11 +48,11 @@ def _subrange_parity(prob, h, dev, coef, ncheck=2048):
     P = fo.Problem(prob.spec.form, prob.spec.cell.kind, prob.spec.element.degree,
                    prob.rule.exactness_degree, prob.spec.params)
     ref = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
-                      prob.mu, prob.lam, 0, ncheck)
+                      prob.mu, prob.lam, 0, ncheck, state=prob.state)
     return fo.rel_l2(y.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("name", ["C2-P4", "C3-Q3", "C3-Q6", "C4-quad-Q4", "C4-hex-Q3"])
+@pytest.mark.parametrize("name", ["C2-P4", "C3-Q3", "C3-Q6", "C4-quad-Q4", "C4-hex-Q3", "C6"])
 def test_full_size_symmetry_linearity_and_parity(name):
     import torch
     prob, h, A, dev, coef = _setup(name)

@@ -13,9 +13,10 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
 
-def oracle_fn(spec, mesh, dm, rule, u, mu=None, lam=None, start=0, end=None):
+def oracle_fn(spec, mesh, dm, rule, u, mu=None, lam=None, start=0, end=None, state=None):
     P = fo.Problem(spec.form, spec.cell.kind, spec.element.degree, rule.exactness_degree, spec.params)
-    return fo.assemble(P, mesh.coords, mesh.cell2vert, dm.cell2dof, u, mu, lam, start, end)
+    return fo.assemble(P, mesh.coords, mesh.cell2vert, dm.cell2dof, u, mu, lam, start, end,
+                       state=state)
 
 
 def handle_for(spec, rule, generic=False):
@@ -50,7 +51,7 @@ CONFIG_CASES = [
     ("C1", 16), ("C2-P1", 5), ("C2-P2", 5), ("C2-P3", 4), ("C2-P4", 3),
     ("C3-Q1", 5), ("C3-Q2", 4), ("C3-Q3", 3), ("C3-Q4", 3), ("C3-Q5", 2), ("C3-Q6", 2),
     ("C4-quad-Q1", 12), ("C4-quad-Q2", 10), ("C4-quad-Q3", 8), ("C4-quad-Q4", 6),
-    ("C4-hex-Q1", 4), ("C4-hex-Q2", 3), ("C4-hex-Q3", 3), ("C5", 4),
+    ("C4-hex-Q1", 4), ("C4-hex-Q2", 3), ("C4-hex-Q3", 3), ("C5", 4), ("C6", 4),
 ]
 
 
@@ -70,13 +71,15 @@ def test_gpu_matches_oracle_on_config(name, n):
     if not _supported(name):
         pytest.xfail(f"no sm_100a kernel for {name} yet")
     h = handle_for(prob.spec, prob.rule)
-    ref = oracle_fn(prob.spec, prob.mesh, prob.dofmap, prob.rule, prob.u, prob.mu, prob.lam)
+    ref = oracle_fn(prob.spec, prob.mesh, prob.dofmap, prob.rule, prob.u, prob.mu, prob.lam,
+                    state=prob.state)
     out = np.zeros(prob.ndofs)
-    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam))
+    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam,
+                                            state=prob.state))
     assert fe.harness.rel_l2(out, ref) <= TOL, (name, h.info, fe.harness.rel_l2(out, ref))
 
 
-@pytest.mark.parametrize("name", ["C1", "C2-P1", "C2-P2", "C2-P3", "C3-Q3", "C5"])
+@pytest.mark.parametrize("name", ["C1", "C2-P1", "C2-P2", "C2-P3", "C3-Q3", "C5", "C6"])
 def test_arbitrary_cell_ranges(name):
     """Any [start, end) must be honoured (the reference's batched targets get
     unaligned start wrong)."""
@@ -86,9 +89,10 @@ def test_arbitrary_cell_ranges(name):
     for start, end in [(1, nc), (0, 1), (7, 7), (3, nc - 5), (nc - 1, nc), (6, 12), (5, 13),
                        (12, nc)]:
         ref = oracle_fn(prob.spec, prob.mesh, prob.dofmap, prob.rule, prob.u, prob.mu, prob.lam,
-                        start, end)
+                        start, end, state=prob.state)
         out = np.zeros(prob.ndofs)
-        h(start, end, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam))
+        h(start, end, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam,
+                                       state=prob.state))
         if end == start:
             assert not out.any()
         else:
@@ -138,14 +142,14 @@ def test_accumulate_semantics():
     assert fe.harness.rel_l2(out - 0.5, ref) <= TOL
 
 
-@pytest.mark.parametrize("name", ["C2-P3", "C5"])
+@pytest.mark.parametrize("name", ["C2-P3", "C5", "C6"])
 def test_device_path_matches_host_path(name):
     import torch
     prob = C.build_problem(C.get_config(name, 3), seed=4)
     h = handle_for(prob.spec, prob.rule)
     host = np.zeros(prob.ndofs)
-    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, host))
-    b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, np.zeros(prob.ndofs))
+    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, host, state=prob.state))
+    b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, np.zeros(prob.ndofs), state=prob.state)
     d = {k: torch.as_tensor(v, device="cuda") for k, v in b.items()}
     h(0, prob.mesh.ncells, d)
     torch.cuda.synchronize()
@@ -214,3 +218,31 @@ def test_missing_vertex_map_with_non_vertex_numbering_is_rejected():
         h.bind(torch.tensor(np.asarray(s.mesh.coords).ravel(), device=dev),
                torch.tensor(np.asarray(s.dofmap.cell2dof, np.int32).ravel(), device=dev), None,
                nglobal=s.dofmap.ndofs_global)
+
+
+def test_tangent_needs_the_state():
+    prob = C.build_problem(C.get_config("C6", 2), seed=9)
+    h = handle_for(prob.spec, prob.rule)
+    b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, np.zeros(prob.ndofs))
+    with pytest.raises(KeyError):
+        h(0, prob.mesh.ncells, b)
+
+
+def test_tangent_matches_central_difference_of_gpu_residual():
+    """GPU-only consistency: the tangent kernel (C6) against central
+    differences of the GPU residual kernel (C5) at the same state."""
+    prob = C.build_problem(C.get_config("C6", 3), seed=10)
+    res_spec = fe.operator_spec("neohookean", "tetrahedron", 2)
+    hr = handle_for(res_spec, prob.rule)
+    ht = handle_for(prob.spec, prob.rule)
+    eps = 1e-3 * 0.01 / 3
+
+    def residual(u):
+        out = np.zeros(prob.ndofs)
+        hr(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, u, out))
+        return out
+
+    fd = (residual(prob.state + eps * prob.u) - residual(prob.state - eps * prob.u)) / (2 * eps)
+    out = np.zeros(prob.ndofs)
+    ht(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, state=prob.state))
+    assert fe.harness.rel_l2(out, fd) < 1e-6

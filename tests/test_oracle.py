@@ -171,7 +171,8 @@ def _asm(prob, u=None, start=0, end=None, form=None):
     P = fo.Problem(form or prob.spec.form, prob.spec.cell.kind, prob.spec.element.degree,
                    prob.rule.exactness_degree, prob.spec.params)
     return fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof,
-                       prob.u if u is None else u, prob.mu, prob.lam, start, end)
+                       prob.u if u is None else u, prob.mu, prob.lam, start, end,
+                       state=prob.state)
 
 
 @pytest.mark.parametrize("name", ["C2-P1", "C2-P2", "C2-P3", "C3-Q1", "C3-Q3"])
@@ -311,3 +312,58 @@ def test_elasticity_lame_half_zero_equals_reference_elasticity():
     Pr = fo.Problem("elasticity", "quadrilateral", 2)
     b = fo.assemble(Pr, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u)
     assert fo.rel_l2(a, b) < 1e-15
+
+
+# ---------------------------------------------------------------------------
+# neohookean_tangent: the linearised residual at a state u0
+# ---------------------------------------------------------------------------
+
+
+def _tangent(prob_c6, du, state):
+    P = fo.Problem("neohookean_tangent", "tetrahedron", 2, 4)
+    return fo.assemble(P, prob_c6.mesh.coords, prob_c6.mesh.cell2vert, prob_c6.dofmap.cell2dof,
+                       du, state=state)
+
+
+def _residual(prob, u):
+    P = fo.Problem("neohookean", "tetrahedron", 2, 4)
+    return fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, u)
+
+
+def test_neohookean_tangent_is_derivative_of_residual():
+    """a(u0; du, v) = d/de r(u0 + e du; v): central differences of the
+    residual (error O(e^2)) along the configured direction."""
+    prob = _problem("C6", 2)
+    a = _tangent(prob, prob.u, prob.state)
+    h = 1e-3 * 0.01 / 2          # step relative to the state's scale
+    fd = (_residual(prob, prob.state + h * prob.u) - _residual(prob, prob.state - h * prob.u)) / (2 * h)
+    assert fo.rel_l2(a, fd) < 1e-6
+
+
+def test_neohookean_tangent_is_symmetric():
+    """Hyperelastic tangent: v . A(u0) du = du . A(u0) v."""
+    prob = _problem("C6", 2)
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1, 1, prob.u.shape)
+    lhs = v @ _tangent(prob, prob.u, prob.state)
+    rhs = prob.u @ _tangent(prob, v, prob.state)
+    assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+
+
+def test_neohookean_tangent_at_zero_state_is_lame_elasticity():
+    """At u0 = 0 (F = I) the tangent is exactly 2 mu eps : eps(v) + lambda
+    div div with mu = 1, lambda = 10."""
+    prob = _problem("C6", 2)
+    y = _tangent(prob, prob.u, np.zeros_like(prob.u))
+    P = fo.Problem("elasticity_lame", "tetrahedron", 2, 4)
+    nv = prob.mesh.nvertices
+    y_lin = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                        np.full(nv, 1.0), np.full(nv, 10.0))
+    assert fo.rel_l2(y, y_lin) < 1e-13
+
+
+def test_neohookean_tangent_annihilates_translations():
+    prob = _problem("C6", 2)
+    t = np.tile([0.3, -0.2, 0.7], prob.u.size // 3)
+    y = _tangent(prob, t, prob.state)
+    assert np.abs(y).max() < 1e-13

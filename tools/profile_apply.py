@@ -39,8 +39,8 @@ def main():
     u = torch.as_tensor(prob.u, device=dev)
     y = torch.zeros_like(u)
     coef = None
-    if prob.mu is not None:
-        coef = (torch.as_tensor(prob.mu, device=dev), torch.as_tensor(prob.lam, device=dev))
+    if prob.coef() is not None:
+        coef = tuple(None if c is None else torch.as_tensor(c, device=dev) for c in prob.coef())
     fn = lambda: h.apply(u, y, coef=coef, overwrite=True)
     if args.time:
         # the reference's protocol (bench.py:196-200): accumulate into an
