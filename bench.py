@@ -49,6 +49,7 @@ WORKLOADS = {
     "C3": [f"C3-Q{k}" for k in range(1, 7)],
     "C4": [f"C4-quad-Q{k}" for k in range(1, 5)] + [f"C4-hex-Q{k}" for k in range(1, 4)],
     "C5": ["C5"],
+    "C6": ["C6"],
 }
 WORKLOAD_TEXT = {
     "C2": "Helmholtz P1-P4 tetrahedra, 64^3 cubes x 6 tets per GPU, jittered",
@@ -56,6 +57,7 @@ WORKLOAD_TEXT = {
     "C3": "scalar Laplacian Q1-Q6 hexahedra 64^3 per GPU, k+1 GL points",
     "C4": "Lame elasticity Q1-Q4 quads 1024^2, Q1-Q3 hexes 64^3 per GPU",
     "C5": "neo-Hookean residual P2 tetrahedra 128^3 x 6 per GPU",
+    "C6": "neo-Hookean tangent action (SURVEY 8f.1) P2 tetrahedra 128^3 x 6 per GPU",
 }
 
 
@@ -165,8 +167,8 @@ def build_ops(names, seed, device, rank, world):
         u = torch.tensor(prob.u, device=device)
         y = torch.zeros_like(u)
         coef = None
-        if prob.mu is not None:
-            coef = (torch.tensor(prob.mu, device=device), torch.tensor(prob.lam, device=device))
+        if prob.coef() is not None:
+            coef = tuple(None if c is None else torch.tensor(c, device=device) for c in prob.coef())
         op = dict(name=name, prob=prob, h=h, u=u, y=y, coef=coef, C=m.ncells, ndofs=prob.ndofs,
                   F=fe.flops_per_cell(prob.spec, prob.rule),
                   B=fe.bytes_per_cell(prob.spec, m, dm))
@@ -199,10 +201,23 @@ def parity_sample(ops, ncheck=4096):
         yd = torch.zeros_like(op["u"])
         op["h"].apply(op["u"], yd, 0, end, coef=op["coef"])
         torch.cuda.synchronize()
-        ref = foc.assemble(oracle_problem(prob), prob.mesh.coords, prob.mesh.cell2vert,
-                           prob.dofmap.cell2dof, prob.u, prob.mu, prob.lam, 0, end, threads=8)
+        ref = _cpu_assemble(prob, end, 8)
         worst = max(worst, fo.rel_l2(yd.cpu().numpy(), ref))
     return worst
+
+
+def _cpu_assemble(prob, end, threads):
+    """C restatement of the reference loop (oracle/fe_oracle.c) over the
+    first `end` cells; the numpy restatement for forms the C one lacks
+    (neohookean_tangent)."""
+    from oracle import fe_oracle as fo
+    from oracle import fe_oracle_c as foc
+    P = oracle_problem(prob)
+    if prob.spec.form in foc.FORMS:
+        return foc.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                            prob.mu, prob.lam, 0, end, threads=threads)
+    return fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                       prob.mu, prob.lam, 0, end, state=getattr(prob, "state", None))
 
 
 def cpu_measure(ops_or_probs, budget_s=20.0):
@@ -235,8 +250,7 @@ def cpu_measure(ops_or_probs, budget_s=20.0):
                 dt = time.perf_counter() - t0
             else:
                 t0 = time.perf_counter()
-                foc.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
-                             prob.mu, prob.lam, 0, end, threads=cores)
+                _cpu_assemble(prob, end, cores)
                 dt = time.perf_counter() - t0
             if dt > per / 3 or end >= op["C"]:
                 break
@@ -265,7 +279,8 @@ def run_e2e(ops, steps):
         u = torch.empty(op["ndofs"], dtype=torch.float64, pin_memory=True).numpy()
         u[:] = prob.u
         out = torch.zeros(op["ndofs"], dtype=torch.float64, pin_memory=True).numpy()
-        hb.append((op, fe.make_bindings(prob.mesh, prob.dofmap, u, out, prob.mu, prob.lam)))
+        hb.append((op, fe.make_bindings(prob.mesh, prob.dofmap, u, out, prob.mu, prob.lam,
+                                        state=getattr(prob, "state", None))))
     for op, b in hb:                 # warm-up: binds the host mesh once
         op["h"](0, op["C"], b)
     t = 0.0

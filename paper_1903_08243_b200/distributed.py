@@ -52,6 +52,14 @@ class Slab:
     z1: int            # one past the last cube layer
     nz_global: int
     plane: int         # nodes per lattice plane (Lx * Ly)
+    state: np.ndarray = None   # u0 of a linearised form (C6), per-plane seeded like u
+
+    def coef(self):
+        if self.mu is not None:
+            return (self.mu, self.lam)
+        if self.state is not None:
+            return (self.state, None)
+        return None
 
     @property
     def ndofs(self) -> int:
@@ -134,7 +142,11 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
         nvp = (nx + 1) * (ny + 1)
         mu = np.concatenate([_plane_rng(seed, 2, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
         lam = np.concatenate([_plane_rng(seed, 3, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
-    return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane)
+    state = None
+    if spec.has_state:
+        state = np.concatenate([_plane_rng(seed, 4, k * z0 + L).uniform(-1.0, 1.0, plane * vs)
+                                for L in range(Lz)]) * (0.01 / max(nx, ny, nz_global))
+    return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane, state)
 
 
 class DistributedOperator:

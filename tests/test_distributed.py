@@ -26,12 +26,13 @@ def _oracle_apply(slab):
 
     def apply(u, y):
         y.copy_(torch.from_numpy(fo.assemble(P, slab.mesh.coords, slab.mesh.cell2vert,
-                                             slab.dofmap.cell2dof, u.numpy(), slab.mu, slab.lam)))
+                                             slab.dofmap.cell2dof, u.numpy(), slab.mu, slab.lam,
+                                             state=slab.state)))
 
     def range_apply(u, y, start, end, overwrite):
         part = torch.from_numpy(fo.assemble(P, slab.mesh.coords, slab.mesh.cell2vert,
                                             slab.dofmap.cell2dof, u.numpy(), slab.mu, slab.lam,
-                                            start, end))
+                                            start, end, state=slab.state))
         if overwrite:
             y.copy_(part)
         else:
@@ -67,7 +68,7 @@ def _worker(rank, world, port, name, nz, q, overlap=False):
 @pytest.mark.parametrize("name,world,nz,overlap", [
     ("C2-P2", 2, 2, False), ("C5", 2, 2, False), ("C3-Q2", 3, 2, False), ("C4-hex-Q1", 2, 2, False),
     # boundary layers first, exchange overlapping the interior layers
-    ("C2-P2", 3, 3, True), ("C4-hex-Q1", 2, 4, True)])
+    ("C2-P2", 3, 3, True), ("C4-hex-Q1", 2, 4, True), ("C6", 2, 2, True)])
 def test_distributed_equals_single_domain(name, world, nz, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -85,12 +86,15 @@ def test_distributed_equals_single_domain(name, world, nz, overlap):
     P = fo.Problem(glob.spec.form, glob.spec.cell.kind, glob.spec.element.degree,
                    glob.rule.exactness_degree, glob.spec.params)
     y_glob = fo.assemble(P, glob.mesh.coords, glob.mesh.cell2vert, glob.dofmap.cell2dof, glob.u,
-                         glob.mu, glob.lam)
+                         glob.mu, glob.lam, state=glob.state)
     k = glob.spec.element.degree
     per_plane = glob.plane * glob.spec.element.value_size
     for rank, z0, y, u in results:
         off = k * z0 * per_plane
         assert np.array_equal(u, glob.u[off:off + u.size])          # consistent inputs
+        if glob.state is not None:                                  # (and state planes)
+            sl = build_slab(cfg, 11, z0, z0 + nz, nz * world).state
+            assert np.array_equal(sl, glob.state[off:off + sl.size])
         assert fo.rel_l2(y, y_glob[off:off + y.size]) <= 1e-14, rank
 
 
