@@ -23,6 +23,7 @@
 #include "kern_quad.cuh"
 #include "kern_tensor.cuh"
 #include "kern_dmma.cuh"
+#include "kern_hexq1.cuh"
 
 using namespace fe;
 
@@ -736,6 +737,48 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   return FE_OK;
 }
 
+// thread-per-cell sum-factorised Q1 hex Laplacian (kern_hexq1.cuh)
+int hexq1_prepare(fe_plan* p) {
+  using TP = TensorParams<2, 2>;
+  for (int i = 0; i < 8; ++i)
+    if ((int)p->lex.size() != 8 || p->lex[i] != i)
+      return fail(FE_EUNSUPPORTED, "hexq1 kernel needs the tensor-ordered Q1 element");
+  TP* hp = new TP();
+  if (int rc = fill_tensor_tables<2, 2>(p, hp)) {
+    delete hp;
+    return rc;
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(TP);
+  // CTAs of 128 threads per SM the register allocation must allow
+  const char* env = getenv("FE_HEXQ1_MINB");
+  p->dmma_cfg = env ? atoi(env) : 3;
+  return FE_OK;
+}
+
+int hexq1_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                 const double*, const double*, cudaStream_t s) {
+  using TP = TensorParams<2, 2>;
+  TP* hp = static_cast<TP*>(p->host_params);
+  hp->mesh = mesh_view(p);
+  hp->maplex = p->d_map_lex;
+  hp->u = u;
+  hp->y = y;
+  hp->mu = hp->lam = nullptr;
+  hp->start = start;
+  hp->end = end;
+  const int n = end - start;
+  const unsigned g = (n + 127) / 128;
+  switch (p->dmma_cfg) {
+    case 1: hexq1_lap_kernel<1><<<g, 128, 0, s>>>(*hp); break;
+    case 2: hexq1_lap_kernel<2><<<g, 128, 0, s>>>(*hp); break;
+    case 4: hexq1_lap_kernel<4><<<g, 128, 0, s>>>(*hp); break;
+    default: hexq1_lap_kernel<3><<<g, 128, 0, s>>>(*hp); break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
 // component-pair 2D elasticity kernel (kern_pair.cuh)
 template <int FORM, int P, int Q, int MINB>
 int pair_prepare(fe_plan* p) {
@@ -810,6 +853,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define QCT(FORM, CELL, DIM, NV, K, ND, NQ, MINB, UNR)                                       \
   {FORM, CELL, K, NQ, 25, "quad_const_tensor", 128,                                          \
    qc_prepare<FORM, DIM, NV, ND, NQ, false, MINB, UNR>, qc_launch<FORM, DIM, NV, ND, NQ, false, MINB, UNR>}
+#define HQ1V()                                                                               \
+  {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 1, 8, 27, "sum_factorised_q1", 128,           \
+   hexq1_prepare, hexq1_launch}
 #define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
   {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
    split_launch<FORM, DIM, ND, NQS>}
@@ -899,6 +945,7 @@ static const Variant kVariants[] = {
     SPV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 2, 10, 4),
     // (..., MINB, quadrature-loop unroll): per measurement, profiles/r01/sweep_unroll*.txt
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1, 8),
+    HQ1V(),
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 1, 1),
@@ -1022,6 +1069,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 22 && getenv("FE_NO_PLANE")) continue;  // experiments: pencil team kernel
     if (v.priority == 23 && getenv("FE_NO_PLANE1")) continue;
     if (v.priority == 26 && getenv("FE_NO_PAIR")) continue;
+    if (v.priority == 27 && getenv("FE_NO_HEXQ1")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;
