@@ -111,6 +111,27 @@ FE_DEVICE void cp_async8_zfill(void* s, const void* g, bool valid) {
 template <int N>
 FE_DEVICE void cp_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// determinant and adjugate (J^-1 = adj / det) of a DIM x DIM matrix
+template <int DIM>
+FE_DEVICE double det_adj(const double (&J)[DIM][DIM], double (&A)[DIM][DIM]) {
+  if constexpr (DIM == 2) {
+    A[0][0] = J[1][1];  A[0][1] = -J[0][1];
+    A[1][0] = -J[1][0]; A[1][1] = J[0][0];
+    return J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  } else {
+    A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    return J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
+  }
+}
+
 // y[idx] += v.  The global scatter P_e^T: FP64 RED at L2 (REDG.E.ADD.F64).
 FE_DEVICE void scatter_add(double* y, int64_t idx, double v) { atomicAdd(y + idx, v); }
 

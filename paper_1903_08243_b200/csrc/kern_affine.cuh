@@ -187,16 +187,23 @@ struct SplitParams {
   double M[ND][ND];               // reference mass matrix (unused for laplacian_scalar)
 };
 
-template <int FORM, int DIM, int ND, int NQS>
+// reciprocal of |det J| per measurement (profiles/r01/sweep_split2.txt): the
+// Newton rcp() for P1 (macro kernel 20.4 -> 19.2 us), the IEEE division for
+// P2 (74.7 -> 66.5 us: rcp() lets ptxas hoist more and raise pressure)
+constexpr bool split_fast_rcp(int nd) { return nd == 4; }
+
+template <int FORM, int DIM, int ND, int NQS, bool MODAL = true>
 FE_DEVICE void split_compute(const SplitParams<NQS, ND, DIM>& p, const double (&X)[DIM + 1][DIM],
                              const double (&w)[ND], double (&yv)[ND]) {
-  // geometry: K = |det J| J^-1 J^-T (symmetric)
-  double J[DIM][DIM], Ji[DIM][DIM];
+  // geometry: K = |det J| J^-1 J^-T = adj(J) adj(J)^T / |det J| (symmetric;
+  // no explicit inverse)
+  double J[DIM][DIM], A[DIM][DIM];
 #pragma unroll
   for (int a = 0; a < DIM; ++a)
 #pragma unroll
     for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
-  const double ad = fabs(det_inv<DIM>(J, Ji));
+  const double ad = fabs(det_adj<DIM>(J, A));
+  const double rad = recip<split_fast_rcp(ND)>(ad);
   double K[DIM][DIM];
 #pragma unroll
   for (int a = 0; a < DIM; ++a)
@@ -204,8 +211,8 @@ FE_DEVICE void split_compute(const SplitParams<NQS, ND, DIM>& p, const double (&
     for (int b = a; b < DIM; ++b) {
       double s = 0.0;
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) s = fma(Ji[a][c], Ji[b][c], s);
-      K[a][b] = K[b][a] = ad * s;
+      for (int c = 0; c < DIM; ++c) s = fma(A[a][c], A[b][c], s);
+      K[a][b] = K[b][a] = rad * s;
     }
   // mass term
 #pragma unroll
@@ -234,7 +241,7 @@ FE_DEVICE void split_compute(const SplitParams<NQS, ND, DIM>& p, const double (&
       double s = 0.0;
 #pragma unroll
       for (int b = 0; b < DIM; ++b) s = fma(K[a][b], g[b], s);
-      f[a] = p.qw[q] * s;
+      f[a] = MODAL ? s : p.qw[q] * s;  // stiffness modes carry unit weights
     }
 #pragma unroll
     for (int j = 0; j < ND; ++j)

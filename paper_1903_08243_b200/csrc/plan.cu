@@ -355,7 +355,9 @@ template <int FORM, int DIM, int ND, int NQS>
 int split_prepare(fe_plan* p) {
   using P = SplitParams<NQS, ND, DIM>;
   static_assert(sizeof(P) <= 32000, "parameter block too large");
-  if ((int)p->qw_aux.size() != NQS) return fail(FE_EUNSUPPORTED, "split kernel needs the degree 2k-2 rule");
+  if ((int)p->qw_aux.size() != NQS) return fail(FE_EUNSUPPORTED, "split kernel needs %d stiffness modes", NQS);
+  for (double w : p->qw_aux)
+    if (w != 1.0) return fail(FE_EUNSUPPORTED, "split kernel takes unit-weight stiffness modes");
   std::vector<double> S;
   element_matrices(p, true, false, S);  // reference mass matrix
   P* hp = new P();
