@@ -171,6 +171,16 @@ int fe_wrap_host(fe_plan* plan, int32_t start, int32_t end, double* dat0,
 
 int fe_plan_get_info(const fe_plan* plan, fe_plan_info* info);
 
+/* Operator diagonal on the bound mesh (Jacobi preconditioner
+ * of a matrix-free solve): diag (+)= sum over cells in [start,end) of
+ * P_e^T diag(A_e), vs*nglobal doubles in the layout of dat2.  Linear forms
+ * only (and neohookean_tangent at the state coef0); FE_EUNSUPPORTED for the
+ * nonlinear residual.  Same coef0/coef1/flags/stream meaning as fe_apply.
+ * A one-time setup kernel: it recomputes the reference quadrature per local
+ * dof (cost ~ ndof x apply). */
+int fe_diagonal(const fe_plan* plan, int32_t start, int32_t end, double* diag,
+                const double* coef0, const double* coef1, uint32_t apply_flags, void* stream);
+
 void fe_plan_destroy(fe_plan* plan);
 
 const char* fe_last_error(void);

@@ -36,7 +36,9 @@ from .harness import (
     verify_target,
     write_csv,
 )
-from .jit import GpuKernelHandle, PlanUnit, Target, ToolchainError, compile_and_load, emit_for
+from .jit import (GpuKernelHandle, KernelError, PlanUnit, Target, ToolchainError, compile_and_load,
+                  emit_for)
+from . import solver
 from .mesh import DofMap, Mesh, build_dof_map, build_mesh, jitter_mesh
 
 __version__ = "0.1.0"

@@ -63,7 +63,7 @@ class FeError(RuntimeError):
 # every symbol include/fe_b200.h declares
 EXPORTS = (
     "fe_abi_version", "fe_plan_create", "fe_plan_bind_mesh", "fe_apply", "fe_wrap",
-    "fe_wrap_host", "fe_plan_get_info", "fe_plan_destroy", "fe_last_error",
+    "fe_wrap_host", "fe_plan_get_info", "fe_plan_destroy", "fe_last_error", "fe_diagonal",
 )
 
 _lib = None
@@ -89,6 +89,7 @@ def load():
     lib.fe_apply.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp,
                              ctypes.c_uint32, vp]
     lib.fe_wrap.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.fe_diagonal.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, ctypes.c_uint32, vp]
     lib.fe_wrap_host.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp]
     lib.fe_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
     lib.fe_plan_destroy.argtypes = [vp]

@@ -293,6 +293,106 @@ __global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Operator diagonal (fe_diagonal, Jacobi preconditioner of a matrix-free
+// solve): diag(A_e)[i][c] = the (i, c) entry of A_e applied to the unit
+// vector e_(i,c), i.e. the reference quadrature loop with w = e_(i,c).  One
+// thread per cell, loops over local dofs outermost (one RED per entry);
+// geometry recomputed per (dof, point) on non-affine cells -- a one-time
+// setup kernel, not a hot path.
+// ---------------------------------------------------------------------------
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
+__global__ void __launch_bounds__(128) quad_diag_kernel(QuadParams p) {
+  constexpr int VS = form_vs(FORM, DIM);
+  using TB = QuadTables<NQ, ND, NV, DIM>;
+  extern __shared__ double smem[];
+  for (int i = threadIdx.x; i < TB::size; i += blockDim.x) smem[i] = p.tables[i];
+  __syncthreads();
+  const double* s_qw = smem + TB::qw;
+  const double* s_phi = smem + TB::phi;
+  const double* s_dphi = smem + TB::dphi;
+  const double* s_gphi = smem + TB::gphi;
+  const double* s_gdphi = smem + TB::gdphi;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  double X[NV][DIM];
+  int vid[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    vid[v] = __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<DIM>(p.mesh.coords, vid[v], X[v]);
+  }
+  double J[DIM][DIM], Ji[DIM][DIM], absdet = 0.0;
+  auto jacobian = [&](int q) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s += X[v][a] * s_gdphi[(q * NV + v) * DIM + b];
+        J[a][b] = s;
+      }
+    absdet = fabs(det_inv<DIM>(J, Ji));
+  };
+  if constexpr (AFFINE) jacobian(0);
+#pragma unroll 1
+  for (int i = 0; i < ND; ++i) {
+    const int dof = __ldg(p.mesh.map + i * cs + cell);
+#pragma unroll 1
+    for (int c = 0; c < VS; ++c) {
+      double acc = 0.0;
+#pragma unroll 1
+      for (int q = 0; q < NQ; ++q) {
+        if constexpr (!AFFINE) jacobian(q);
+        const double tw = s_qw[q] * absdet;
+        double uq[VS], g[VS][DIM], g0[VS][DIM];
+#pragma unroll
+        for (int cc = 0; cc < VS; ++cc) {
+          uq[cc] = cc == c ? s_phi[q * ND + i] : 0.0;
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) g[cc][b] = cc == c ? s_dphi[(q * ND + i) * DIM + b] : 0.0;
+        }
+        if constexpr (form_has_state(FORM)) {
+#pragma unroll
+          for (int cc = 0; cc < VS; ++cc)
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) g0[cc][b] = 0.0;
+          for (int j = 0; j < ND; ++j) {
+            const int dj = __ldg(p.mesh.map + j * cs + cell);
+#pragma unroll
+            for (int cc = 0; cc < VS; ++cc) {
+              const double w0 = __ldg(p.mu + (int64_t)VS * dj + cc);
+#pragma unroll
+              for (int b = 0; b < DIM; ++b) g0[cc][b] += s_dphi[(q * ND + j) * DIM + b] * w0;
+            }
+          }
+        }
+        double mu = p.p0, lam = p.p1;
+        if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+          mu = 0.0;
+          lam = 0.0;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double gv = s_gphi[q * NV + v];
+            mu += gv * __ldg(p.mu + vid[v]);
+            lam += gv * __ldg(p.lam + vid[v]);
+          }
+        }
+        double cv[VS], cg[VS][DIM];
+        pointwise<FORM, DIM, VS>(Ji, tw, uq, g, mu, lam, cv, cg, g0);
+        if constexpr (form_needs_values(FORM)) acc += s_phi[q * ND + i] * cv[c];
+        if constexpr (form_needs_grads(FORM)) {
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) acc += s_dphi[(q * ND + i) * DIM + b] * cg[c][b];
+        }
+      }
+      scatter_add(p.y, (int64_t)VS * dof + c, acc);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Quadrature kernel with the tables in the kernel parameter block.
 //  * affine simplices (C5: neo-Hookean P2 tetrahedra, 27 points): the
 //    Jacobian and its inverse are computed once per cell from vertex

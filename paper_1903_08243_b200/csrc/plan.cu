@@ -72,6 +72,8 @@ struct fe_plan {
   // device tables (kernel-family specific layout)
   double* d_tables = nullptr;
   size_t tables_bytes = 0;
+  double* d_diag_tables = nullptr;  // generic quadrature tables of fe_diagonal (lazy)
+  size_t diag_tables_bytes = 0;
   int persistent_ctas = 0;
   int dmma_cfg = 0;
   int cells_per_block = 0;
@@ -119,6 +121,9 @@ typedef int (*PrepareFn)(fe_plan*);
 typedef int (*LaunchFn)(const fe_plan*, int32_t, int32_t, double*, const double*, const double*,
                         const double*, cudaStream_t);
 
+typedef int (*DiagFn)(const fe_plan*, int32_t, int32_t, double*, const double*, const double*,
+                      cudaStream_t);
+
 struct Variant {
   int form, cell, degree, nq;  // nq = -1: any rule accepted by the prepare step
   int priority;                // higher wins
@@ -126,6 +131,7 @@ struct Variant {
   int block;
   PrepareFn prepare;
   LaunchFn launch;
+  DiagFn diag = nullptr;       // operator diagonal (generic quadrature entries only)
 };
 
 // ---------------------------------------------------------------------------
@@ -178,6 +184,47 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
       <<<(n + 127) / 128, 128, p->tables_bytes, s>>>(k);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
+}
+
+// operator diagonal: the generic tables, uploaded on first use
+template <int FORM, int DIM, int NV, int ND, int NQ, bool AFFINE>
+int quad_diag(const fe_plan* cp, int32_t start, int32_t end, double* y, const double* c0,
+              const double* c1, cudaStream_t s) {
+  if constexpr (FORM == FE_FORM_NEOHOOKEAN) {
+    return fail(FE_EUNSUPPORTED, "the neohookean residual is nonlinear: no operator diagonal");
+  } else {
+    fe_plan* p = const_cast<fe_plan*>(cp);
+    using TB = QuadTables<NQ, ND, NV, DIM>;
+    if (!p->d_diag_tables) {
+      std::vector<double> t(TB::size);
+      std::copy(p->qw.begin(), p->qw.end(), t.begin() + TB::qw);
+      std::copy(p->phi.begin(), p->phi.end(), t.begin() + TB::phi);
+      std::copy(p->dphi.begin(), p->dphi.end(), t.begin() + TB::dphi);
+      std::copy(p->gphi.begin(), p->gphi.end(), t.begin() + TB::gphi);
+      std::copy(p->gdphi.begin(), p->gdphi.end(), t.begin() + TB::gdphi);
+      p->diag_tables_bytes = t.size() * sizeof(double);
+      CUDA_TRY(cudaMalloc(&p->d_diag_tables, p->diag_tables_bytes));
+      CUDA_TRY(cudaMemcpy(p->d_diag_tables, t.data(), p->diag_tables_bytes, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaFuncSetAttribute(quad_diag_kernel<FORM, DIM, NV, ND, NQ, AFFINE>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)p->diag_tables_bytes));
+    }
+    QuadParams k;
+    k.mesh = mesh_view(p);
+    k.start = start;
+    k.end = end;
+    k.u = nullptr;
+    k.y = y;
+    k.mu = c0;
+    k.lam = c1;
+    k.tables = p->d_diag_tables;
+    k.p0 = p->params[0];
+    k.p1 = p->params[1];
+    const int n = end - start;
+    quad_diag_kernel<FORM, DIM, NV, ND, NQ, AFFINE><<<(n + 127) / 128, 128, p->diag_tables_bytes, s>>>(k);
+    CUDA_TRY(cudaGetLastError());
+    return FE_OK;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -821,7 +868,7 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 
 #define QV(FORM, CELL, DIM, NV, K, ND, NQ, AFF)                                              \
   {FORM, CELL, K, NQ, 0, "quad", 128, quad_prepare<FORM, DIM, NV, ND, NQ, AFF>,           \
-   quad_launch<FORM, DIM, NV, ND, NQ, AFF>}
+   quad_launch<FORM, DIM, NV, ND, NQ, AFF>, quad_diag<FORM, DIM, NV, ND, NQ, AFF>}
 #define DMV(FORM, CELL, DIM, K, ND)                                                          \
   {FORM, CELL, K, -1, 20, "dmma_element_tensor", kDmmaBlock, dmma_prepare<FORM, DIM, ND>,    \
    dmma_launch<FORM, DIM, ND>}
@@ -1352,6 +1399,29 @@ int fe_apply(const fe_plan* p, int32_t start, int32_t end, double* y, const doub
   return p->var->launch(p, start, end, y, u, c0, c1, s);
 }
 
+int fe_diagonal(const fe_plan* p, int32_t start, int32_t end, double* diag, const double* c0,
+                const double* c1, uint32_t apply_flags, void* stream) {
+  if (!p) return fail(FE_EINVAL, "null plan");
+  if (!p->d_map) return fail(FE_ENOMESH, "no mesh bound to the plan");
+  if (start < 0 || end > p->ncells || start > end)
+    return fail(FE_EINVAL, "cell range [%d, %d) outside [0, %d)", start, end, p->ncells);
+  if (!diag) return fail(FE_EINVAL, "null diag");
+  if (p->form == FE_FORM_ELASTICITY_LAME && (!c0 || !c1))
+    return fail(FE_EINVAL, "elasticity_lame needs the mu and lambda vertex fields");
+  if (p->form == FE_FORM_NEOHOOKEAN_TANGENT && !c0)
+    return fail(FE_EINVAL, "neohookean_tangent needs the state u (coef0)");
+  // the generic quadrature entry of this (form, cell, degree, rule)
+  const Variant* g = nullptr;
+  for (const Variant& v : kVariants)
+    if (v.diag && v.form == p->form && v.cell == p->cell && v.degree == p->degree && v.nq == p->nq) g = &v;
+  if (!g) return fail(FE_EUNSUPPORTED, "no diagonal kernel for this (form, cell, degree, rule)");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (apply_flags & FE_APPLY_OVERWRITE)
+    CUDA_TRY(cudaMemsetAsync(diag, 0, (size_t)p->vs * p->nglobal * sizeof(double), s));
+  if (end == start) return FE_OK;
+  return g->diag(p, start, end, diag, c0, c1, s);
+}
+
 int fe_wrap(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat1,
             const double* dat2, const double* dat3, const double* dat4, const int32_t* map0,
             const int32_t* map1, void* stream) {
@@ -1448,6 +1518,7 @@ void fe_plan_destroy(fe_plan* p) {
   if (!p) return;
   free_mesh(p);
   cudaFree(p->d_tables);
+  cudaFree(p->d_diag_tables);
   cudaFree(p->d_lex);
   cudaFree(p->d_u);
   cudaFree(p->d_y);

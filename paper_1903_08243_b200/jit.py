@@ -300,6 +300,25 @@ class GpuKernelHandle:
                                 ctypes.c_void_p(stream) if stream else None)
         _lib.check(rc, "fe_apply")
 
+    def diagonal(self, coef=None, out=None, start=0, end=None, stream=None):
+        """Operator diagonal on the bound mesh (fe_diagonal): a CUDA float64
+        tensor of vs*nglobal entries, e.g. the Jacobi preconditioner of
+        ``solver.cg``.  Linear forms (and the tangent at its state) only."""
+        import torch
+        if self._bound is None:
+            raise _lib.FeError("no mesh bound: call bind() first")
+        end = self._bound[2] if end is None else end
+        if out is None:
+            out = torch.zeros(self.value_size * self._bound[3], dtype=torch.float64, device="cuda")
+        ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())
+        c0, c1 = (None, None) if coef is None else coef
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        rc = self._lib.fe_diagonal(self._plan, int(start), int(end), ptr(out), ptr(c0), ptr(c1),
+                                   _lib.FE_APPLY_ACCUMULATE, ctypes.c_void_p(stream))
+        _lib.check(rc, "fe_diagonal")
+        return out
+
     def __del__(self):
         plan = getattr(self, "_plan", None)
         if plan:
