@@ -317,8 +317,8 @@ def run_configuration(spec, target, mesh, dofmap, trials=20, seed=0, rule=None, 
     ud = torch.as_tensor(u, device=dev)
     yd = torch.zeros_like(ud)
     coef = None
-    if mu is not None:
-        coef = (torch.as_tensor(mu, device=dev), torch.as_tensor(lam, device=dev))
+    if mu is not None:   # (mu, lambda) vertex fields, or (state u0, None) of a linearised form
+        coef = tuple(None if c is None else torch.as_tensor(c, device=dev) for c in (mu, lam))
     times = time_device(lambda: handle.apply(ud, yd, coef=coef, overwrite=True), trials=trials)
     best, mean = min(times), sum(times) / len(times)
     fpc = flops_per_cell(spec, rule)
