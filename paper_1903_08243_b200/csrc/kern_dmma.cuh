@@ -195,8 +195,8 @@ struct ModalShape {
   static constexpr int NSTEP = DIM * TPL;       // stage-2 modal k-steps (one per lane slot)
 };
 
-template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB>
-__global__ void __launch_bounds__(256, MINB) dmma_modal_kernel(DmmaParams p) {
+template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB, int BLK = 256>
+__global__ void __launch_bounds__(BLK, MINB) dmma_modal_kernel(DmmaParams p) {
   constexpr bool MASS = FORM == FE_FORM_HELMHOLTZ;
   constexpr int NM = et_nmats<FORM, DIM>();
   constexpr int KT = DmmaShape<ND>::KT, MT = DmmaShape<ND>::MT, NV = DIM + 1;

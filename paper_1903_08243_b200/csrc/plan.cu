@@ -551,14 +551,28 @@ int dmma_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 // modal two-stage DMMA kernel (kern_dmma.cuh): fragment-ordered G (stage 1,
 // B operand) and [G^T | Mhat] (stage 2, A operand) from the plan's stiffness
 // modes (qw_aux / dphi_aux, elements.stiffness_modes) and mass matrix.
-template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB>
+// (NT, MINB, BLK) configurations of the modal kernel (FE_DMMA_CFG):
+// 0 = (2,1,256) 1 = (1,2,256) 2 = (2,2,256) 3 = (1,1,256) 4 = (1,5,128)
+// 5 = (1,6,128) 6 = (1,3,256)
+#define FE_MODAL_CFGS(F)                                                          \
+  switch (p->dmma_cfg) {                                                          \
+    case 1: return F(1, 2, 256);                                                  \
+    case 2: return F(2, 2, 256);                                                  \
+    case 3: return F(1, 1, 256);                                                  \
+    case 4: return F(1, 5, 128);                                                  \
+    case 5: return F(1, 6, 128);                                                  \
+    case 6: return F(1, 3, 256);                                                  \
+    default: return F(2, 1, 256);                                                 \
+  }
+
+template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB, int BLK>
 int dmma_modal_setup(fe_plan* p) {
-  auto kfn = dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB>;
+  auto kfn = dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB, BLK>;
   CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tables_bytes));
   int dev = 0, sms = 0, per_sm = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kDmmaBlock, p->tables_bytes));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, BLK, p->tables_bytes));
   p->persistent_ctas = sms * (per_sm > 0 ? per_sm : 1);
   return FE_OK;
 }
@@ -608,21 +622,18 @@ int dmma_modal_prepare(fe_plan* p) {
   CUDA_TRY(cudaMemcpy(p->d_tables, T.data(), p->tables_bytes, cudaMemcpyHostToDevice));
   const char* env = getenv("FE_DMMA_CFG");
   p->dmma_cfg = env ? atoi(env) : 1;
-  if (p->dmma_cfg < 0 || p->dmma_cfg > 3) p->dmma_cfg = 0;
-  switch (p->dmma_cfg) {
-    case 1: return dmma_modal_setup<FORM, DIM, ND, NMODE, 1, 2>(p);
-    case 2: return dmma_modal_setup<FORM, DIM, ND, NMODE, 2, 2>(p);
-    case 3: return dmma_modal_setup<FORM, DIM, ND, NMODE, 1, 1>(p);
-    default: return dmma_modal_setup<FORM, DIM, ND, NMODE, 2, 1>(p);
-  }
+  if (p->dmma_cfg < 0 || p->dmma_cfg > 6) p->dmma_cfg = 0;
+#define FE_SETUP(NT, MINB, BLK) dmma_modal_setup<FORM, DIM, ND, NMODE, NT, MINB, BLK>(p)
+  FE_MODAL_CFGS(FE_SETUP)
+#undef FE_SETUP
 }
 
-template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB>
+template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB, int BLK>
 int dmma_modal_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_t s) {
   const int ngroups = (n + 8 * NT - 1) / (8 * NT);
-  const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
+  const int need = (ngroups + BLK / 32 - 1) / (BLK / 32);
   const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
-  dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k);
+  dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB, BLK><<<grid, BLK, p->tables_bytes, s>>>(k);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -637,12 +648,9 @@ int dmma_modal_launch(const fe_plan* p, int32_t start, int32_t end, double* y, c
   k.afrag = p->d_tables;
   k.start = start;
   k.end = end;
-  switch (p->dmma_cfg) {
-    case 1: return dmma_modal_run<FORM, DIM, ND, NMODE, 1, 2>(p, k, end - start, s);
-    case 2: return dmma_modal_run<FORM, DIM, ND, NMODE, 2, 2>(p, k, end - start, s);
-    case 3: return dmma_modal_run<FORM, DIM, ND, NMODE, 1, 1>(p, k, end - start, s);
-    default: return dmma_modal_run<FORM, DIM, ND, NMODE, 2, 1>(p, k, end - start, s);
-  }
+#define FE_RUN(NT, MINB, BLK) dmma_modal_run<FORM, DIM, ND, NMODE, NT, MINB, BLK>(p, k, end - start, s)
+  FE_MODAL_CFGS(FE_RUN)
+#undef FE_RUN
 }
 
 // ---------------------------------------------------------------------------

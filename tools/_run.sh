@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q -k "cli" > gpurun_out/pytest_cli.log 2>&1; tail -3 gpurun_out/pytest_cli.log
-python -m paper_1903_08243_b200 verify --n 4 > gpurun_out/cli_verify.txt 2>&1; tail -25 gpurun_out/cli_verify.txt
+for c in C2-P3 C2-P4; do for cfg in 1 4 5 6; do
+echo "cfg=$cfg $(FE_DMMA_CFG=$cfg python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+done; done > gpurun_out/sweep_modal_occ.txt 2>&1
+cut -c1-200 gpurun_out/sweep_modal_occ.txt
+FE_DMMA_CFG=4 python -m pytest tests -m gpu -x -q -k "C2-P3 or alternative" 2>&1 | tail -1
