@@ -313,7 +313,71 @@ struct KuhnTetP1 {
   }
 };
 
-template <int FORM, int DIM, int ND, int NQS, class PAT>
+// NCX consecutive Kuhn cubes along x (cells ordered x-fastest): they share
+// their x-faces, so 4 + 4 NCX distinct corners; macro-dof id of corner bits
+// (bx, by, bz) of cube c = (c + bx) + (NCX + 1) (by + 2 bz)
+template <int NCX>
+struct KuhnTetRowP1 {
+  static constexpr int MC = 6 * NCX, NU = 4 * (NCX + 1), ND = 4;
+  __host__ __device__ static constexpr int at(int t, int i) {
+    const int c = t / 6, k = KuhnTetP1::at(t % 6, i);
+    return (c + (k & 1)) + (NCX + 1) * (((k >> 1) & 1) + 2 * ((k >> 2) & 1));
+  }
+};
+
+// P1 simplex with the element's tables as compile-time constants (what the
+// reference's codegen bakes into the emitted source, codegen.py:409-424):
+// reference gradients e_b - e_0, so grad_ref u = (w_b+1 - w_0); stiffness
+// (1/(d! |det J|)) adj(J) adj(J)^T grad_ref u (adjugate form, no inverse);
+// mass |det J| (1 + delta_ij) / ((d+1)(d+2) d!/2 ... ) = |det J|(1+delta_ij)/120
+// in 3D, /24 in 2D -> |det J| c (w_i + sum w).  ~80 FP64 instructions per
+// tet instead of ~110 for the table-driven split_compute; the plan only
+// enables it after checking its tables against these constants.
+template <int FORM, int DIM>
+FE_DEVICE void p1_simplex_compute(const double (&X)[DIM + 1][DIM], const double (&w)[DIM + 1],
+                                  double (&yv)[DIM + 1]) {
+  constexpr double VREF = DIM == 3 ? 1.0 / 6.0 : 0.5;
+  constexpr double CMASS = DIM == 3 ? 1.0 / 120.0 : 1.0 / 24.0;
+  double J[DIM][DIM], A[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+  const double ad = fabs(det_adj<DIM>(J, A));
+  const double rs = VREF * rcp(ad);
+  double d[DIM], t[DIM], f[DIM];
+#pragma unroll
+  for (int b = 0; b < DIM; ++b) d[b] = w[b + 1] - w[0];
+#pragma unroll
+  for (int e = 0; e < DIM; ++e) {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < DIM; ++r) s = fma(A[r][e], d[r], s);
+    t[e] = rs * s;
+  }
+  double fs = 0.0;
+#pragma unroll
+  for (int r = 0; r < DIM; ++r) {
+    double s = 0.0;
+#pragma unroll
+    for (int e = 0; e < DIM; ++e) s = fma(A[r][e], t[e], s);
+    f[r] = s;
+    fs += s;
+  }
+  yv[0] = -fs;
+#pragma unroll
+  for (int b = 0; b < DIM; ++b) yv[b + 1] = f[b];
+  if constexpr (FORM == FE_FORM_HELMHOLTZ) {
+    double sw = w[0];
+#pragma unroll
+    for (int i = 1; i <= DIM; ++i) sw += w[i];
+    const double cm = CMASS * ad;
+#pragma unroll
+    for (int i = 0; i <= DIM; ++i) yv[i] = fma(cm, w[i] + sw, yv[i]);
+  }
+}
+
+template <int FORM, int DIM, int ND, int NQS, class PAT, bool ANALYTIC = false>
 __global__ void __launch_bounds__(128)
 macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const int32_t* __restrict__ corner,
                    int64_t mstride, int32_t m0, int32_t m1) {
@@ -340,7 +404,8 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
       for (int a = 0; a < DIM; ++a) Xt[i][a] = X[PAT::at(t, i)][a];
       wt[i] = w[PAT::at(t, i)];
     }
-    split_compute<FORM, DIM, ND, NQS>(p, Xt, wt, yt);
+    if constexpr (ANALYTIC) p1_simplex_compute<FORM, DIM>(Xt, wt, yt);
+    else split_compute<FORM, DIM, ND, NQS>(p, Xt, wt, yt);
 #pragma unroll
     for (int i = 0; i < ND; ++i) yl[PAT::at(t, i)] += yt[i];
   }

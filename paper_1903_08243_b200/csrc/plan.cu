@@ -100,6 +100,7 @@ struct fe_plan {
   int macro_mc = 0, macro_nu = 0;
   int32_t* d_macro = nullptr;
   int64_t macro_stride = 0;
+  bool p1_analytic = false;  // tables verified equal to the compile-time P1 constants
   double* d_coords = nullptr;   // padded [nverts][cstride]
   const void* b_coords = nullptr;
   const void* b_map0 = nullptr;
@@ -321,6 +322,13 @@ static void element_matrices(const fe_plan* p, bool mass, bool grads, std::vecto
 #ifndef FE_GROUP_TRI_P2
 #define FE_GROUP_TRI_P2 1
 #endif
+// macro-cell of the P1 tet kernel: cubes per thread along x (measured,
+// profiles/r01/sweep_p1const.txt)
+#ifndef FE_MACRO_NCX
+#define FE_MACRO_NCX 1
+#endif
+using MacroP1 = std::conditional_t<FE_MACRO_NCX == 1, KuhnTetP1, KuhnTetRowP1<FE_MACRO_NCX>>;
+
 constexpr int affine_group(int dim, int nd) {
   return dim == 3 ? (nd == 4 ? FE_GROUP_TET_P1 : nd == 10 ? FE_GROUP_TET_P2 : 1)
                   : (nd == 6 ? FE_GROUP_TRI_P2 : 1);
@@ -416,8 +424,24 @@ int split_prepare(fe_plan* p) {
   std::memcpy(hp->M, S.data(), sizeof(hp->M));
   p->host_params = hp;
   p->host_params_bytes = sizeof(P);
+  if (DIM + 1 == ND && NQS == 1 && !getenv("FE_NO_P1CONST")) {
+    // P1: the plan's tables must equal the constants p1_simplex_compute bakes in
+    const double vref = DIM == 3 ? 1.0 / 6.0 : 0.5, cmass = DIM == 3 ? 1.0 / 120.0 : 1.0 / 24.0;
+    auto gref = [](int i, int b) { return i == 0 ? -1.0 : (i == b + 1 ? 1.0 : 0.0); };
+    bool ok = true;
+    for (int i = 0; i < ND; ++i)
+      for (int j = 0; j < ND; ++j) {
+        if (std::fabs(hp->M[i][j] - cmass * (i == j ? 2.0 : 1.0)) > 1e-15) ok = false;
+        for (int a = 0; a < DIM; ++a)
+          for (int b = 0; b < DIM; ++b) {
+            const double s = hp->qw[0] * hp->dphi[0][i][a] * hp->dphi[0][j][b];
+            if (std::fabs(s - vref * gref(i, a) * gref(j, b)) > 1e-14) ok = false;
+          }
+      }
+    p->p1_analytic = ok;
+  }
   if (DIM == 3 && ND == 4 && !getenv("FE_NO_MACRO")) {
-    using PAT = KuhnTetP1;
+    using PAT = MacroP1;
     p->macro_mc = PAT::MC;
     p->macro_nu = PAT::NU;
     p->macro_pat.clear();
@@ -448,11 +472,15 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   if constexpr (DIM == 3 && ND == 4) {
     if (p->d_macro) {
       // whole macro-cells inside [start, end) on the macro kernel, ragged ends per cell
-      const int mc = KuhnTetP1::MC;
+      const int mc = MacroP1::MC;
       const int32_t m0 = (start + mc - 1) / mc, m1 = end / mc;
       if (m0 < m1) {
-        macro_split_kernel<FORM, DIM, ND, NQS, KuhnTetP1>
-            <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+        if (p->p1_analytic)
+          macro_split_kernel<FORM, DIM, ND, NQS, MacroP1, true>
+              <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+        else
+          macro_split_kernel<FORM, DIM, ND, NQS, MacroP1>
+              <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
         per_cell(start, m0 * mc);
         per_cell(m1 * mc, end);
         CUDA_TRY(cudaGetLastError());

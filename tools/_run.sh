@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
-for c in C2-P3 C2-P4; do for cfg in 1 4 5 6; do
-echo "cfg=$cfg $(FE_DMMA_CFG=$cfg python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
-done; done > gpurun_out/sweep_modal_occ.txt 2>&1
-cut -c1-200 gpurun_out/sweep_modal_occ.txt
-FE_DMMA_CFG=4 python -m pytest tests -m gpu -x -q -k "C2-P3 or alternative" 2>&1 | tail -1
+FE_LIB_PATH=paper_1903_08243_b200/libfeb200_ncx2.so python -m pytest tests -m gpu -x -q -k "C2-P1 or macro or range" > gpurun_out/pytest_ncx2.log 2>&1; tail -1 gpurun_out/pytest_ncx2.log
+for i in 1 2; do
+echo "ncx1 $(python tools/profile_apply.py --config C2-P1 --time --reps 30 2>&1 | tail -1)"
+echo "ncx2 $(FE_LIB_PATH=paper_1903_08243_b200/libfeb200_ncx2.so python tools/profile_apply.py --config C2-P1 --time --reps 30 2>&1 | tail -1)"
+done >> gpurun_out/sweep_p1const.txt 2>&1
+tail -4 gpurun_out/sweep_p1const.txt | cut -c1-200
