@@ -110,6 +110,7 @@ struct fe_plan {
   cudaStream_t hstream = nullptr;
   cudaStream_t hstream2 = nullptr;
   cudaEvent_t ev_u = nullptr, ev_y0 = nullptr;
+  cudaEvent_t ev_y0c[8] = {};  // per-chunk completion of the dat0 upload (host entry)
   double* d_u = nullptr;
   double* d_y = nullptr;
   double* d_y0 = nullptr;
@@ -1516,24 +1517,39 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
     }
   }
   // u first; then the operator runs (into a zeroed buffer) while the caller's
-  // dat0 uploads on a second stream behind it; the accumulate dat0 + A(u)
-  // is one axpy before the download.
+  // dat0 uploads on a second stream behind it, in chunks; the accumulate
+  // dat0 + A(u) and the download of result chunk i start as soon as dat0
+  // chunk i has landed, so the D2H copy engine works while the H2D one is
+  // still bringing in the rest of dat0 (PCIe is full duplex).
+  constexpr int NCH = 8;
   if (!p->hstream2) {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream2, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0, cudaEventDisableTiming));
+    for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
   }
   CUDA_TRY(cudaMemcpyAsync(p->d_u, dat2, n * sizeof(double), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaEventRecord(p->ev_u, s));
   CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_u, 0));
-  CUDA_TRY(cudaMemcpyAsync(p->d_y0, dat0, n * sizeof(double), cudaMemcpyHostToDevice, p->hstream2));
-  CUDA_TRY(cudaEventRecord(p->ev_y0, p->hstream2));
+  const size_t chunk = ((n + NCH - 1) / NCH + 31) / 32 * 32;
+  for (int c = 0; c < NCH; ++c) {
+    const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
+    if (b > a)
+      CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
+                               p->hstream2));
+    CUDA_TRY(cudaEventRecord(p->ev_y0c[c], p->hstream2));
+  }
   int rc = fe_apply(p, start, end, p->d_y, p->d_u, c0, c1, FE_APPLY_OVERWRITE, s);
   if (rc) return rc;
-  CUDA_TRY(cudaStreamWaitEvent(s, p->ev_y0, 0));
-  k_add<<<std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(p->d_y, p->d_y0, (int64_t)n);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaMemcpyAsync(dat0, p->d_y, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  for (int c = 0; c < NCH; ++c) {
+    const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
+    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_y0c[c], 0));
+    if (b <= a) continue;
+    k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, s>>>(p->d_y + a, p->d_y0 + a,
+                                                                                   (int64_t)(b - a));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(dat0 + a, p->d_y + a, (b - a) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
   CUDA_TRY(cudaStreamSynchronize(s));
   return FE_OK;
 }
@@ -1565,6 +1581,8 @@ void fe_plan_destroy(fe_plan* p) {
   if (p->hstream2) cudaStreamDestroy(p->hstream2);
   if (p->ev_u) cudaEventDestroy(p->ev_u);
   if (p->ev_y0) cudaEventDestroy(p->ev_y0);
+  for (cudaEvent_t e : p->ev_y0c)
+    if (e) cudaEventDestroy(e);
   ::operator delete(p->host_params);
   delete p;
 }

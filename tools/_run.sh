@@ -1,8 +1,6 @@
 mkdir -p gpurun_out
-export FE_LIB_PATH=paper_1903_08243_b200/libfeb200_plq56.so
-python -m pytest tests -m gpu -x -q -k "C3-Q5 or C3-Q6" > gpurun_out/pytest_plq56.log 2>&1; tail -1 gpurun_out/pytest_plq56.log
-for c in C3-Q5 C3-Q6; do
-echo "plane $(python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
-echo "team $(FE_NO_PLANE=1 python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
-done > gpurun_out/sweep_plq56.txt 2>&1
-cut -c1-200 gpurun_out/sweep_plq56.txt
+python -m pytest tests -m gpu -x -q -k "device_path or golden or accumulate or C6 or fault" > gpurun_out/pytest_e2e.log 2>&1; tail -1 gpurun_out/pytest_e2e.log
+for lib in libfeb200 libfeb200_old libfeb200; do
+FE_LIB_PATH=paper_1903_08243_b200/$lib.so python bench.py --steps 10 > gpurun_out/bench_e2e_$lib.log 2>&1
+echo "$lib $(tail -1 gpurun_out/bench_e2e_$lib.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["e2e"]["value"], d["value"], d["ms_per_step"])')"
+done
