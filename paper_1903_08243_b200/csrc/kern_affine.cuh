@@ -311,6 +311,27 @@ struct KuhnTetP1 {
     constexpr unsigned rows[6] = {0x7310u, 0x5710u, 0x3720u, 0x7620u, 0x7540u, 0x6740u};
     return (int)((rows[t] >> (4 * i)) & 15u);
   }
+  __host__ __device__ static constexpr bool vertex(int) { return true; }
+};
+
+// P2 on the same 6 Kuhn tets: the 27 lattice points of the cube (8 corners,
+// 12 edge + 6 face-diagonal + 1 body-diagonal midpoints); local node order
+// vertices then edges (elements.lagrange_nodes), macro-dof ids in order of
+// first appearance
+struct KuhnTetP2 {
+  static constexpr int MC = 6, NU = 27, ND = 10;
+  __host__ __device__ static constexpr int at(int t, int i) {
+    constexpr unsigned char tab[6][10] = {{0, 1, 2, 3, 4, 5, 6, 7, 8, 9},
+                                          {0, 1, 3, 10, 4, 6, 11, 8, 12, 13},
+                                          {0, 14, 3, 2, 15, 6, 5, 16, 17, 9},
+                                          {0, 14, 18, 3, 15, 19, 6, 20, 16, 21},
+                                          {0, 22, 10, 3, 23, 11, 6, 24, 25, 13},
+                                          {0, 22, 3, 18, 23, 6, 19, 25, 26, 21}};
+    return tab[t][i];
+  }
+  __host__ __device__ static constexpr bool vertex(int k) {
+    return k == 0 || k == 1 || k == 2 || k == 3 || k == 10 || k == 14 || k == 18 || k == 22;
+  }
 };
 
 // NCX consecutive Kuhn cubes along x (cells ordered x-fastest): they share
@@ -381,7 +402,7 @@ template <int FORM, int DIM, int ND, int NQS, class PAT, bool ANALYTIC = false>
 __global__ void __launch_bounds__(128)
 macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const int32_t* __restrict__ corner,
                    int64_t mstride, int32_t m0, int32_t m1) {
-  static_assert(PAT::ND == ND && ND == DIM + 1, "macro pattern covers vertex dofs only");
+  static_assert(PAT::ND == ND, "macro pattern of this element");
   constexpr int NU = PAT::NU, MC = PAT::MC;
   const int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= m1) return;
@@ -391,7 +412,7 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
   double X[NU][DIM], w[NU], yl[NU];
 #pragma unroll
   for (int k = 0; k < NU; ++k) {
-    load_vertex<DIM>(p.mesh.coords, dof[k], X[k]);
+    if (PAT::vertex(k)) load_vertex<DIM>(p.mesh.coords, dof[k], X[k]);  // vertex dof = vertex id
     w[k] = __ldg(p.u + dof[k]);
     yl[k] = 0.0;
   }
@@ -400,8 +421,10 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
     double Xt[DIM + 1][DIM], wt[ND], yt[ND];
 #pragma unroll
     for (int i = 0; i < ND; ++i) {
+      if (i <= DIM) {
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) Xt[i][a] = X[PAT::at(t, i)][a];
+        for (int a = 0; a < DIM; ++a) Xt[i][a] = X[PAT::at(t, i)][a];
+      }
       wt[i] = w[PAT::at(t, i)];
     }
     if constexpr (ANALYTIC) p1_simplex_compute<FORM, DIM>(Xt, wt, yt);

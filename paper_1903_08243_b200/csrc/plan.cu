@@ -329,6 +329,8 @@ static void element_matrices(const fe_plan* p, bool mass, bool grads, std::vecto
 #define FE_MACRO_NCX 1
 #endif
 using MacroP1 = std::conditional_t<FE_MACRO_NCX == 1, KuhnTetP1, KuhnTetRowP1<FE_MACRO_NCX>>;
+template <int ND>
+using MacroFor = std::conditional_t<ND == 4, MacroP1, KuhnTetP2>;
 
 constexpr int affine_group(int dim, int nd) {
   return dim == 3 ? (nd == 4 ? FE_GROUP_TET_P1 : nd == 10 ? FE_GROUP_TET_P2 : 1)
@@ -441,13 +443,15 @@ int split_prepare(fe_plan* p) {
       }
     p->p1_analytic = ok;
   }
-  if (DIM == 3 && ND == 4 && !getenv("FE_NO_MACRO")) {
-    using PAT = MacroP1;
-    p->macro_mc = PAT::MC;
-    p->macro_nu = PAT::NU;
-    p->macro_pat.clear();
-    for (int t = 0; t < PAT::MC; ++t)
-      for (int i = 0; i < PAT::ND; ++i) p->macro_pat.push_back(PAT::at(t, i));
+  if constexpr (DIM == 3 && (ND == 4 || ND == 10)) {
+    if (!getenv("FE_NO_MACRO") && (ND == 4 || getenv("FE_MACRO_P2"))) {
+      using PAT = MacroFor<ND>;
+      p->macro_mc = PAT::MC;
+      p->macro_nu = PAT::NU;
+      p->macro_pat.clear();
+      for (int t = 0; t < PAT::MC; ++t)
+        for (int i = 0; i < PAT::ND; ++i) p->macro_pat.push_back(PAT::at(t, i));
+    }
   }
   return FE_OK;
 }
@@ -470,18 +474,24 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
     const int nt = (b - a + G - 1) / G;
     affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
   };
-  if constexpr (DIM == 3 && ND == 4) {
+  if constexpr (DIM == 3 && (ND == 4 || ND == 10)) {
+    using PAT = MacroFor<ND>;
     if (p->d_macro) {
       // whole macro-cells inside [start, end) on the macro kernel, ragged ends per cell
-      const int mc = MacroP1::MC;
+      const int mc = PAT::MC;
       const int32_t m0 = (start + mc - 1) / mc, m1 = end / mc;
       if (m0 < m1) {
-        if (p->p1_analytic)
-          macro_split_kernel<FORM, DIM, ND, NQS, MacroP1, true>
+        if constexpr (ND == 4) {
+          if (p->p1_analytic)
+            macro_split_kernel<FORM, DIM, ND, NQS, PAT, true>
+                <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+          else
+            macro_split_kernel<FORM, DIM, ND, NQS, PAT>
+                <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+        } else {
+          macro_split_kernel<FORM, DIM, ND, NQS, PAT>
               <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
-        else
-          macro_split_kernel<FORM, DIM, ND, NQS, MacroP1>
-              <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+        }
         per_cell(start, m0 * mc);
         per_cell(m1 * mc, end);
         CUDA_TRY(cudaGetLastError());

@@ -1,6 +1,8 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q -k "device_path or golden or accumulate or C6 or fault" > gpurun_out/pytest_e2e.log 2>&1; tail -1 gpurun_out/pytest_e2e.log
-for lib in libfeb200 libfeb200_old libfeb200; do
-FE_LIB_PATH=paper_1903_08243_b200/$lib.so python bench.py --steps 10 > gpurun_out/bench_e2e_$lib.log 2>&1
-echo "$lib $(tail -1 gpurun_out/bench_e2e_$lib.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["e2e"]["value"], d["value"], d["ms_per_step"])')"
-done
+FE_MACRO_P2=1 python -m pytest tests -m gpu -x -q -k "C2-P2 or range" > gpurun_out/pytest_p2m.log 2>&1; tail -1 gpurun_out/pytest_p2m.log
+for i in 1 2; do
+echo "macro $(FE_MACRO_P2=1 python tools/profile_apply.py --config C2-P2 --time --reps 20 2>&1 | tail -1)"
+echo "split $(python tools/profile_apply.py --config C2-P2 --time --reps 20 2>&1 | tail -1)"
+done > gpurun_out/sweep_p2macro.txt 2>&1
+cut -c1-200 gpurun_out/sweep_p2macro.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v15.log 2>&1; tail -13 gpurun_out/smoke_v15.log
