@@ -81,27 +81,29 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
           else T[c][a] = 2.0 * mu * e + (c == a ? lam * tr : 0.0);
         }
     } else if constexpr (FORM == FE_FORM_NEOHOOKEAN) {
+      // P = mu (F - F^-T) + lambda ln J F^-T = mu G + mu I + (lambda ln J - mu) F^-T
+      // with F^-T[c][a] = adj(F)[a][c] / J; the weight tw is folded into the
+      // two scalars (no inverse formed, no per-entry weight multiply)
       static_assert(VS == DIM, "vector form");
-      double F[DIM][DIM], Fi[DIM][DIM];
+      double F[DIM][DIM], A[DIM][DIM];
 #pragma unroll
       for (int c = 0; c < DIM; ++c)
 #pragma unroll
         for (int a = 0; a < DIM; ++a) F[c][a] = G[c][a] + (c == a ? 1.0 : 0.0);
-      double Jf = det_inv<DIM, FAST>(F, Fi);
-      double ll = lam * log(Jf);
+      const double Jf = det_adj<DIM>(F, A);
+      const double m = tw * mu;
+      const double s = tw * (lam * log(Jf) - mu) * recip<FAST>(Jf);
 #pragma unroll
       for (int c = 0; c < DIM; ++c)
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          double fit = Fi[a][c];  // F^{-T}[c][a]
-          T[c][a] = mu * (F[c][a] - fit) + ll * fit;
-        }
+        for (int a = 0; a < DIM; ++a) T[c][a] = fma(m, G[c][a], s * A[a][c]) + (c == a ? m : 0.0);
     } else if constexpr (FORM == FE_FORM_NEOHOOKEAN_TANGENT) {
       // dP = mu dF + (mu - lambda ln J) F^-T dF^T F^-T + lambda tr(F^-1 dF) F^-T
-      // with F = I + grad u0 (state), dF = grad du = G; F^-T dF^T F^-T = (M F^-1)^T
-      // for M = F^-1 dF
+      // with F = I + grad u0 (state), dF = grad du = G.  With F^-1 = A / J
+      // (A = adj F) and M = A dF: F^-T dF^T F^-T = (M A)^T / J^2 and
+      // tr(F^-1 dF) = tr(M) / J; the weight tw is folded into the scalars.
       static_assert(VS == DIM, "vector form");
-      double F[DIM][DIM], Fi[DIM][DIM];
+      double F[DIM][DIM], A[DIM][DIM];
 #pragma unroll
       for (int c = 0; c < DIM; ++c)
 #pragma unroll
@@ -111,8 +113,8 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
           for (int b = 0; b < DIM; ++b) s += Ji[b][a] * g0[c][b];
           F[c][a] = s + (c == a ? 1.0 : 0.0);
         }
-      double Jf = det_inv<DIM, FAST>(F, Fi);
-      const double cc = mu - lam * log(Jf);
+      const double Jf = det_adj<DIM>(F, A);
+      const double r = recip<FAST>(Jf);
       double M[DIM][DIM];
       double tr = 0.0;
 #pragma unroll
@@ -121,21 +123,26 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
         for (int b = 0; b < DIM; ++b) {
           double s = 0.0;
 #pragma unroll
-          for (int c = 0; c < DIM; ++c) s += Fi[a][c] * G[c][b];
+          for (int c = 0; c < DIM; ++c) s += A[a][c] * G[c][b];
           M[a][b] = s;
           if (a == b) tr += s;
         }
-      const double lt = lam * tr;
+      const double m = tw * mu;
+      const double r2 = tw * r * r;
+      const double c2 = (mu - lam * log(Jf)) * r2;
+      const double l2 = lam * tr * r2;
 #pragma unroll
       for (int c = 0; c < DIM; ++c)
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
-          double s = 0.0;  // (M F^-1)[a][c] = (F^-T dF^T F^-T)[c][a]
+          double s = 0.0;  // (M A)[a][c]
 #pragma unroll
-          for (int b = 0; b < DIM; ++b) s += M[a][b] * Fi[b][c];
-          T[c][a] = mu * G[c][a] + cc * s + lt * Fi[a][c];
+          for (int b = 0; b < DIM; ++b) s += M[a][b] * A[b][c];
+          T[c][a] = fma(m, G[c][a], fma(c2, s, l2 * A[a][c]));
         }
     }
+    // hyperelastic fluxes already carry the weight
+    constexpr bool WEIGHTED = FORM == FE_FORM_NEOHOOKEAN || FORM == FE_FORM_NEOHOOKEAN_TANGENT;
 #pragma unroll
     for (int c = 0; c < VS; ++c)
 #pragma unroll
@@ -143,7 +150,7 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
         double s = 0.0;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) s += Ji[b][a] * T[c][a];
-        cg[c][b] = tw * s;
+        cg[c][b] = WEIGHTED ? s : tw * s;
       }
   }
 }
