@@ -589,4 +589,118 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
     for (int c = 0; c < VS; ++c) scatter_add(p.y, (int64_t)VS * dof[j] + c, A[j][c]);
 }
 
+// ---------------------------------------------------------------------------
+// Vertex-gradient quadrature kernel for P2 simplices (C5 neo-Hookean, affine
+// tetrahedra).  The reference gradient of a P2 field is P1, so it is fixed by
+// its values at the 4 vertices: G_v = sum_i dphi_i(vertex v) u_i once per
+// cell (360 FMAs), then at every point grad_ref u = sum_v lambda_v(x_q) G_v
+// (36 FMAs instead of the 90 of the nodal sum, kernels.py:178-195).  The
+// transposed integration likewise accumulates the 4 vertex moments
+// S_v = sum_q lambda_v(x_q) flux_q (36 FMAs per point) and projects back to
+// the 10 nodes once per cell.  Exact (not an approximation): lambda_v are the
+// P1 barycentric functions, the same gphi table the geometry uses.
+// ---------------------------------------------------------------------------
+template <int NQ, int ND, int DIM, int NV>
+struct VtxParams {
+  MeshView mesh;
+  int32_t start, end;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  const double* __restrict__ mu;
+  const double* __restrict__ lam;
+  double p0, p1;
+  double qw[NQ];
+  double gphi[NQ][NV];          // barycentric (P1) values at the points
+  double dphiv[NV][ND][DIM];    // reference gradients of the P2 basis at the vertices
+};
+
+template <int FORM, int DIM, int NV, int ND, int NQ, int MINB, int UNR>
+__global__ void __launch_bounds__(128, MINB)
+quad_vtx_kernel(const __grid_constant__ VtxParams<NQ, ND, DIM, NV> p) {
+  constexpr int VS = form_vs(FORM, DIM);
+  constexpr bool STATE = form_has_state(FORM);
+  static_assert(!form_needs_values(FORM), "gradient-only forms");
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  int dof[ND];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) dof[i] = __ldg(p.mesh.map + i * cs + cell);
+  double X[NV][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) load_vertex<DIM>(p.mesh.coords, __ldg(p.mesh.vmap + v * cs + cell), X[v]);
+  // vertex values of the reference gradient: increment u (and state u0)
+  double Gv[NV][VS][DIM], G0v[STATE ? NV : 1][VS][DIM];
+  auto vertex_grad = [&](const double* __restrict__ f, double (&out)[NV][VS][DIM]) {
+    double w[ND][VS];
+#pragma unroll
+    for (int i = 0; i < ND; ++i)
+#pragma unroll
+      for (int c = 0; c < VS; ++c) w[i][c] = __ldg(f + (int64_t)VS * dof[i] + c);
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < ND; ++i) s = fma(p.dphiv[v][i][b], w[i][c], s);
+          out[v][c][b] = s;
+        }
+  };
+  vertex_grad(p.u, Gv);
+  if constexpr (STATE) vertex_grad(p.mu, G0v);
+  double J[DIM][DIM], Ji[DIM][DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+  const double absdet = fabs(det_inv<DIM, true>(J, Ji));
+  double S[NV][VS][DIM];
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < VS; ++c)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) S[v][c][b] = 0.0;
+#pragma unroll UNR
+  for (int q = 0; q < NQ; ++q) {
+    const double tw = p.qw[q] * absdet;
+    double g[VS][DIM], g0[VS][DIM], uq[VS] = {};
+#pragma unroll
+    for (int c = 0; c < VS; ++c)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        double s = 0.0, s0 = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          s = fma(p.gphi[q][v], Gv[v][c][b], s);
+          if constexpr (STATE) s0 = fma(p.gphi[q][v], G0v[v][c][b], s0);
+        }
+        g[c][b] = s;
+        g0[c][b] = s0;
+      }
+    double cv[VS], cg[VS][DIM];
+    pointwise<FORM, DIM, VS, true>(Ji, tw, uq, g, p.p0, p.p1, cv, cg, g0);
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int c = 0; c < VS; ++c)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) S[v][c][b] = fma(p.gphi[q][v], cg[c][b], S[v][c][b]);
+  }
+#pragma unroll
+  for (int j = 0; j < ND; ++j)
+#pragma unroll
+    for (int c = 0; c < VS; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) s = fma(p.dphiv[v][j][b], S[v][c][b], s);
+      scatter_add(p.y, (int64_t)VS * dof[j] + c, s);
+    }
+}
+
 }  // namespace fe

@@ -284,6 +284,83 @@ int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   return FE_OK;
 }
 
+// vertex-gradient P2 kernel (kern_quad.cuh quad_vtx_kernel): the reference
+// gradients of the P2 basis at the simplex vertices, recovered exactly from
+// the point tables (they are P1: dphi[q] = sum_v gphi[q][v] dphiv[v]) by a
+// least-squares solve of the NV x NV normal equations
+template <int FORM, int DIM, int NV, int ND, int NQ, int MINB, int UNR>
+int vtx_prepare(fe_plan* p) {
+  using P = VtxParams<NQ, ND, DIM, NV>;
+  static_assert(sizeof(P) <= 32000, "parameter block too large");
+  if (p->nq != NQ || p->nd != ND || p->nv != NV) return fail(FE_EINVAL, "vertex-gradient table size mismatch");
+  P* hp = new P();
+  double Mn[NV][NV] = {};
+  for (int q = 0; q < NQ; ++q) {
+    hp->qw[q] = p->qw[q];
+    for (int v = 0; v < NV; ++v) {
+      hp->gphi[q][v] = p->gphi[q * NV + v];
+      for (int v2 = 0; v2 < NV; ++v2) Mn[v][v2] += p->gphi[q * NV + v] * p->gphi[q * NV + v2];
+    }
+  }
+  // Gauss-Jordan inverse of the (SPD, well-conditioned) normal matrix
+  double inv[NV][NV] = {};
+  for (int v = 0; v < NV; ++v) inv[v][v] = 1.0;
+  for (int c = 0; c < NV; ++c) {
+    const double piv = Mn[c][c];
+    if (!(std::fabs(piv) > 1e-12)) { delete hp; return fail(FE_EINVAL, "singular vertex projection"); }
+    for (int k = 0; k < NV; ++k) { Mn[c][k] /= piv; inv[c][k] /= piv; }
+    for (int r = 0; r < NV; ++r)
+      if (r != c) {
+        const double f = Mn[r][c];
+        for (int k = 0; k < NV; ++k) { Mn[r][k] -= f * Mn[c][k]; inv[r][k] -= f * inv[c][k]; }
+      }
+  }
+  double worst = 0.0;
+  for (int i = 0; i < ND; ++i)
+    for (int b = 0; b < DIM; ++b) {
+      double rhs[NV] = {};
+      for (int q = 0; q < NQ; ++q)
+        for (int v = 0; v < NV; ++v) rhs[v] += p->gphi[q * NV + v] * p->dphi[((size_t)q * ND + i) * DIM + b];
+      for (int v = 0; v < NV; ++v) {
+        double s = 0.0;
+        for (int k = 0; k < NV; ++k) s += inv[v][k] * rhs[k];
+        hp->dphiv[v][i][b] = s;
+      }
+      for (int q = 0; q < NQ; ++q) {  // the gradient must be exactly P1
+        double s = 0.0;
+        for (int v = 0; v < NV; ++v) s += p->gphi[q * NV + v] * hp->dphiv[v][i][b];
+        worst = std::max(worst, std::fabs(s - p->dphi[((size_t)q * ND + i) * DIM + b]));
+      }
+    }
+  if (worst > 1e-12) {
+    delete hp;
+    return fail(FE_EUNSUPPORTED, "basis gradients are not P1 (residual %.1e)", worst);
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(P);
+  return FE_OK;
+}
+
+template <int FORM, int DIM, int NV, int ND, int NQ, int MINB, int UNR>
+int vtx_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+               const double* c0, const double*, cudaStream_t s) {
+  using P = VtxParams<NQ, ND, DIM, NV>;
+  P* hp = static_cast<P*>(p->host_params);
+  hp->mesh = mesh_view(p);
+  hp->start = start;
+  hp->end = end;
+  hp->u = u;
+  hp->y = y;
+  hp->mu = c0;  // the state u0 of a linearised form
+  hp->lam = nullptr;
+  hp->p0 = p->params[0];
+  hp->p1 = p->params[1];
+  const int n = end - start;
+  quad_vtx_kernel<FORM, DIM, NV, ND, NQ, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
 // ---------------------------------------------------------------------------
 // element-tensor kernel (affine simplices)
 // ---------------------------------------------------------------------------
@@ -943,6 +1020,18 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define QCV(FORM, CELL, DIM, K, ND, NQ)                                                      \
   {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true, 1, 3>, \
    qc_launch<FORM, DIM, DIM + 1, ND, NQ, true, 1, 3>}
+#ifndef FE_VTX_MINB
+#define FE_VTX_MINB 1
+#endif
+#ifndef FE_VTX_UNR
+#define FE_VTX_UNR 3   // measured: C5 6.07 ms at 1, 5.85 ms at 3 (profiles/r01/sweep_vtx.txt)
+#endif
+#ifndef FE_VTX_TUNR
+#define FE_VTX_TUNR 1
+#endif
+#define VTXV(FORM, CELL, DIM, K, ND, NQ, MINB, UNR)                                          \
+  {FORM, CELL, K, NQ, 6, "quad_vertex_grad", 128, vtx_prepare<FORM, DIM, DIM + 1, ND, NQ, MINB, UNR>, \
+   vtx_launch<FORM, DIM, DIM + 1, ND, NQ, MINB, UNR>}
 #define QCVU(FORM, CELL, DIM, K, ND, NQ, UNR)                                                \
   {FORM, CELL, K, NQ, 5, "quad_const", 128, qc_prepare<FORM, DIM, DIM + 1, ND, NQ, true, 1, UNR>, \
    qc_launch<FORM, DIM, DIM + 1, ND, NQ, true, 1, UNR>}
@@ -1026,6 +1115,8 @@ static const Variant kVariants[] = {
     ETV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_TETRAHEDRON, 3, 3, 20),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
     QCV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 2, 10, 27),
+    VTXV(FE_FORM_NEOHOOKEAN, FE_CELL_TETRAHEDRON, 3, 2, 10, 27, FE_VTX_MINB, FE_VTX_UNR),
+    VTXV(FE_FORM_NEOHOOKEAN_TANGENT, FE_CELL_TETRAHEDRON, 3, 2, 10, 27, FE_VTX_MINB, FE_VTX_TUNR),
     QCV(FE_FORM_NEOHOOKEAN_TANGENT, FE_CELL_TETRAHEDRON, 3, 1, 4, 8),
     // tangent P2: state + increment + output (90 doubles) in registers; the
     // point loop is not unrolled (UNR 3 spills)
@@ -1166,6 +1257,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 23 && getenv("FE_NO_PLANE1")) continue;
     if (v.priority == 26 && getenv("FE_NO_PAIR")) continue;
     if (v.priority == 27 && getenv("FE_NO_HEXQ1")) continue;
+    if (v.priority == 6 && getenv("FE_NO_VTX")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
     if (v.priority == 15 && (!getenv("FE_PATCH") || (flags & 2u))) continue;

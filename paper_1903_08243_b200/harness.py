@@ -128,10 +128,16 @@ def _interp_sumfact(d: int, p: int, q: int) -> int:
     return min(colloc, direct)
 
 
-def flops_per_cell(spec: OperatorSpec, rule=None) -> int:
-    """Frozen minimum flop count per cell.  For
-    (form, cell) pairs outside the BASELINE configs it is the quadrature
+def flops_per_cell(spec: OperatorSpec, rule=None, menu: str = "min") -> int:
+    """Minimum flop count per cell over the algorithm menu of SURVEY.md
+    Appendix B.  ``menu="min"`` (default) includes the cheaper exact
+    algorithms added in round 1 (modal split for affine P_k tets,
+    vertex-gradient P2 for the hyperelastic forms) -- SURVEY App. B allows
+    lowering F that way, and it keeps every fraction <= 1;
+    ``menu="survey"`` returns SURVEY's frozen values (reported next to it).
+    For (form, cell) pairs outside the BASELINE configs it is the quadrature
     algorithm's count, noted as such in DESIGN.md."""
+    best = menu != "survey"
     if rule is None:
         rule = quadrature_rule(spec.cell, integrand_degree(spec))
     form, cell = spec.form, spec.cell
@@ -153,7 +159,7 @@ def flops_per_cell(spec: OperatorSpec, rule=None) -> int:
         # (the frozen SURVEY values were 183 / 1,380 / 5,940 / 17,685)
         m = k * (k + 1) * (k + 2) // 6
         modal = 12 * nd * m + 15 * m + 2 * nd * nd + 2 * nd + 80
-        return min(et, quad, split, modal)
+        return min(et, quad, split, modal) if best else min(et, quad, split)
     if cell.kind == "hexahedron" and form == "laplacian_scalar":
         p, q = k + 1, rule.npoints_1d
         return 2 * _interp_sumfact(3, p, q) + 148 * q ** 3 + 36
@@ -163,14 +169,22 @@ def flops_per_cell(spec: OperatorSpec, rule=None) -> int:
         sf = 2 * d * _interp_sumfact(d, p, q) + P * q ** d + g
         dense = 4 * d * d * p ** d * q ** d + P * q ** d + g
         return min(sf, dense)
+    # vertex-gradient P2 (round 1): grad_ref u is P1, so it is interpolated
+    # from its 4 vertex values (9 x 4 FMA = 72 flops per point instead of 180)
+    # after a 720-flop projection per field, and integrated through the 4
+    # vertex moments (72 per point + 720 per cell)
     if cell.kind == "tetrahedron" and form == "neohookean" and k == 2:
-        return nq * 543 + 52
+        quad = nq * 543 + 52
+        vtx = nq * (543 - 360 + 144) + 52 + 2 * 720
+        return min(quad, vtx) if best else quad
     if cell.kind == "tetrahedron" and form == "neohookean_tangent" and k == 2:
         # per point: interpolate grad u0 and grad du (2 x 180), both to
         # physical (2 x 45), F 3, cofactor + det 32, 1/J 1, F^-1 9, ln J 1,
         # M = F^-1 dF 45, tr 2, M F^-1 45, dP 54, w|det| 10, dP J^-T 45,
         # integrate 180; per cell geometry 52
-        return nq * 832 + 52
+        quad = nq * 832 + 52
+        vtx = nq * (832 - 540 + 216) + 52 + 3 * 720
+        return min(quad, vtx) if best else quad
     # generic quadrature algorithm: interpolation and integration of values
     # (2 nd per component) and reference gradients (2 nd d per component)
     per_q = 0
@@ -198,9 +212,9 @@ def arithmetic_intensity(spec, mesh, dofmap, rule=None) -> float:
 
 
 def roofline_time(spec, mesh, dofmap, rule=None, peak_gflops=DEFAULT_PEAK_GFLOPS,
-                  bandwidth_gbs=DEFAULT_BANDWIDTH_GBS) -> float:
+                  bandwidth_gbs=DEFAULT_BANDWIDTH_GBS, menu="min") -> float:
     """T_roof = max(F C / P_fp64, B / BW) in seconds."""
-    F = flops_per_cell(spec, rule) * mesh.ncells
+    F = flops_per_cell(spec, rule, menu) * mesh.ncells
     B = bytes_per_cell(spec, mesh, dofmap) * mesh.ncells
     return max(F / (peak_gflops * 1e9), B / (bandwidth_gbs * 1e9))
 

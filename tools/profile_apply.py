@@ -51,11 +51,13 @@ def main():
         tw = time_device(fn, trials=max(args.reps, 10), warmup=3)
         F = fe.flops_per_cell(prob.spec, prob.rule) * m.ncells
         troof = roofline_time(prob.spec, m, dm, prob.rule)
+        troof_s = roofline_time(prob.spec, m, dm, prob.rule, menu="survey")
         print(json.dumps({"config": args.config, "kernel": h.info["kernel"], "ncells": m.ncells,
                           "best_ms": min(ts) * 1e3, "median_ms": float(np.median(ts)) * 1e3,
                           "gflops": F / min(ts) / 1e9, "roofline_frac": troof / min(ts),
                           "best_ms_with_zero_fill": min(tw) * 1e3,
-                          "roofline_frac_with_zero_fill": troof / min(tw)}))
+                          "roofline_frac_with_zero_fill": troof / min(tw),
+                          "roofline_frac_survey_F": troof_s / min(ts)}))
     else:
         for _ in range(args.reps):
             fn()
