@@ -42,7 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.094   # measured FP64 DMMA peak on this pool (profiles/r01_fp64_peaks.json)
-METRIC = "FP64 GFLOP/s per matrix-free operator action (frozen flop counts, SURVEY.md App. B)"
+METRIC = "FP64 GFLOP/s per matrix-free operator action (minimum flop counts of the SURVEY.md App. B menu, round-1 entries included)"
 WORKLOADS = {
     "C2": ["C2-P1", "C2-P2", "C2-P3", "C2-P4"],
     "C1": ["C1"],

@@ -1,7 +1,8 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q -k "C6 or tangent or C5" > gpurun_out/pytest_vtx2.log 2>&1; tail -1 gpurun_out/pytest_vtx2.log
-echo "vtx1 $(python tools/profile_apply.py --config C6 --time --reps 10 2>&1 | tail -1)" > gpurun_out/sweep_vtx2.txt
-echo "vtx3 $(FE_LIB_PATH=paper_1903_08243_b200/libfeb200_t3.so python tools/profile_apply.py --config C6 --time --reps 10 2>&1 | tail -1)" >> gpurun_out/sweep_vtx2.txt
-echo "qc $(FE_NO_VTX=1 python tools/profile_apply.py --config C6 --time --reps 10 2>&1 | tail -1)" >> gpurun_out/sweep_vtx2.txt
-echo "c5 $(python tools/profile_apply.py --config C5 --time --reps 10 2>&1 | tail -1)" >> gpurun_out/sweep_vtx2.txt
-cut -c1-200 gpurun_out/sweep_vtx2.txt
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v15.log 2>&1; tail -1 gpurun_out/pytest_v15.log
+tools/sweep.sh > gpurun_out/sweep_v15.txt 2>&1
+python tools/fmt_sweep.py gpurun_out/sweep_v15.txt
+python bench.py > gpurun_out/bench_v15.log 2>&1; tail -1 gpurun_out/bench_v15.log | cut -c1-400
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_v15.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_bench_v15.log 2>&1
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_v15.log 2>&1; tail -1 gpurun_out/bench_ref_v15.log | cut -c1-200
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v15b.log 2>&1; tail -2 gpurun_out/smoke_v15b.log
