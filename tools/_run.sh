@@ -1,8 +1,7 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v15.log 2>&1; tail -1 gpurun_out/pytest_v15.log
-tools/sweep.sh > gpurun_out/sweep_v15.txt 2>&1
-python tools/fmt_sweep.py gpurun_out/sweep_v15.txt
-python bench.py > gpurun_out/bench_v15.log 2>&1; tail -1 gpurun_out/bench_v15.log | cut -c1-400
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_v15.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_bench_v15.log 2>&1
-python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_v15.log 2>&1; tail -1 gpurun_out/bench_ref_v15.log | cut -c1-200
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v15b.log 2>&1; tail -2 gpurun_out/smoke_v15b.log
+python -m pytest tests -m gpu -x -q -k "C3-Q1 or hexahedron-1 or laplacian_scalar-hexahedron" > gpurun_out/pytest_hq1b.log 2>&1; tail -1 gpurun_out/pytest_hq1b.log
+for m in 3 1 4; do
+echo "new minb=$m $(FE_HEXQ1_MINB=$m python tools/profile_apply.py --config C3-Q1 --time --reps 30 2>&1 | tail -1)"
+done > gpurun_out/sweep_hq1b.txt 2>&1
+echo "old $(FE_LIB_PATH=paper_1903_08243_b200/libfeb200_old.so python tools/profile_apply.py --config C3-Q1 --time --reps 30 2>&1 | tail -1)" >> gpurun_out/sweep_hq1b.txt
+cut -c1-200 gpurun_out/sweep_hq1b.txt
