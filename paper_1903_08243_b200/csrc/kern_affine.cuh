@@ -404,11 +404,20 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
                    int64_t mstride, int32_t m0, int32_t m1) {
   static_assert(PAT::ND == ND, "macro pattern of this element");
   constexpr int NU = PAT::NU, MC = PAT::MC;
-  const int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= m1) return;
+  // persistent grid-stride loop; the macro-dof ids of the NEXT macro-cell are
+  // loaded while this one computes, so only one dependent DRAM round trip
+  // (ids -> coordinates/u) per macro-cell is exposed instead of two
+  const int stride = gridDim.x * blockDim.x;
+  int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
+  int nxt[NU];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) nxt[k] = m < m1 ? __ldg(corner + k * mstride + m) : 0;
+  for (; m < m1; m += stride) {
   int dof[NU];
 #pragma unroll
-  for (int k = 0; k < NU; ++k) dof[k] = __ldg(corner + k * mstride + m);
+  for (int k = 0; k < NU; ++k) dof[k] = nxt[k];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) nxt[k] = m + stride < m1 ? __ldg(corner + k * mstride + m + stride) : 0;
   double X[NU][DIM], w[NU], yl[NU];
 #pragma unroll
   for (int k = 0; k < NU; ++k) {
@@ -434,6 +443,7 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
   }
 #pragma unroll
   for (int k = 0; k < NU; ++k) scatter_add(p.y, dof[k], yl[k]);
+  }
 }
 
 // ---------------------------------------------------------------------------

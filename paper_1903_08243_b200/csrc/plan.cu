@@ -408,6 +408,9 @@ static void element_matrices(const fe_plan* p, bool mass, bool grads, std::vecto
 using MacroP1 = std::conditional_t<FE_MACRO_NCX == 1, KuhnTetP1, KuhnTetRowP1<FE_MACRO_NCX>>;
 template <int ND>
 using MacroFor = std::conditional_t<ND == 4, MacroP1, KuhnTetP2>;
+#ifndef FE_MACRO_WAVES_DEFAULT
+#define FE_MACRO_WAVES_DEFAULT 1
+#endif
 
 constexpr int affine_group(int dim, int nd) {
   return dim == 3 ? (nd == 4 ? FE_GROUP_TET_P1 : nd == 10 ? FE_GROUP_TET_P2 : 1)
@@ -558,16 +561,26 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
       const int mc = PAT::MC;
       const int32_t m0 = (start + mc - 1) / mc, m1 = end / mc;
       if (m0 < m1) {
+        // persistent grid: FE_MACRO_WAVES resident waves of CTAs (0 = one thread per macro-cell)
+        static const int waves = getenv("FE_MACRO_WAVES") ? atoi(getenv("FE_MACRO_WAVES")) : FE_MACRO_WAVES_DEFAULT;
+        int nb = (m1 - m0 + 127) / 128;
+        auto launch = [&](auto kfn) {
+          if (waves > 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 128, 0);
+            nb = std::min(nb, std::max(1, waves * sms * per_sm));
+          }
+          kfn<<<nb, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+        };
         if constexpr (ND == 4) {
           if (p->p1_analytic)
-            macro_split_kernel<FORM, DIM, ND, NQS, PAT, true>
-                <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+            launch(macro_split_kernel<FORM, DIM, ND, NQS, PAT, true>);
           else
-            macro_split_kernel<FORM, DIM, ND, NQS, PAT>
-                <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+            launch(macro_split_kernel<FORM, DIM, ND, NQS, PAT>);
         } else {
-          macro_split_kernel<FORM, DIM, ND, NQS, PAT>
-              <<<(m1 - m0 + 127) / 128, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+          launch(macro_split_kernel<FORM, DIM, ND, NQS, PAT>);
         }
         per_cell(start, m0 * mc);
         per_cell(m1 * mc, end);

@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q -k "C3-Q1 or hexahedron-1 or laplacian_scalar-hexahedron" > gpurun_out/pytest_hq1b.log 2>&1; tail -1 gpurun_out/pytest_hq1b.log
-for m in 3 1 4; do
-echo "new minb=$m $(FE_HEXQ1_MINB=$m python tools/profile_apply.py --config C3-Q1 --time --reps 30 2>&1 | tail -1)"
-done > gpurun_out/sweep_hq1b.txt 2>&1
-echo "old $(FE_LIB_PATH=paper_1903_08243_b200/libfeb200_old.so python tools/profile_apply.py --config C3-Q1 --time --reps 30 2>&1 | tail -1)" >> gpurun_out/sweep_hq1b.txt
-cut -c1-200 gpurun_out/sweep_hq1b.txt
+python -m pytest tests -m gpu -x -q -k "C2-P1 or macro or range or slab" > gpurun_out/pytest_mw.log 2>&1; tail -1 gpurun_out/pytest_mw.log
+for w in 0 1 2 4; do
+echo "waves=$w $(FE_MACRO_WAVES=$w python tools/profile_apply.py --config C2-P1 --time --reps 30 2>&1 | tail -1)"
+done > gpurun_out/sweep_macro_waves.txt 2>&1
+cut -c1-200 gpurun_out/sweep_macro_waves.txt
