@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q -k "C3-Q1 or hexahedron-1" > gpurun_out/pytest_hw.log 2>&1; tail -1 gpurun_out/pytest_hw.log
-for m in 3 4; do for w in 0 1 2; do
-echo "minb=$m waves=$w $(FE_HEXQ1_MINB=$m FE_HEXQ1_WAVES=$w python tools/profile_apply.py --config C3-Q1 --time --reps 30 2>&1 | tail -1)"
-done; done > gpurun_out/sweep_hq1_waves.txt 2>&1
-cut -c1-200 gpurun_out/sweep_hq1_waves.txt
+python -m pytest tests -m gpu -x -q -k "C3-Q5 or C3-Q6 or C4-hex-Q2 or C4-hex-Q3 or hexahedron-5 or hexahedron-6 or elasticity_lame-hexahedron or slab" > gpurun_out/pytest_pre.log 2>&1; tail -1 gpurun_out/pytest_pre.log
+for c in C3-Q5 C3-Q6 C4-hex-Q2 C4-hex-Q3; do
+echo "pre $(python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+echo "team $(FE_NO_PREGEO=1 python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+done > gpurun_out/sweep_pre.txt 2>&1
+cut -c1-220 gpurun_out/sweep_pre.txt
