@@ -111,6 +111,11 @@ struct fe_plan {
   cudaStream_t hstream2 = nullptr;
   cudaEvent_t ev_u = nullptr, ev_y0 = nullptr;
   cudaEvent_t ev_y0c[8] = {};  // per-chunk completion of the dat0 upload (host entry)
+  cudaEvent_t ev_uc[8] = {};   // per-chunk completion of the u upload (host entry)
+  cudaStream_t hstream_u = nullptr;
+  // host entry pipelining: cell chunks (kHostChunks, boundaries aligned to
+  // 192 cells) and the largest dof index each one reads (computed at bind)
+  std::vector<int32_t> chunk_cell, chunk_maxdof;
   double* d_u = nullptr;
   double* d_y = nullptr;
   double* d_y0 = nullptr;
@@ -1207,6 +1212,17 @@ __global__ void k_check_vmap(const int32_t* __restrict__ map0, const int32_t* __
   if (map0[(int64_t)c * nd + v] != map1[t]) *flag = 1;
 }
 
+// largest dof index read by each chunk of cells (row-major map)
+__global__ void k_chunk_maxdof(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
+                               int nchunk, int* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * nd) return;
+  const int c = (int)(t / nd);
+  int k = 0;
+  while (k + 1 < nchunk && c >= bounds[k + 1]) ++k;
+  atomicMax(out + k, rm[t]);
+}
+
 __global__ void k_check_range(const int32_t* __restrict__ m, int64_t n, int64_t hi, int* flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < n && (m[t] < 0 || m[t] >= hi)) *flag = 1;
@@ -1511,6 +1527,29 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     free_mesh(p);
     return fail(FE_EINVAL, "map entry out of range");
   }
+  {
+    // host-entry pipelining: per cell chunk, the largest dof index it reads
+    constexpr int NCH = 8;
+    p->chunk_cell.assign(NCH + 1, 0);
+    for (int c = 0; c <= NCH; ++c)
+      p->chunk_cell[c] = (int32_t)std::min<int64_t>(ncells, ((int64_t)ncells * c / NCH + 191) / 192 * 192);
+    p->chunk_cell[NCH] = ncells;
+    p->chunk_maxdof.assign(NCH, -1);
+    if (ncells > 0) {
+      int32_t* d_b = nullptr;
+      int* d_o = nullptr;
+      CUDA_TRY(cudaMalloc(&d_b, (NCH + 1) * sizeof(int32_t)));
+      CUDA_TRY(cudaMalloc(&d_o, NCH * sizeof(int)));
+      CUDA_TRY(cudaMemcpyAsync(d_b, p->chunk_cell.data(), (NCH + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemsetAsync(d_o, 0xff, NCH * sizeof(int), s));
+      const int64_t n = (int64_t)ncells * nd;
+      k_chunk_maxdof<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, d_o);
+      CUDA_TRY(cudaMemcpyAsync(p->chunk_maxdof.data(), d_o, NCH * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      cudaFree(d_b);
+      cudaFree(d_o);
+    }
+  }
   if (h_flag[1]) {
     // map0[:, :nv] is not the vertex map: keep a separate SoA vertex map
     CUDA_TRY(cudaMalloc(&p->d_vmap, (size_t)nv * p->stride * sizeof(int32_t) + 4));
@@ -1646,14 +1685,29 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   constexpr int NCH = 8;
   if (!p->hstream2) {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream2, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream_u, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0, cudaEventDisableTiming));
-    for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
+    for (int c = 0; c < NCH; ++c) {
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_uc[c], cudaEventDisableTiming));
+    }
   }
-  CUDA_TRY(cudaMemcpyAsync(p->d_u, dat2, n * sizeof(double), cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaEventRecord(p->ev_u, s));
-  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_u, 0));
   const size_t chunk = ((n + NCH - 1) / NCH + 31) / 32 * 32;
+  // u in chunks on its own stream (after the coefficient fields); the cell
+  // chunk r of the operator starts as soon as every u chunk it reads (up to
+  // its largest dof, found at bind time) has landed, so the arithmetic runs
+  // under the rest of the upload
+  CUDA_TRY(cudaEventRecord(p->ev_u, s));
+  CUDA_TRY(cudaStreamWaitEvent(p->hstream_u, p->ev_u, 0));
+  for (int c = 0; c < NCH; ++c) {
+    const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
+    if (b > a)
+      CUDA_TRY(cudaMemcpyAsync(p->d_u + a, dat2 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
+                               p->hstream_u));
+    CUDA_TRY(cudaEventRecord(p->ev_uc[c], p->hstream_u));
+  }
+  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
   for (int c = 0; c < NCH; ++c) {
     const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
     if (b > a)
@@ -1661,8 +1715,18 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
                                p->hstream2));
     CUDA_TRY(cudaEventRecord(p->ev_y0c[c], p->hstream2));
   }
-  int rc = fe_apply(p, start, end, p->d_y, p->d_u, c0, c1, FE_APPLY_OVERWRITE, s);
-  if (rc) return rc;
+  CUDA_TRY(cudaMemsetAsync(p->d_y, 0, n * sizeof(double), s));
+  const int vs = p->vs;
+  for (size_t r = 0; r + 1 < p->chunk_cell.size(); ++r) {
+    const int32_t a = std::max(start, p->chunk_cell[r]), b = std::min(end, p->chunk_cell[r + 1]);
+    if (a >= b) continue;
+    const int64_t last = (int64_t)vs * p->chunk_maxdof[r] + vs - 1;  // last u entry this chunk reads
+    const int cu = (int)std::min<int64_t>(NCH - 1, last < 0 ? 0 : (int64_t)(last / (int64_t)chunk));
+    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[cu], 0));
+    int rc = fe_apply(p, a, b, p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[NCH - 1], 0));  // stream order for the next call's reuse of d_u
   for (int c = 0; c < NCH; ++c) {
     const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
     CUDA_TRY(cudaStreamWaitEvent(s, p->ev_y0c[c], 0));
@@ -1705,6 +1769,9 @@ void fe_plan_destroy(fe_plan* p) {
   if (p->ev_y0) cudaEventDestroy(p->ev_y0);
   for (cudaEvent_t e : p->ev_y0c)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_uc)
+    if (e) cudaEventDestroy(e);
+  if (p->hstream_u) cudaStreamDestroy(p->hstream_u);
   ::operator delete(p->host_params);
   delete p;
 }

@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q -k "C3-Q5 or C3-Q6 or C4-hex-Q2 or C4-hex-Q3 or hexahedron-5 or hexahedron-6 or elasticity_lame-hexahedron or slab" > gpurun_out/pytest_pre.log 2>&1; tail -1 gpurun_out/pytest_pre.log
-for c in C3-Q5 C3-Q6 C4-hex-Q2 C4-hex-Q3; do
-echo "pre $(python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
-echo "team $(FE_NO_PREGEO=1 python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
-done > gpurun_out/sweep_pre.txt 2>&1
-cut -c1-220 gpurun_out/sweep_pre.txt
+python -m pytest tests -m gpu -x -q -k "golden or device_path or accumulate or range or fault or config or C6 or cli" > gpurun_out/pytest_e2e2.log 2>&1; tail -1 gpurun_out/pytest_e2e2.log
+for lib in libfeb200 libfeb200_old libfeb200; do
+FE_LIB_PATH=paper_1903_08243_b200/$lib.so python bench.py --steps 10 > gpurun_out/bench_e2e2_$lib.log 2>&1
+echo "$lib $(tail -1 gpurun_out/bench_e2e2_$lib.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["e2e"]["value"], d["value"], d["ms_per_step"])')"
+done
