@@ -9,7 +9,10 @@ same timing protocol as the sweep (L2 flushed, GPU spin, CUDA events):
             with no arithmetic and no scatter (torch gather + sum);
 * C1:       the operator (element_tensor kernel), accumulate protocol;
 * C1 warm:  the operator back to back with the L2 NOT flushed (inputs
-            L2-resident, as inside a solver loop).
+            L2-resident, as inside a solver loop; SURVEY 8d);
+* C1 graph: 100 applies captured in one CUDA graph, time per apply
+            (launch overhead amortised, L2-resident: the throughput of the
+            operator inside a captured solver iteration).
 
     python tools/c1_floor.py
 """
@@ -54,6 +57,19 @@ def main():
     rows["gather_map_u_us"] = best(lambda: torch.sum(u[soa], dim=0, out=out))
     rows["c1_us"] = best(lambda: h.apply(u, y), setup=lambda: y.zero_())
     rows["c1_warm_us"] = best(lambda: h.apply(u, y), flush=False)
+    try:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            h.apply(u, y)                      # warm-up on the capture stream
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(100):
+                    h.apply(u, y)
+        torch.cuda.current_stream().wait_stream(side)
+        rows["c1_graph_us_per_apply"] = best(lambda: g.replay(), flush=False) / 100
+    except Exception as e:  # capture unsupported: report why
+        rows["c1_graph_error"] = str(e)[:120]
     rows["compulsory_MB"] = 8.41
     rows["hbm_time_us"] = 8.41e6 / 6547.8e9 * 1e6
     print(json.dumps({k: round(v, 2) if isinstance(v, float) else v for k, v in rows.items()}))
