@@ -398,8 +398,11 @@ FE_DEVICE void p1_simplex_compute(const double (&X)[DIM + 1][DIM], const double 
   }
 }
 
+#ifndef FE_MACRO_MINB
+#define FE_MACRO_MINB 1
+#endif
 template <int FORM, int DIM, int ND, int NQS, class PAT, bool ANALYTIC = false>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FE_MACRO_MINB)
 macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const int32_t* __restrict__ corner,
                    int64_t mstride, int32_t m0, int32_t m1) {
   static_assert(PAT::ND == ND, "macro pattern of this element");
