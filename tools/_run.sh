@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-for lib in libfeb200 libfeb200_mm4 libfeb200_mm5 libfeb200_mm6; do
-echo "$lib $(FE_LIB_PATH=paper_1903_08243_b200/$lib.so python tools/profile_apply.py --config C2-P1 --time --reps 30 2>&1 | tail -1)"
-done > gpurun_out/sweep_macro_minb.txt 2>&1
-cut -c1-190 gpurun_out/sweep_macro_minb.txt
+python -m pytest tests -m gpu -x -q -k "C4-quad or quadrilateral-3 or quadrilateral-4" > gpurun_out/pytest_c2d.log 2>&1; tail -1 gpurun_out/pytest_c2d.log
+for c in C4-quad-Q3 C4-quad-Q4; do
+echo "cell2d $(python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+echo "pair $(FE_NO_CELL2D=1 python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
+done > gpurun_out/sweep_cell2d.txt 2>&1
+cut -c1-200 gpurun_out/sweep_cell2d.txt
