@@ -1,0 +1,80 @@
+"""Edge cases of the sm_100a path against the CPU oracle: inverted cells
+(det J < 0: the reference integrates with |det J|, kernels.py:156-167),
+shuffled cell orders (no structure for the macro-cell / lattice fast paths
+to find), an empty mesh, and repeated applies accumulating."""
+
+import numpy as np
+import pytest
+
+import paper_1903_08243_b200 as fe
+from paper_1903_08243_b200 import configs as C
+from oracle import fe_oracle as fo
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+NAMES = ["C1", "C2-P1", "C2-P2", "C2-P3", "C2-P4", "C3-Q1", "C3-Q2", "C3-Q3", "C4-quad-Q1",
+         "C4-quad-Q3", "C4-hex-Q1", "C4-hex-Q2", "C5", "C6"]
+SIZES = {"C1": 6, "C4-quad-Q1": 5, "C4-quad-Q3": 4}
+
+
+def _oracle(prob, mesh, dm):
+    P = fo.Problem(prob.spec.form, prob.spec.cell.kind, prob.spec.element.degree,
+                   prob.rule.exactness_degree, prob.spec.params)
+    return fo.assemble(P, mesh.coords, mesh.cell2vert, dm.cell2dof, prob.u, prob.mu, prob.lam,
+                       state=prob.state)
+
+
+def _gpu(prob, mesh, dm, out=None):
+    h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(), prob.rule))
+    out = np.zeros(prob.ndofs) if out is None else out
+    h(0, mesh.ncells, fe.make_bindings(mesh, dm, prob.u, out, prob.mu, prob.lam, state=prob.state))
+    return out, h.info["kernel"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_inverted_cells(name):
+    """Mirror the mesh (x -> -x): every det J changes sign."""
+    prob = C.build_problem(C.get_config(name, SIZES.get(name, 2)), seed=21)
+    coords = np.array(prob.mesh.coords)
+    coords[:, 0] *= -1.0
+    mesh = fe.Mesh(coords, prob.mesh.cell2vert, prob.mesh.cell)
+    out, kernel = _gpu(prob, mesh, prob.dofmap)
+    assert fo.rel_l2(out, _oracle(prob, mesh, prob.dofmap)) <= TOL, kernel
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_shuffled_cell_order(name):
+    prob = C.build_problem(C.get_config(name, SIZES.get(name, 2)), seed=22)
+    perm = np.random.default_rng(5).permutation(prob.mesh.ncells)
+    mesh = fe.Mesh(prob.mesh.coords, np.ascontiguousarray(prob.mesh.cell2vert[perm]), prob.mesh.cell)
+    dm = fe.DofMap(np.ascontiguousarray(prob.dofmap.cell2dof[perm]), prob.dofmap.ndofs_global,
+                   prob.dofmap.element)
+    out, kernel = _gpu(prob, mesh, dm)
+    assert fo.rel_l2(out, _oracle(prob, mesh, dm)) <= TOL, kernel
+
+
+def test_repeated_applies_accumulate():
+    prob = C.build_problem(C.get_config("C2-P3", 2), seed=23)
+    ref = _oracle(prob, prob.mesh, prob.dofmap)
+    out = np.zeros(prob.ndofs)
+    h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(), prob.rule))
+    b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out)
+    for _ in range(3):
+        h(0, prob.mesh.ncells, b)
+    assert fo.rel_l2(out, 3 * ref) <= TOL
+
+
+def test_empty_range_and_single_cell():
+    prob = C.build_problem(C.get_config("C2-P4", 1), seed=24)
+    h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(), prob.rule))
+    out = np.zeros(prob.ndofs)
+    h(0, 0, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out))
+    assert not out.any()
+    P = fo.Problem(prob.spec.form, "tetrahedron", 4, prob.rule.exactness_degree, prob.spec.params)
+    for c in (0, 5):
+        out = np.zeros(prob.ndofs)
+        h(c, c + 1, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out))
+        ref = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                          start=c, end=c + 1)
+        assert fo.rel_l2(out, ref) <= TOL
