@@ -1,6 +1,7 @@
-mkdir -p gpurun_out
-for lib in libfeb200 libfeb200_xs33 libfeb200_xs36 libfeb200_xs40; do for c in C3-Q3 C3-Q4; do
-echo "$lib $(FE_LIB_PATH=paper_1903_08243_b200/$lib.so python tools/profile_apply.py --config $c --time --reps 20 2>&1 | tail -1)"
-done; done > gpurun_out/sweep_xs.txt 2>&1
-cut -c1-175 gpurun_out/sweep_xs.txt
-FE_LIB_PATH=paper_1903_08243_b200/libfeb200_xs33.so python -m pytest tests -m gpu -x -q -k "C3-Q3 or C3-Q4" 2>&1 | tail -1
+mkdir -p gpurun_out /tmp/prof
+for c in C5 C6 C2-P1 C3-Q1 C2-P2; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'^(?!k_|spin|vectorized).*' -c 1 -o /tmp/prof/prof17_$c python tools/profile_apply.py --config $c --reps 1 > /tmp/prof/ncu17_$c.log 2>&1
+  python tools/ncu_summary.py /tmp/prof/prof17_$c.ncu-rep >> gpurun_out/ncu17_summaries.txt 2>&1
+done
+cp /tmp/prof/prof17_C5.ncu-rep /tmp/prof/prof17_C2-P1.ncu-rep gpurun_out/
+du -sh gpurun_out
