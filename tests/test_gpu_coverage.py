@@ -77,6 +77,14 @@ ALTERNATIVES = [
     ("helmholtz", "tetrahedron", 4, {"FE_DMMA_CFG": "0"}, "dmma_modal"),
     ("helmholtz", "tetrahedron", 3, {"FE_DMMA_CFG": "2"}, "dmma_modal"),
     ("laplacian_scalar", "tetrahedron", 3, {"FE_DMMA_CFG": "3"}, "dmma_modal"),
+    ("helmholtz", "tetrahedron", 1, {}, "element_split_macro"),
+    ("helmholtz", "tetrahedron", 1, {"FE_NO_P1CONST": "1"}, "element_split_macro"),
+    ("helmholtz", "tetrahedron", 1, {"FE_MACRO_WAVES": "0"}, "element_split_macro"),
+    ("helmholtz", "tetrahedron", 1, {"FE_NO_MACRO": "1"}, "element_split"),
+    ("helmholtz", "tetrahedron", 2, {"FE_MACRO_P2": "1"}, "element_split_macro"),
+    ("neohookean", "tetrahedron", 2, {}, "quad_vertex_grad"),
+    ("neohookean", "tetrahedron", 2, {"FE_NO_VTX": "1"}, "quad_const"),
+    ("neohookean_tangent", "tetrahedron", 2, {"FE_NO_VTX": "1"}, "quad_const"),
 ]
 
 
