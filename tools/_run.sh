@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-for i in 1 2; do for lib in libfeb200 libfeb200_pf libfeb200_pf2; do
-echo "$lib $(FE_LIB_PATH=paper_1903_08243_b200/$lib.so python tools/profile_apply.py --config C2-P1 --time --reps 30 2>&1 | tail -1)"
-done; done > gpurun_out/sweep_l2pf.txt 2>&1
-cut -c1-175 gpurun_out/sweep_l2pf.txt
+python -m pytest tests -m gpu -q > gpurun_out/pytest_final.log 2>&1; tail -1 gpurun_out/pytest_final.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final.log 2>&1; tail -1 gpurun_out/smoke_final.log
+python bench.py > gpurun_out/bench_final.log 2>&1; tail -1 gpurun_out/bench_final.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["e2e"]["value"], d["roofline"]["frac"], d["clocks"])'
