@@ -412,6 +412,14 @@ __global__ void __launch_bounds__(128) quad_diag_kernel(QuadParams p) {
 // threads of a warp read the same entry): no shared-memory traffic at all.
 // ---------------------------------------------------------------------------
 
+#ifndef QC_ADJ
+#define QC_ADJ 1
+#endif
+constexpr bool linear_grad_form(int form) {
+  return form == FE_FORM_LAPLACIAN_SCALAR || form == FE_FORM_LAPLACIAN || form == FE_FORM_ELASTICITY ||
+         form == FE_FORM_ELASTICITY_LAME;
+}
+
 template <int NQ, int ND, int DIM, int NV, bool VALUES, bool AFFINE>
 struct QuadConstParams {
   MeshView mesh;
@@ -524,9 +532,12 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
           J[d][1] = fma(cf[2][d], xi, cf[1][d]);
         }
       }
-      absdet = fabs(det_inv<DIM, true>(J, Ji));
+      if constexpr (QC_ADJ && linear_grad_form(FORM)) absdet = fabs(det_adj<DIM>(J, Ji));
+      else absdet = fabs(det_inv<DIM, true>(J, Ji));
     }
-    const double tw = p.qw[q] * absdet;
+    // linear gradient-only forms on non-affine cells: Ji holds adj(J) and the
+    // weight w / |det J| absorbs both 1/det factors (no inverse formed)
+    const double tw = (QC_ADJ && !AFFINE && linear_grad_form(FORM)) ? p.qw[q] * rcp(absdet) : p.qw[q] * absdet;
     double uq[VS], g[VS][DIM];
 #pragma unroll
     for (int c = 0; c < VS; ++c) {
