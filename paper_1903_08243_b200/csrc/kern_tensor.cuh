@@ -480,8 +480,14 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         }
         // fast reciprocal except in the DIRECT (Q5/Q6) variants: measured
         // (profiles/r01/sweep_rcp.txt)
-        const double det = det_inv<DIM, !DIRECT>(J, Ji);
-        const double tw = (p.w[a] * wbc) * fabs(det);
+#ifndef TK_ADJ
+#define TK_ADJ 1
+#endif
+        // linear gradient forms: Ji holds adj(J), the weight w / |det J|
+        // absorbs both 1/det factors (no inverse formed)
+        constexpr bool ADJ = TK_ADJ && linear_grad_form(FORM);
+        const double det = ADJ ? det_adj<DIM>(J, Ji) : det_inv<DIM, !DIRECT>(J, Ji);
+        const double tw = ADJ ? (p.w[a] * wbc) * recip<!DIRECT>(fabs(det)) : (p.w[a] * wbc) * fabs(det);
         double mu = p.p0, lam = p.p1;
         if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
           mu = fma(xi, dm, m0);
