@@ -68,18 +68,19 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
 #pragma unroll
         for (int a = 0; a < DIM; ++a) T[c][a] = G[c][a];
     } else if constexpr (FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_ELASTICITY_LAME) {
+      // T = 2 mu eps + lam tr(eps) I = mu (G + G^T) + lam tr(G) I (reference
+      // elasticity: eps = (G + G^T) / 2), with the weight folded into the two
+      // scalars
       static_assert(VS == DIM, "vector form");
       double tr = 0.0;
 #pragma unroll
       for (int c = 0; c < VS; ++c) tr += G[c][c];
+      const double m = tw * (FORM == FE_FORM_ELASTICITY ? 0.5 : mu);
+      const double lt = FORM == FE_FORM_ELASTICITY ? 0.0 : tw * lam * tr;
 #pragma unroll
       for (int c = 0; c < VS; ++c)
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) {
-          double e = 0.5 * (G[c][a] + G[a][c]);
-          if constexpr (FORM == FE_FORM_ELASTICITY) T[c][a] = e;
-          else T[c][a] = 2.0 * mu * e + (c == a ? lam * tr : 0.0);
-        }
+        for (int a = 0; a < DIM; ++a) T[c][a] = fma(m, G[c][a] + G[a][c], c == a ? lt : 0.0);
     } else if constexpr (FORM == FE_FORM_NEOHOOKEAN) {
       // P = mu (F - F^-T) + lambda ln J F^-T = mu G + mu I + (lambda ln J - mu) F^-T
       // with F^-T[c][a] = adj(F)[a][c] / J; the weight tw is folded into the
@@ -142,7 +143,8 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
         }
     }
     // hyperelastic fluxes already carry the weight
-    constexpr bool WEIGHTED = FORM == FE_FORM_NEOHOOKEAN || FORM == FE_FORM_NEOHOOKEAN_TANGENT;
+    constexpr bool WEIGHTED = FORM == FE_FORM_NEOHOOKEAN || FORM == FE_FORM_NEOHOOKEAN_TANGENT ||
+                              FORM == FE_FORM_ELASTICITY || FORM == FE_FORM_ELASTICITY_LAME;
 #pragma unroll
     for (int c = 0; c < VS; ++c)
 #pragma unroll
