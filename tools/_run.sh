@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q > gpurun_out/pytest_v17.log 2>&1; tail -1 gpurun_out/pytest_v17.log
-tools/sweep.sh > gpurun_out/sweep_v17.txt 2>&1
-python tools/fmt_sweep.py gpurun_out/sweep_v17.txt
-python bench.py > gpurun_out/bench_v17.log 2>&1; tail -1 gpurun_out/bench_v17.log | cut -c1-200
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v17.log 2>&1; tail -1 gpurun_out/smoke_v17.log
+for i in 1 2; do for lib in libfeb200 libfeb200_p1m3 libfeb200_p1m4; do
+echo "$lib $(FE_LIB_PATH=paper_1903_08243_b200/$lib.so python tools/profile_apply.py --config C3-Q2 --time --reps 20 2>&1 | tail -1)"
+done; done > gpurun_out/sweep_p1minb.txt 2>&1
+cut -c1-170 gpurun_out/sweep_p1minb.txt
