@@ -63,6 +63,40 @@ FE_DEVICE double recip(double x) {
   else return 1.0 / x;
 }
 
+// Natural logarithm without the library routine's slow-path branches (the
+// hyperelastic kernels take ln det F at every point; measured, the library
+// log() was 25% of C5's time).  x = 2^e m with m in [1/sqrt2, sqrt2),
+// ln m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, as an odd series in s
+// to s^23 (truncation < 2e-17 relative); e ln2 added with a two-part ln2.
+// A few ulp for positive normal x; NaN for x <= 0 or NaN (as the library).
+FE_DEVICE double fast_log(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  int e = ((hi >> 20) & 0x7ff) - 1023;
+  double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);  // [1, 2)
+  const bool big = m > 1.4142135623730951;
+  m = big ? 0.5 * m : m;
+  e = big ? e + 1 : e;
+  const double f = m - 1.0;  // exact (Sterbenz)
+  const double s = f * rcp(m + 1.0);
+  const double z = s * s;
+  double p = 1.0 / 23.0;
+  p = fma(p, z, 1.0 / 21.0);
+  p = fma(p, z, 1.0 / 19.0);
+  p = fma(p, z, 1.0 / 17.0);
+  p = fma(p, z, 1.0 / 15.0);
+  p = fma(p, z, 1.0 / 13.0);
+  p = fma(p, z, 1.0 / 11.0);
+  p = fma(p, z, 1.0 / 9.0);
+  p = fma(p, z, 1.0 / 7.0);
+  p = fma(p, z, 1.0 / 5.0);
+  p = fma(p, z, 1.0 / 3.0);
+  const double ts = 2.0 * s;
+  const double r = fma(ts * z, p, ts);  // 2s (1 + z p)
+  const double de = (double)e;
+  const double res = fma(de, 6.93147180369123816490e-01, fma(de, 1.90821492927058770002e-10, r));
+  return x > 0.0 ? res : __longlong_as_double(0x7ff8000000000000LL);
+}
+
 // determinant and inverse of a DIM x DIM matrix stored row-major J[a][b]
 template <int DIM, bool FAST = false>
 FE_DEVICE double det_inv(const double (&J)[DIM][DIM], double (&Ji)[DIM][DIM]) {

@@ -24,6 +24,9 @@ struct QuadParams {
   double p0, p1;                      // neohookean mu, lambda
 };
 
+#ifndef FE_LOG
+#define FE_LOG fast_log
+#endif
 template <int NQ, int ND, int NV, int DIM>
 struct QuadTables {
   static constexpr int qw = 0;
@@ -93,7 +96,7 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
         for (int a = 0; a < DIM; ++a) F[c][a] = G[c][a] + (c == a ? 1.0 : 0.0);
       const double Jf = det_adj<DIM>(F, A);
       const double m = tw * mu;
-      const double s = tw * (lam * log(Jf) - mu) * recip<FAST>(Jf);
+      const double s = tw * (lam * FE_LOG(Jf) - mu) * recip<FAST>(Jf);
 #pragma unroll
       for (int c = 0; c < DIM; ++c)
 #pragma unroll
@@ -130,7 +133,7 @@ FE_DEVICE void pointwise(const double (&Ji)[DIM][DIM], double tw, const double (
         }
       const double m = tw * mu;
       const double r2 = tw * r * r;
-      const double c2 = (mu - lam * log(Jf)) * r2;
+      const double c2 = (mu - lam * FE_LOG(Jf)) * r2;
       const double l2 = lam * tr * r2;
 #pragma unroll
       for (int c = 0; c < DIM; ++c)

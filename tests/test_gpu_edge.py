@@ -78,3 +78,21 @@ def test_empty_range_and_single_cell():
         ref = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
                           start=c, end=c + 1)
         assert fo.rel_l2(out, ref) <= TOL
+
+
+@pytest.mark.parametrize("name,scale", [("C5", 6.0), ("C5", 12.0), ("C6", 6.0), ("C6", 10.0)])
+def test_hyperelastic_large_deformation(name, scale):
+    """ln det F over a wide range of det F (0.10..3.3 at C5 x12, 0.15..2.2
+    at C6 x10 on this mesh; the kernels' own logarithm, common.cuh
+    fast_log) against the oracle's numpy log."""
+    prob = C.build_problem(C.get_config(name, 2), seed=25)
+    if prob.state is not None:
+        prob.state = prob.state * scale
+    else:
+        prob.u = prob.u * scale
+    try:
+        ref = _oracle(prob, prob.mesh, prob.dofmap)
+    except ValueError:
+        pytest.skip("det F <= 0 at this scale")
+    out, kernel = _gpu(prob, prob.mesh, prob.dofmap)
+    assert fo.rel_l2(out, ref) <= TOL, kernel
