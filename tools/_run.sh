@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_edge.py -q -rs -k "hyperelastic" 2>&1 | tail -3
-FE_LIB_PATH=paper_1903_08243_b200/libfeb200_old.so python -m pytest tests/test_gpu_edge.py -q -rs -k "hyperelastic" 2>&1 | tail -2
+python -m pytest tests -m gpu -q > gpurun_out/pytest_final2.log 2>&1; tail -1 gpurun_out/pytest_final2.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_final2.log 2>&1; tail -2 gpurun_out/smoke_final2.log
