@@ -42,7 +42,14 @@ FE_DEVICE void et_coeffs(const double (&X)[DIM + 1][DIM], double (&cm)[NM]) {
   for (int a = 0; a < DIM; ++a)
 #pragma unroll
     for (int b = 0; b < DIM; ++b) J[a][b] = X[b + 1][a] - X[0][a];
-  double ad = fabs(det_inv<DIM>(J, Ji));
+  double ad;
+  if constexpr (FORM == FE_FORM_MASS) {
+    double A[DIM][DIM];  // the mass form needs |det J| only: no inverse, no division
+    ad = fabs(det_adj<DIM>(J, A));
+    (void)Ji;
+  } else {
+    ad = fabs(det_inv<DIM>(J, Ji));
+  }
   int m = 0;
   if constexpr (FORM == FE_FORM_MASS || FORM == FE_FORM_HELMHOLTZ) cm[m++] = ad;
   if constexpr (FORM != FE_FORM_MASS) {
