@@ -110,7 +110,7 @@ struct fe_plan {
   cudaStream_t hstream = nullptr;
   cudaStream_t hstream2 = nullptr;
   cudaEvent_t ev_u = nullptr, ev_y0 = nullptr;
-  cudaEvent_t ev_y0c[8] = {};  // per-chunk completion of the dat0 upload (host entry)
+  cudaEvent_t ev_y0c[32] = {};  // per-chunk completion of the dat0 upload (host entry)
   cudaEvent_t ev_uc[8] = {};   // per-chunk completion of the u upload (host entry)
   cudaStream_t hstream_u = nullptr;
   // host entry pipelining: cell chunks (kHostChunks, boundaries aligned to
@@ -1632,6 +1632,9 @@ int fe_wrap(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* 
   return fe_apply(p, start, end, dat0, dat2, dat3, dat4, FE_APPLY_ACCUMULATE, stream);
 }
 
+#ifndef FE_HOST_YCHUNKS
+#define FE_HOST_YCHUNKS 8
+#endif
 int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat1,
                  const double* dat2, const double* dat3, const double* dat4,
                  const int32_t* map0, const int32_t* map1) {
@@ -1682,16 +1685,16 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   // dat0 + A(u) and the download of result chunk i start as soon as dat0
   // chunk i has landed, so the D2H copy engine works while the H2D one is
   // still bringing in the rest of dat0 (PCIe is full duplex).
-  constexpr int NCH = 8;
+  constexpr int NCH = 8;     // u chunks (operator cell chunks follow them)
+  constexpr int NYC = FE_HOST_YCHUNKS;  // dat0 / result chunks (download tail = 1/NYC of y)
+  static_assert(NYC <= 32, "ev_y0c size");
   if (!p->hstream2) {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream2, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream_u, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0, cudaEventDisableTiming));
-    for (int c = 0; c < NCH; ++c) {
-      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
-      CUDA_TRY(cudaEventCreateWithFlags(&p->ev_uc[c], cudaEventDisableTiming));
-    }
+    for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_uc[c], cudaEventDisableTiming));
+    for (int c = 0; c < NYC; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
   }
   const size_t chunk = ((n + NCH - 1) / NCH + 31) / 32 * 32;
   // u in chunks on its own stream (after the coefficient fields); the cell
@@ -1708,8 +1711,9 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
     CUDA_TRY(cudaEventRecord(p->ev_uc[c], p->hstream_u));
   }
   CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
-  for (int c = 0; c < NCH; ++c) {
-    const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
+  const size_t ychunk = ((n + NYC - 1) / NYC + 31) / 32 * 32;
+  for (int c = 0; c < NYC; ++c) {
+    const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
     if (b > a)
       CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
                                p->hstream2));
@@ -1727,8 +1731,8 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
     if (rc) return rc;
   }
   CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[NCH - 1], 0));  // stream order for the next call's reuse of d_u
-  for (int c = 0; c < NCH; ++c) {
-    const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
+  for (int c = 0; c < NYC; ++c) {
+    const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
     CUDA_TRY(cudaStreamWaitEvent(s, p->ev_y0c[c], 0));
     if (b <= a) continue;
     k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, s>>>(p->d_y + a, p->d_y0 + a,
