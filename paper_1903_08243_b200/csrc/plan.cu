@@ -1049,7 +1049,7 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define FE_VTX_MINB 1
 #endif
 #ifndef FE_VTX_UNR
-#define FE_VTX_UNR 3   // measured: C5 6.07 ms at 1, 5.85 ms at 3 (profiles/r01/sweep_vtx.txt)
+#define FE_VTX_UNR 2   // measured with the fast log: C5 5.62 ms at 1, 5.17 at 2, 5.34 at 3 (profiles/r01/sweep_c5unr.txt)
 #endif
 #ifndef FE_VTX_TUNR
 #define FE_VTX_TUNR 1

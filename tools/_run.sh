@@ -1,7 +1,5 @@
 mkdir -p gpurun_out
-python tools/pcie_bw.py
-for i in 1 2 3; do for lib in libfeb200 libfeb200_y16; do
-FE_LIB_PATH=paper_1903_08243_b200/$lib.so python bench.py --steps 10 > gpurun_out/b.log 2>&1
-echo "$lib $(tail -1 gpurun_out/b.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["e2e"]["value"])')"
-done; done > gpurun_out/ych.txt
-cat gpurun_out/ych.txt
+for lib in libfeb200 libfeb200_u1 libfeb200_u2; do
+echo "$lib $(FE_LIB_PATH=paper_1903_08243_b200/$lib.so python tools/profile_apply.py --config C5 --time --reps 10 2>&1 | tail -1)"
+done > gpurun_out/sweep_c5unr.txt 2>&1
+cut -c1-150 gpurun_out/sweep_c5unr.txt
