@@ -16,6 +16,10 @@
 #include <type_traits>
 
 #include "common.cuh"
+
+#ifndef FE_HOST_YCHUNKS
+#define FE_HOST_YCHUNKS 8  // result chunks of the host entry
+#endif
 #include "kern_affine.cuh"
 #include "kern_plane.cuh"
 #include "kern_plane1.cuh"
@@ -113,6 +117,11 @@ struct fe_plan {
   cudaEvent_t ev_y0c[32] = {};  // per-chunk completion of the dat0 upload (host entry)
   cudaEvent_t ev_uc[8] = {};   // per-chunk completion of the u upload (host entry)
   cudaStream_t hstream_u = nullptr;
+  cudaStream_t hstream_d = nullptr;  // result downloads (host entry)
+  cudaEvent_t ev_cell[8] = {};       // completion of each cell chunk (host entry)
+  // per result chunk: the last cell chunk that scatters into it (computed at
+  // bind), so its download starts while later cell chunks still run
+  std::vector<int32_t> ychunk_last;
   // host entry pipelining: cell chunks (kHostChunks, boundaries aligned to
   // 192 cells) and the largest dof index each one reads (computed at bind)
   std::vector<int32_t> chunk_cell, chunk_maxdof;
@@ -1212,6 +1221,21 @@ __global__ void k_check_vmap(const int32_t* __restrict__ map0, const int32_t* __
   if (map0[(int64_t)c * nd + v] != map1[t]) *flag = 1;
 }
 
+// per result chunk (ychunk entries of the vs-interleaved result), the last
+// cell chunk whose scatter touches it (row-major map)
+__global__ void k_ychunk_last(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
+                              int nchunk, int vs, int64_t ychunk, int* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * nd) return;
+  const int c = (int)(t / nd);
+  int k = 0;
+  while (k + 1 < nchunk && c >= bounds[k + 1]) ++k;
+  const int64_t e = (int64_t)vs * rm[t];
+  const int y0 = (int)(e / ychunk), y1 = (int)((e + vs - 1) / ychunk);
+  if (out[y0] < k) atomicMax(out + y0, k);
+  if (y1 != y0 && out[y1] < k) atomicMax(out + y1, k);
+}
+
 // largest dof index read by each chunk of cells (row-major map)
 __global__ void k_chunk_maxdof(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
                                int nchunk, int* __restrict__ out) {
@@ -1535,6 +1559,7 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
       p->chunk_cell[c] = (int32_t)std::min<int64_t>(ncells, ((int64_t)ncells * c / NCH + 191) / 192 * 192);
     p->chunk_cell[NCH] = ncells;
     p->chunk_maxdof.assign(NCH, -1);
+    p->ychunk_last.assign(FE_HOST_YCHUNKS, 0);
     if (ncells > 0) {
       int32_t* d_b = nullptr;
       int* d_o = nullptr;
@@ -1546,6 +1571,19 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
       k_chunk_maxdof<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, d_o);
       CUDA_TRY(cudaMemcpyAsync(p->chunk_maxdof.data(), d_o, NCH * sizeof(int), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
+      {
+        constexpr int NYC = FE_HOST_YCHUNKS;
+        const int64_t ny = (int64_t)p->vs * p->nglobal;
+        const int64_t ychunk = ((ny + NYC - 1) / NYC + 31) / 32 * 32;
+        int* d_y = nullptr;
+        CUDA_TRY(cudaMalloc(&d_y, NYC * sizeof(int)));
+        CUDA_TRY(cudaMemsetAsync(d_y, 0, NYC * sizeof(int), s));
+        k_ychunk_last<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, p->vs,
+                                                               ychunk, d_y);
+        CUDA_TRY(cudaMemcpyAsync(p->ychunk_last.data(), d_y, NYC * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        cudaFree(d_y);
+      }
       cudaFree(d_b);
       cudaFree(d_o);
     }
@@ -1632,9 +1670,6 @@ int fe_wrap(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* 
   return fe_apply(p, start, end, dat0, dat2, dat3, dat4, FE_APPLY_ACCUMULATE, stream);
 }
 
-#ifndef FE_HOST_YCHUNKS
-#define FE_HOST_YCHUNKS 8
-#endif
 int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat1,
                  const double* dat2, const double* dat3, const double* dat4,
                  const int32_t* map0, const int32_t* map1) {
@@ -1680,27 +1715,29 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
       c1 = p->d_c1;
     }
   }
-  // u first; then the operator runs (into a zeroed buffer) while the caller's
-  // dat0 uploads on a second stream behind it, in chunks; the accumulate
-  // dat0 + A(u) and the download of result chunk i start as soon as dat0
-  // chunk i has landed, so the D2H copy engine works while the H2D one is
-  // still bringing in the rest of dat0 (PCIe is full duplex).
+  // u first, in chunks on its own stream; cell chunk r of the operator
+  // starts as soon as every u chunk it reads has landed (largest dof per
+  // cell chunk, found at bind).  Result chunk c is final once the last cell
+  // chunk scattering into it (ychunk_last, found at bind) is done: its
+  // download then starts on a third stream while later cell chunks run and
+  // the rest of u is still uploading (PCIe is full duplex).  Accumulate
+  // semantics: result chunks whose dat0 is all zero (the common y = A u call,
+  // detected on the host while u uploads) are downloaded straight into dat0;
+  // the others upload dat0, add on the device, then download.
   constexpr int NCH = 8;     // u chunks (operator cell chunks follow them)
-  constexpr int NYC = FE_HOST_YCHUNKS;  // dat0 / result chunks (download tail = 1/NYC of y)
+  constexpr int NYC = FE_HOST_YCHUNKS;  // dat0 / result chunks
   static_assert(NYC <= 32, "ev_y0c size");
   if (!p->hstream2) {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream2, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream_u, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream_d, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0, cudaEventDisableTiming));
     for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_uc[c], cudaEventDisableTiming));
+    for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_cell[c], cudaEventDisableTiming));
     for (int c = 0; c < NYC; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
   }
   const size_t chunk = ((n + NCH - 1) / NCH + 31) / 32 * 32;
-  // u in chunks on its own stream (after the coefficient fields); the cell
-  // chunk r of the operator starts as soon as every u chunk it reads (up to
-  // its largest dof, found at bind time) has landed, so the arithmetic runs
-  // under the rest of the upload
   CUDA_TRY(cudaEventRecord(p->ev_u, s));
   CUDA_TRY(cudaStreamWaitEvent(p->hstream_u, p->ev_u, 0));
   for (int c = 0; c < NCH; ++c) {
@@ -1710,36 +1747,63 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
                                p->hstream_u));
     CUDA_TRY(cudaEventRecord(p->ev_uc[c], p->hstream_u));
   }
-  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
   const size_t ychunk = ((n + NYC - 1) / NYC + 31) / 32 * 32;
+  // which dat0 chunks are all zero (+0.0 or -0.0); scanned while u uploads
+  int nonzero[NYC] = {};
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)NYC * 64; ++i) {
+    const int c = (int)(i / 64), part = (int)(i % 64);
+    const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
+    const size_t w = (b - a + 63) / 64;
+    const size_t lo = std::min(b, a + part * w), hi = std::min(b, lo + w);
+    uint64_t acc = 0;
+    const uint64_t* y = reinterpret_cast<const uint64_t*>(dat0);
+    for (size_t k0 = lo; k0 < hi && !acc; k0 += 1024)  // stops at the first nonzero block
+      for (size_t k = k0; k < std::min(hi, k0 + 1024); ++k) acc |= y[k] << 1;  // drop the sign bit
+    if (acc) {
+#pragma omp atomic write
+      nonzero[c] = 1;
+    }
+  }
+  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
   for (int c = 0; c < NYC; ++c) {
     const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
-    if (b > a)
+    if (nonzero[c] && b > a)
       CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
                                p->hstream2));
     CUDA_TRY(cudaEventRecord(p->ev_y0c[c], p->hstream2));
   }
   CUDA_TRY(cudaMemsetAsync(p->d_y, 0, n * sizeof(double), s));
   const int vs = p->vs;
-  for (size_t r = 0; r + 1 < p->chunk_cell.size(); ++r) {
+  const int ncc = (int)p->chunk_cell.size() - 1;
+  for (int r = 0; r < ncc; ++r) {
     const int32_t a = std::max(start, p->chunk_cell[r]), b = std::min(end, p->chunk_cell[r + 1]);
-    if (a >= b) continue;
-    const int64_t last = (int64_t)vs * p->chunk_maxdof[r] + vs - 1;  // last u entry this chunk reads
-    const int cu = (int)std::min<int64_t>(NCH - 1, last < 0 ? 0 : (int64_t)(last / (int64_t)chunk));
-    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[cu], 0));
-    int rc = fe_apply(p, a, b, p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
-    if (rc) return rc;
+    if (a < b) {
+      const int64_t last = (int64_t)vs * p->chunk_maxdof[r] + vs - 1;  // last u entry this chunk reads
+      const int cu = (int)std::min<int64_t>(NCH - 1, last < 0 ? 0 : (int64_t)(last / (int64_t)chunk));
+      CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[cu], 0));
+      int rc = fe_apply(p, a, b, p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaEventRecord(p->ev_cell[r], s));
   }
   CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[NCH - 1], 0));  // stream order for the next call's reuse of d_u
   for (int c = 0; c < NYC; ++c) {
     const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
-    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_y0c[c], 0));
+    const int r = ncc > 0 ? std::min(ncc - 1, std::max(0, (int)p->ychunk_last[c])) : -1;
+    CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, r >= 0 ? p->ev_cell[r] : p->ev_uc[NCH - 1], 0));
     if (b <= a) continue;
-    k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, s>>>(p->d_y + a, p->d_y0 + a,
-                                                                                   (int64_t)(b - a));
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(dat0 + a, p->d_y + a, (b - a) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (nonzero[c]) {
+      CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, p->ev_y0c[c], 0));
+      k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, p->hstream_d>>>(
+          p->d_y + a, p->d_y0 + a, (int64_t)(b - a));
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaMemcpyAsync(dat0 + a, p->d_y + a, (b - a) * sizeof(double), cudaMemcpyDeviceToHost,
+                             p->hstream_d));
   }
+  CUDA_TRY(cudaStreamSynchronize(p->hstream_d));
+  CUDA_TRY(cudaStreamSynchronize(p->hstream2));
   CUDA_TRY(cudaStreamSynchronize(s));
   return FE_OK;
 }
@@ -1776,6 +1840,9 @@ void fe_plan_destroy(fe_plan* p) {
   for (cudaEvent_t e : p->ev_uc)
     if (e) cudaEventDestroy(e);
   if (p->hstream_u) cudaStreamDestroy(p->hstream_u);
+  if (p->hstream_d) cudaStreamDestroy(p->hstream_d);
+  for (cudaEvent_t e : p->ev_cell)
+    if (e) cudaEventDestroy(e);
   ::operator delete(p->host_params);
   delete p;
 }

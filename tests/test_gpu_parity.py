@@ -244,5 +244,37 @@ def test_tangent_matches_central_difference_of_gpu_residual():
 
     fd = (residual(prob.state + eps * prob.u) - residual(prob.state - eps * prob.u)) / (2 * eps)
     out = np.zeros(prob.ndofs)
-    ht(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, state=prob.state))
+    ht(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, mu, lam, state=prob.state))
     assert fe.harness.rel_l2(out, fd) < 1e-6
+
+
+@pytest.mark.parametrize("name,size", [("C2-P1", 32), ("C2-P4", 12), ("C4-quad-Q2", 160), ("C5", 16)])
+def test_host_entry_mixed_zero_chunks(name, size):
+    """Host entry (fe_wrap_host): result chunks whose dat0 is all zero are
+    downloaded directly, the others are uploaded and accumulated, and each
+    result chunk is downloaded as soon as its last cell chunk is done.  dat0
+    here mixes zero, -0.0 and nonzero chunks; a cell sub-range is applied
+    too (accumulate semantics, reference codegen.py:168-169)."""
+    prob = C.build_problem(C.get_config(name, size), seed=6)
+    h = handle_for(prob.spec, prob.rule)
+    mu, lam = getattr(prob, "mu", None), getattr(prob, "lam", None)
+    ref_full = oracle_fn(prob.spec, prob.mesh, prob.dofmap, prob.rule, prob.u, mu, lam,
+                         state=prob.state)
+    out = np.zeros_like(ref_full)
+    flat = out.reshape(-1)
+    m = flat.size
+    rng = np.random.default_rng(1)
+    y0 = np.zeros(m)
+    y0[m // 8: m // 4] = rng.uniform(-1, 1, m // 4 - m // 8)   # one nonzero stripe
+    y0[m // 2] = 3.0                                              # a single nonzero entry
+    y0[-(m // 8):] = -0.0                                         # negative zeros
+    flat[:] = y0
+    h(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, mu, lam, state=prob.state))
+    assert fe.harness.rel_l2(out.reshape(-1) - y0, ref_full.reshape(-1)) <= TOL
+    # sub-range [0, half): zero dat0, then the second half accumulated on top
+    out2 = np.zeros_like(ref_full)
+    half = prob.mesh.ncells // 2
+    b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out2, mu, lam, state=prob.state)
+    h(0, half, b)
+    h(half, prob.mesh.ncells, b)
+    assert fe.harness.rel_l2(out2, ref_full) <= TOL
