@@ -360,7 +360,7 @@ def run_ours(args):
     value = world * flop_step * args.steps / t_total / 1e9
     if rank == 0:
         peaks = measured_peaks()
-        e2e = run_e2e(ops, max(2, min(args.steps, 5)))
+        e2e = run_e2e(ops, max(3, min(args.steps, 20)))
         dom = int(np.argmax([op["F"] * op["C"] for op in ops]))
         t_dom = per_op[dom] / args.steps
         achieved = ops[dom]["F"] * ops[dom]["C"] / t_dom / 1e12

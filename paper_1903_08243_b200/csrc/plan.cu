@@ -20,6 +20,9 @@
 #ifndef FE_HOST_YCHUNKS
 #define FE_HOST_YCHUNKS 8  // result chunks of the host entry
 #endif
+#ifndef FE_HOST_UCHUNKS
+#define FE_HOST_UCHUNKS 8  // u / cell chunks of the host entry
+#endif
 #include "kern_affine.cuh"
 #include "kern_plane.cuh"
 #include "kern_plane1.cuh"
@@ -115,10 +118,10 @@ struct fe_plan {
   cudaStream_t hstream2 = nullptr;
   cudaEvent_t ev_u = nullptr, ev_y0 = nullptr;
   cudaEvent_t ev_y0c[32] = {};  // per-chunk completion of the dat0 upload (host entry)
-  cudaEvent_t ev_uc[8] = {};   // per-chunk completion of the u upload (host entry)
+  cudaEvent_t ev_uc[32] = {};   // per-chunk completion of the u upload (host entry)
   cudaStream_t hstream_u = nullptr;
   cudaStream_t hstream_d = nullptr;  // result downloads (host entry)
-  cudaEvent_t ev_cell[8] = {};       // completion of each cell chunk (host entry)
+  cudaEvent_t ev_cell[32] = {};       // completion of each cell chunk (host entry)
   // per result chunk: the last cell chunk that scatters into it (computed at
   // bind), so its download starts while later cell chunks still run
   std::vector<int32_t> ychunk_last;
@@ -1553,7 +1556,7 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
   }
   {
     // host-entry pipelining: per cell chunk, the largest dof index it reads
-    constexpr int NCH = 8;
+    constexpr int NCH = FE_HOST_UCHUNKS;
     p->chunk_cell.assign(NCH + 1, 0);
     for (int c = 0; c <= NCH; ++c)
       p->chunk_cell[c] = (int32_t)std::min<int64_t>(ncells, ((int64_t)ncells * c / NCH + 191) / 192 * 192);
@@ -1724,7 +1727,8 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   // semantics: result chunks whose dat0 is all zero (the common y = A u call,
   // detected on the host while u uploads) are downloaded straight into dat0;
   // the others upload dat0, add on the device, then download.
-  constexpr int NCH = 8;     // u chunks (operator cell chunks follow them)
+  constexpr int NCH = FE_HOST_UCHUNKS;  // u chunks (operator cell chunks follow them)
+  static_assert(NCH <= 32, "ev_uc size");
   constexpr int NYC = FE_HOST_YCHUNKS;  // dat0 / result chunks
   static_assert(NYC <= 32, "ev_y0c size");
   if (!p->hstream2) {

@@ -244,7 +244,7 @@ def test_tangent_matches_central_difference_of_gpu_residual():
 
     fd = (residual(prob.state + eps * prob.u) - residual(prob.state - eps * prob.u)) / (2 * eps)
     out = np.zeros(prob.ndofs)
-    ht(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, mu, lam, state=prob.state))
+    ht(0, prob.mesh.ncells, fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, state=prob.state))
     assert fe.harness.rel_l2(out, fd) < 1e-6
 
 
