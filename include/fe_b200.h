@@ -162,9 +162,12 @@ int fe_wrap(fe_plan* plan, int32_t start, int32_t end, double* dat0,
             const double* dat4, const int32_t* map0, const int32_t* map1, void* stream);
 
 /* Reference-order entry on HOST pointers (the drop-in for a ctypes caller
- * holding numpy buffers): uploads dat0/dat2 (+ dat3/dat4), applies,
- * downloads dat0; synchronous.  The mesh is re-bound when dat1/map0/map1
- * differ from the bound host pointers. */
+ * holding numpy buffers): uploads dat2 (+ dat3/dat4), applies, and
+ * returns dat0 + A(u) in dat0; synchronous.  dat0 is scanned per chunk on
+ * the host: all-zero chunks (+0.0 / -0.0) are not uploaded, the others are
+ * uploaded and accumulated on the device; each result chunk is downloaded as
+ * soon as the last cell chunk scattering into it is done.  The mesh is
+ * re-bound when dat1/map0/map1 differ from the bound host pointers. */
 int fe_wrap_host(fe_plan* plan, int32_t start, int32_t end, double* dat0,
                  const double* dat1, const double* dat2, const double* dat3,
                  const double* dat4, const int32_t* map0, const int32_t* map1);
