@@ -1752,31 +1752,8 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
     CUDA_TRY(cudaEventRecord(p->ev_uc[c], p->hstream_u));
   }
   const size_t ychunk = ((n + NYC - 1) / NYC + 31) / 32 * 32;
-  // which dat0 chunks are all zero (+0.0 or -0.0); scanned while u uploads
-  int nonzero[NYC] = {};
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < (int64_t)NYC * 64; ++i) {
-    const int c = (int)(i / 64), part = (int)(i % 64);
-    const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
-    const size_t w = (b - a + 63) / 64;
-    const size_t lo = std::min(b, a + part * w), hi = std::min(b, lo + w);
-    uint64_t acc = 0;
-    const uint64_t* y = reinterpret_cast<const uint64_t*>(dat0);
-    for (size_t k0 = lo; k0 < hi && !acc; k0 += 1024)  // stops at the first nonzero block
-      for (size_t k = k0; k < std::min(hi, k0 + 1024); ++k) acc |= y[k] << 1;  // drop the sign bit
-    if (acc) {
-#pragma omp atomic write
-      nonzero[c] = 1;
-    }
-  }
-  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
-  for (int c = 0; c < NYC; ++c) {
-    const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
-    if (nonzero[c] && b > a)
-      CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
-                               p->hstream2));
-    CUDA_TRY(cudaEventRecord(p->ev_y0c[c], p->hstream2));
-  }
+  // the operator first (it does not read dat0): memset + one launch per cell
+  // chunk, each gated on the u chunks it reads
   CUDA_TRY(cudaMemsetAsync(p->d_y, 0, n * sizeof(double), s));
   const int vs = p->vs;
   const int ncc = (int)p->chunk_cell.size() - 1;
@@ -1792,12 +1769,39 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
     CUDA_TRY(cudaEventRecord(p->ev_cell[r], s));
   }
   CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[NCH - 1], 0));  // stream order for the next call's reuse of d_u
-  for (int c = 0; c < NYC; ++c) {
+  // then, per result chunk in the order the chunks become final (one stream:
+  // a chunk waiting for the last cell chunk must not hold back the others;
+  // with vertex dofs numbered first, chunk 0 is final only at the end):
+  // scan its dat0 on the host (all +0.0/-0.0 -> not uploaded), otherwise
+  // upload it behind u and add it on the device, then download
+  int order[NYC];
+  for (int c = 0; c < NYC; ++c) order[c] = c;
+  std::stable_sort(order, order + NYC, [&](int x, int y) { return p->ychunk_last[x] < p->ychunk_last[y]; });
+  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
+  const uint64_t* ybits = reinterpret_cast<const uint64_t*>(dat0);
+  for (int oc = 0; oc < NYC; ++oc) {
+    const int c = order[oc];
     const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
+    int nonzero = 0;
+    if (b > a) {
+      constexpr int NP = 64;
+      const size_t w = (b - a + NP - 1) / NP;
+#pragma omp parallel for schedule(static) reduction(| : nonzero)
+      for (int part = 0; part < NP; ++part) {
+        const size_t lo = std::min(b, a + part * w), hi = std::min(b, lo + w);
+        uint64_t acc = 0;
+        for (size_t k0 = lo; k0 < hi && !acc; k0 += 1024)  // stops at the first nonzero block
+          for (size_t k = k0; k < std::min(hi, k0 + 1024); ++k) acc |= ybits[k] << 1;  // drop the sign bit
+        nonzero |= acc != 0;
+      }
+    }
     const int r = ncc > 0 ? std::min(ncc - 1, std::max(0, (int)p->ychunk_last[c])) : -1;
     CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, r >= 0 ? p->ev_cell[r] : p->ev_uc[NCH - 1], 0));
     if (b <= a) continue;
-    if (nonzero[c]) {
+    if (nonzero) {
+      CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
+                               p->hstream2));
+      CUDA_TRY(cudaEventRecord(p->ev_y0c[c], p->hstream2));
       CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, p->ev_y0c[c], 0));
       k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, p->hstream_d>>>(
           p->d_y + a, p->d_y0 + a, (int64_t)(b - a));
