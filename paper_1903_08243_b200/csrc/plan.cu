@@ -125,6 +125,7 @@ struct fe_plan {
   // per result chunk: the last cell chunk that scatters into it (computed at
   // bind), so its download starts while later cell chunks still run
   std::vector<int32_t> ychunk_last;
+  std::vector<int64_t> ybound;  // result chunk boundaries (vertex dofs, when numbered first, are chunk 0)
   // host entry pipelining: cell chunks (kHostChunks, boundaries aligned to
   // 192 cells) and the largest dof index each one reads (computed at bind)
   std::vector<int32_t> chunk_cell, chunk_maxdof;
@@ -1224,19 +1225,23 @@ __global__ void k_check_vmap(const int32_t* __restrict__ map0, const int32_t* __
   if (map0[(int64_t)c * nd + v] != map1[t]) *flag = 1;
 }
 
-// per result chunk (ychunk entries of the vs-interleaved result), the last
-// cell chunk whose scatter touches it (row-major map)
+// per result chunk ([ybound[k], ybound[k+1]) of the vs-interleaved result),
+// the last cell chunk whose scatter touches it (row-major map)
 __global__ void k_ychunk_last(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
-                              int nchunk, int vs, int64_t ychunk, int* __restrict__ out) {
+                              int nchunk, int vs, const int64_t* __restrict__ ybound, int ny,
+                              int* __restrict__ out) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)nc * nd) return;
   const int c = (int)(t / nd);
   int k = 0;
   while (k + 1 < nchunk && c >= bounds[k + 1]) ++k;
   const int64_t e = (int64_t)vs * rm[t];
-  const int y0 = (int)(e / ychunk), y1 = (int)((e + vs - 1) / ychunk);
-  if (out[y0] < k) atomicMax(out + y0, k);
-  if (y1 != y0 && out[y1] < k) atomicMax(out + y1, k);
+  int y0 = 0;
+  while (y0 + 1 < ny && e >= ybound[y0 + 1]) ++y0;
+  int y1 = y0;
+  while (y1 + 1 < ny && e + vs - 1 >= ybound[y1 + 1]) ++y1;
+  for (int y = y0; y <= y1; ++y)
+    if (out[y] < k) atomicMax(out + y, k);
 }
 
 // largest dof index read by each chunk of cells (row-major map)
@@ -1563,6 +1568,26 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     p->chunk_cell[NCH] = ncells;
     p->chunk_maxdof.assign(NCH, -1);
     p->ychunk_last.assign(FE_HOST_YCHUNKS, 0);
+    {
+      // result chunks: when the vertex dofs are numbered first (map0[:, :nv]
+      // is the vertex map) and are a small part of the result, they form
+      // chunk 0 on their own -- every cell chunk scatters into them, so that
+      // chunk is final only at the end and should be short; the rest is
+      // split evenly (32-entry aligned)
+      constexpr int NYC = FE_HOST_YCHUNKS;
+      const int64_t ny = (int64_t)p->vs * p->nglobal;
+      const int64_t vert = h_flag[1] ? 0 : (int64_t)p->vs * p->nverts;
+      p->ybound.assign(NYC + 1, ny);
+      p->ybound[0] = 0;
+      if (NYC > 1 && vert > 0 && vert < ny / NYC) {
+        p->ybound[1] = vert;
+        for (int c = 2; c < NYC; ++c)
+          p->ybound[c] = std::min(ny, vert + (((ny - vert) * (c - 1) / (NYC - 1)) + 31) / 32 * 32);
+      } else {
+        const int64_t ychunk = ((ny + NYC - 1) / NYC + 31) / 32 * 32;
+        for (int c = 1; c < NYC; ++c) p->ybound[c] = std::min(ny, c * ychunk);
+      }
+    }
     if (ncells > 0) {
       int32_t* d_b = nullptr;
       int* d_o = nullptr;
@@ -1576,16 +1601,18 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
       CUDA_TRY(cudaStreamSynchronize(s));
       {
         constexpr int NYC = FE_HOST_YCHUNKS;
-        const int64_t ny = (int64_t)p->vs * p->nglobal;
-        const int64_t ychunk = ((ny + NYC - 1) / NYC + 31) / 32 * 32;
         int* d_y = nullptr;
+        int64_t* d_yb = nullptr;
         CUDA_TRY(cudaMalloc(&d_y, NYC * sizeof(int)));
+        CUDA_TRY(cudaMalloc(&d_yb, (NYC + 1) * sizeof(int64_t)));
         CUDA_TRY(cudaMemsetAsync(d_y, 0, NYC * sizeof(int), s));
+        CUDA_TRY(cudaMemcpyAsync(d_yb, p->ybound.data(), (NYC + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
         k_ychunk_last<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, p->vs,
-                                                               ychunk, d_y);
+                                                               d_yb, NYC, d_y);
         CUDA_TRY(cudaMemcpyAsync(p->ychunk_last.data(), d_y, NYC * sizeof(int), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         cudaFree(d_y);
+        cudaFree(d_yb);
       }
       cudaFree(d_b);
       cudaFree(d_o);
@@ -1751,7 +1778,6 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
                                p->hstream_u));
     CUDA_TRY(cudaEventRecord(p->ev_uc[c], p->hstream_u));
   }
-  const size_t ychunk = ((n + NYC - 1) / NYC + 31) / 32 * 32;
   // the operator first (it does not read dat0): memset + one launch per cell
   // chunk, each gated on the u chunks it reads
   CUDA_TRY(cudaMemsetAsync(p->d_y, 0, n * sizeof(double), s));
@@ -1781,7 +1807,7 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   const uint64_t* ybits = reinterpret_cast<const uint64_t*>(dat0);
   for (int oc = 0; oc < NYC; ++oc) {
     const int c = order[oc];
-    const size_t a = std::min(n, c * ychunk), b = std::min(n, a + ychunk);
+    const size_t a = (size_t)p->ybound[c], b = (size_t)p->ybound[c + 1];
     int nonzero = 0;
     if (b > a) {
       constexpr int NP = 64;
