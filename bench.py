@@ -2,29 +2,45 @@
 """Benchmark of the matrix-free FE operator action on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2] [--seed S]
+                    [--config all|C1..C6] [--seed S]
 
-Workload (BASELINE.json configs[1] -- configs[0] is the reference's own CPU
-case): the Helmholtz action on P1..P4 tetrahedra, 64^3 cubes x 6 Kuhn tets
-(1,572,864 cells) per GPU, interior vertices jittered +-0.1h, u ~ U[-1,1]
-(seeded synthetic inputs; BASELINE names no dataset).  One STEP applies the
-four operators P1..P4 once each (y = A_k u_k, y zero-filled inside the
-step).  Inputs (u, y, maps: 0.1-1 GB per operator) exceed the 126 MB L2 and
-the L2 is additionally flushed between steps, outside the event pairs.
+Workload (default ``all``): every BASELINE.json config -- C1 mass P2
+triangles 256^2x2, C2 Helmholtz P1..P4 tetrahedra 64^3x6, C3 scalar
+Laplacian Q1..Q6 hexahedra 64^3, C4 Lame elasticity Q1..Q4 quadrilaterals
+1024^2 and Q1..Q3 hexahedra 64^3, C5 neo-Hookean residual P2 tetrahedra
+128^3x6 -- 19 operators on seeded synthetic inputs (BASELINE names no
+dataset): interior vertices jittered +-0.1h, u ~ U[-1,1] (C5: 0.01h U[-1,1],
+SURVEY A.5), mu/lambda ~ U[0.5,2].  One STEP applies each of the 19
+operators once (y = A u, the zero-fill of y inside the timed call).
 
-Multi-GPU (torchrun, one process per GPU): every rank owns a 64^3-cube
-z-slab of a 64 x 64 x 64N global mesh (weak scaling) and the interface node
-planes are summed with the neighbouring ranks over NCCL after every apply
-(paper_1903_08243_b200/distributed.py).  Timing: CUDA events per step on
-the launching stream, barrier + synchronize around the timed loop, max over
-ranks.
+Multi-GPU (``--gpus N``; re-launches itself under torchrun when WORLD_SIZE
+is unset): STRONG scaling -- every config's ONE fixed mesh is cut into N
+slabs of nz/N cell layers (3D: z-slabs, 2D: rows of squares; BASELINE C5:
+128 cube layers -> 128/N per GPU), each rank applies its slab with the
+sm_100a kernels and the interface node planes are summed with the
+neighbouring ranks over NCCL, overlapped with the interior cells
+(paper_1903_08243_b200/distributed.py).  After timing, the distributed y
+is gathered on rank 0 and compared with a single-domain run of the same
+mesh (``parity_gathered_rel_l2``).
 
-value    = sum_k F_k C_k / time, GFLOP/s with the FROZEN per-cell flop counts
-           of SURVEY.md Appendix B, over all ranks;
-e2e      = the same metric through the public host API (GpuKernelHandle
-           with numpy bindings -> fe_wrap_host: pinned host u/y uploaded,
-           applied, y downloaded every step);
-roofline = the dominant kernel (P4) against the measured FP64 peak.
+Timing: per operator, a read-based L2 flush (3x L2, outside the events:
+every apply starts with a cold, clean L2), a device-side all-reduce across
+ranks (N > 1: the ranks start each operator together), a GPU spin covering
+the host's launch latency, then CUDA events on the launching stream around
+the apply.  Per (step, operator) the MAX over ranks is taken; ``value`` =
+the whole job's flops x K / the sum of those maxima.
+
+value      = sum_k F_k C_k / time in GFLOP/s; F = minimum flops per cell
+             over SURVEY.md App. B's menu plus the two exact cheaper
+             algorithms of round 1 (modal split for affine P_k tets,
+             vertex-gradient P2) -- harness.flops_per_cell;
+e2e        = the same metric through the public host API: at N = 1 the
+             C-ABI host entry (GpuKernelHandle with numpy bindings ->
+             fe_wrap_host: pinned host u uploaded, applied, y downloaded,
+             every step); at N > 1 pinned host u -> device, the distributed
+             apply, y -> pinned host, max over ranks;
+roofline   = the dominant operator's kernel (largest F C: C5) against the
+             measured FP64 peak; per-operator fractions for all 19 next to it.
 """
 
 from __future__ import annotations
@@ -32,6 +48,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -42,23 +60,83 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.094   # measured FP64 DMMA peak on this pool (profiles/r01_fp64_peaks.json)
-METRIC = "FP64 GFLOP/s per matrix-free operator action (minimum flop counts of the SURVEY.md App. B menu, round-1 entries included)"
+METRIC = ("FP64 GFLOP/s per matrix-free operator action, all BASELINE configs C1-C5 "
+          "(minimum flop counts of the SURVEY.md App. B menu, round-1 entries included)")
+BASELINE_OPS = (["C1"] + [f"C2-P{k}" for k in range(1, 5)] + [f"C3-Q{k}" for k in range(1, 7)]
+                + [f"C4-quad-Q{k}" for k in range(1, 5)] + [f"C4-hex-Q{k}" for k in range(1, 4)]
+                + ["C5"])
 WORKLOADS = {
-    "C2": ["C2-P1", "C2-P2", "C2-P3", "C2-P4"],
+    "all": BASELINE_OPS,
     "C1": ["C1"],
+    "C2": [f"C2-P{k}" for k in range(1, 5)],
     "C3": [f"C3-Q{k}" for k in range(1, 7)],
     "C4": [f"C4-quad-Q{k}" for k in range(1, 5)] + [f"C4-hex-Q{k}" for k in range(1, 4)],
     "C5": ["C5"],
     "C6": ["C6"],
 }
 WORKLOAD_TEXT = {
-    "C2": "Helmholtz P1-P4 tetrahedra, 64^3 cubes x 6 tets per GPU, jittered",
+    "all": "every BASELINE config: C1 mass P2 tri 256^2x2; C2 Helmholtz P1-P4 tet 64^3x6; "
+           "C3 scalar Laplacian Q1-Q6 hex 64^3 (k+1 GL points); C4 Lame elasticity Q1-Q4 quad "
+           "1024^2 and Q1-Q3 hex 64^3; C5 neo-Hookean residual P2 tet 128^3x6",
     "C1": "mass P2 triangles, 256^2 x 2, jittered (reference's own config)",
-    "C3": "scalar Laplacian Q1-Q6 hexahedra 64^3 per GPU, k+1 GL points",
-    "C4": "Lame elasticity Q1-Q4 quads 1024^2, Q1-Q3 hexes 64^3 per GPU",
-    "C5": "neo-Hookean residual P2 tetrahedra 128^3 x 6 per GPU",
-    "C6": "neo-Hookean tangent action (SURVEY 8f.1) P2 tetrahedra 128^3 x 6 per GPU",
+    "C2": "Helmholtz P1-P4 tetrahedra, 64^3 cubes x 6, jittered",
+    "C3": "scalar Laplacian Q1-Q6 hexahedra 64^3, k+1 GL points",
+    "C4": "Lame elasticity Q1-Q4 quads 1024^2, Q1-Q3 hexes 64^3",
+    "C5": "neo-Hookean residual P2 tetrahedra 128^3 x 6",
+    "C6": "neo-Hookean tangent action (SURVEY 8f.1) P2 tetrahedra 128^3 x 6",
 }
+
+
+# ---------------------------------------------------------------------------
+# shared: problem sizes and the config dict (identical in both arms)
+# ---------------------------------------------------------------------------
+
+
+def op_meta(name):
+    """Global (single-domain) sizes and the flop count of one operator,
+    without building its mesh."""
+    import paper_1903_08243_b200 as fe
+    from paper_1903_08243_b200 import configs as C
+    cfg = C.get_config(name)
+    spec = fe.operator_spec(cfg.form, cfg.cell, cfg.degree)
+    rule = fe.quadrature_rule(cfg.cell, cfg.qdegree)
+    k, vs = spec.element.degree, spec.element.value_size
+    dofs = vs * int(np.prod([k * n + 1 for n in cfg.n]))
+    return dict(name=name, cfg=cfg, cells=cfg.ncells, dofs=dofs,
+                F=fe.flops_per_cell(spec, rule))
+
+
+def config_dict(args, world, names):
+    metas = [op_meta(n) for n in names]
+    return {
+        "workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}",
+        "operators": names,
+        "cells": [m["cells"] for m in metas],
+        "dofs": [m["dofs"] for m in metas],
+        "seed": args.seed,
+        "l2": "inputs larger than L2 (C1: 8 MB, L2-resident) and a read-based 3x-L2 flush before "
+              "every operator apply, outside the events",
+        "parallelism": (f"strong scaling: each mesh split into {world} slabs of nz/{world} cell layers, "
+                        "NCCL halo sums on the interface planes" if world > 1 else "1 GPU"),
+    }
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+            d["source"] = "MEASURED_PEAKS.json"
+            return d
+    except OSError:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 def ncu_traffic(label):
@@ -70,16 +148,6 @@ def ncu_traffic(label):
     except (OSError, ValueError):
         return None
     return None if entry is None else entry["dram_bytes_per_launch"]
-
-
-def measured_peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            d = json.load(f)
-            d["source"] = "MEASURED_PEAKS.json"
-            return d
-    except OSError:
-        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -100,8 +168,6 @@ class ClockSampler:
             self.nv = None
 
     def sample(self):
-        """One reading (also called from the timed loop after every step, so
-        short timed regions are covered even if the thread is starved)."""
         if not self.nv:
             return
         try:
@@ -140,15 +206,12 @@ class ClockSampler:
 
 
 def build_problem_for_rank(name, seed, rank, world):
-    """3D configs: this rank's z-slab of the weak-scaled global mesh;
-    2D configs: the full problem (independent replica per rank)."""
+    """This rank's slab of the config's fixed mesh (strong scaling; the
+    whole mesh at world = 1), slab-local lattice numbering."""
     from paper_1903_08243_b200 import configs as C
-    from paper_1903_08243_b200.distributed import build_slab, slab_range
+    from paper_1903_08243_b200.distributed import build_slab, slab_split
     cfg = C.get_config(name)
-    if len(cfg.n) == 3:
-        z0, z1, nzg = slab_range(rank, world, cfg.n[2])
-        return build_slab(cfg, seed, z0, z1, nzg), True
-    return C.build_problem(cfg, seed), False
+    return build_slab(cfg, seed, *slab_split(rank, world, cfg.n[-1]))
 
 
 def build_ops(names, seed, device, rank, world):
@@ -157,7 +220,7 @@ def build_ops(names, seed, device, rank, world):
     from paper_1903_08243_b200.distributed import DistributedOperator
     ops = []
     for name in names:
-        prob, slab = build_problem_for_rank(name, seed, rank, world)
+        prob = build_problem_for_rank(name, seed, rank, world)
         h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(), prob.rule))
         m, dm = prob.mesh, prob.dofmap
         h.bind(torch.tensor(np.asarray(m.coords).ravel(), device=device),
@@ -175,8 +238,7 @@ def build_ops(names, seed, device, rank, world):
         local = (lambda h, coef: lambda uu, yy: h.apply(uu, yy, coef=coef, overwrite=True))(h, coef)
         rng = (lambda h, coef: lambda uu, yy, a, b, ow: h.apply(uu, yy, a, b, coef=coef,
                                                                  overwrite=ow))(h, coef)
-        op["dist"] = (DistributedOperator(prob, local, rank, world, range_apply=rng)
-                      if (slab and world > 1) else None)
+        op["dist"] = DistributedOperator(prob, local, rank, world, range_apply=rng) if world > 1 else None
         op["run"] = op["dist"].apply if op["dist"] else local
         ops.append(op)
     return ops
@@ -188,90 +250,154 @@ def oracle_problem(prob):
                       prob.rule.exactness_degree, prob.spec.params)
 
 
-def parity_sample(ops, ncheck=4096):
-    """rel-L2 of the GPU action against the C oracle on the first cells of
-    every operator (the full-size oracle is minutes; tests/ cover it)."""
-    import torch
-    from oracle import fe_oracle as fo
-    from oracle import fe_oracle_c as foc
-    worst = 0.0
-    for op in ops:
-        prob = op["prob"]
-        end = min(ncheck, op["C"])
-        yd = torch.zeros_like(op["u"])
-        op["h"].apply(op["u"], yd, 0, end, coef=op["coef"])
-        torch.cuda.synchronize()
-        ref = _cpu_assemble(prob, end, 8)
-        worst = max(worst, fo.rel_l2(yd.cpu().numpy(), ref))
-    return worst
-
-
-def _cpu_assemble(prob, end, threads):
-    """C restatement of the reference loop (oracle/fe_oracle.c) over the
-    first `end` cells; the numpy restatement for forms the C one lacks
-    (neohookean_tangent)."""
+def _cpu_assemble(prob, start, end, threads, out=None):
+    """C restatement of the reference loop (oracle/fe_oracle.c) over cells
+    [start, end); the numpy restatement for forms the C one lacks."""
     from oracle import fe_oracle as fo
     from oracle import fe_oracle_c as foc
     P = oracle_problem(prob)
     if prob.spec.form in foc.FORMS:
         return foc.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
-                            prob.mu, prob.lam, 0, end, threads=threads)
-    return fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
-                       prob.mu, prob.lam, 0, end, state=getattr(prob, "state", None))
+                            prob.mu, prob.lam, start, end, threads=threads, out=out)
+    y = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                    prob.mu, prob.lam, start, end, state=getattr(prob, "state", None))
+    if out is not None:
+        out += y
+        return out
+    return y
 
 
-def cpu_measure(ops_or_probs, budget_s=20.0):
-    """Reference CPU path on the host cores over a bounded sample of each
-    operator: the reference's own generated C (oracle/_ref, vector-ext w8)
-    where the reference supports the config, else the C restatement of its
-    loop (oracle/fe_oracle.c); all host cores, time in the metric's unit."""
-    from oracle import fe_oracle_c as foc
+def parity_sample(ops, ncheck=4096):
+    """rel-L2 of this rank's GPU action against the C oracle on its first
+    cells, every operator (full-size parity: tests/test_gpu_fullsize.py)."""
+    import torch
+    from oracle import fe_oracle as fo
+    worst = 0.0
+    for op in ops:
+        end = min(ncheck, op["C"])
+        yd = torch.zeros_like(op["u"])
+        op["h"].apply(op["u"], yd, 0, end, coef=op["coef"])
+        torch.cuda.synchronize()
+        ref = _cpu_assemble(op["prob"], 0, end, 8)
+        worst = max(worst, fo.rel_l2(yd.cpu().numpy(), ref))
+    return worst
+
+
+def gathered_parity(ops, rank, world, dev, seed):
+    """N > 1: every rank's y (after the halo sums) against the single-domain
+    apply of the same fixed mesh on rank 0 (the global vector restricted to
+    the slab -- partition independence, reference test_reference.py:72-89)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1903_08243_b200 as fe
+    from oracle import fe_oracle as fo
+    from paper_1903_08243_b200.distributed import build_slab, slab_split
+    worst = 0.0
+    for op in ops:
+        sizes = torch.zeros(world, dtype=torch.int64, device=dev)
+        sizes[rank] = op["y"].numel()
+        dist.all_reduce(sizes)
+        if rank != 0:
+            dist.send(op["y"], 0)
+            continue
+        ys = [op["y"]] + [torch.empty(int(sizes[r]), dtype=torch.float64, device=dev)
+                          for r in range(1, world)]
+        for r in range(1, world):
+            dist.recv(ys[r], r)
+        cfg = op["prob"].config
+        glob = build_slab(cfg, seed, 0, cfg.n[-1], cfg.n[-1])
+        g = fe.compile_and_load(fe.emit_for(glob.spec, fe.Target(), glob.rule))
+        m, dm = glob.mesh, glob.dofmap
+        g.bind(torch.tensor(np.asarray(m.coords).ravel(), device=dev),
+               torch.tensor(np.asarray(dm.cell2dof, np.int32).ravel(), device=dev),
+               torch.tensor(np.asarray(m.cell2vert, np.int32).ravel(), device=dev),
+               nglobal=dm.ndofs_global)
+        coef = None
+        if glob.coef() is not None:
+            coef = tuple(None if c is None else torch.tensor(c, device=dev) for c in glob.coef())
+        yg = torch.zeros(glob.ndofs, dtype=torch.float64, device=dev)
+        g.apply(torch.tensor(glob.u, device=dev), yg, coef=coef, overwrite=True)
+        for r in range(world):
+            off = glob.spec.element.degree * slab_split(r, world, cfg.n[-1])[0] * glob.plane \
+                * glob.spec.element.value_size
+            ref = yg[off:off + ys[r].numel()]
+            worst = max(worst, float(torch.linalg.norm(ys[r] - ref) / torch.linalg.norm(ref)))
+        del g, yg
+    out = torch.tensor([worst], device=dev)
+    dist.broadcast(out, 0)
+    return float(out.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (the oracle port / the reference's own generated C)
+# ---------------------------------------------------------------------------
+
+
+def cpu_run(prob, F, start, end, cores):
+    """One timed CPU pass over cells [start, end) of an operator: the
+    reference's own generated C (oracle/_ref, vector-ext w8) where the
+    reference supports the config, else the C restatement of its loop."""
     from oracle import ref_c
     import paper_1903_08243_b200 as fe
+    sp = prob.spec
+    rcell = {"triangle": "tri", "quadrilateral": "quad"}.get(sp.cell.kind)
+    use_ref = rcell is not None and ref_c.available(sp.form, rcell, sp.element.degree)
+    if use_ref:
+        k = ref_c.RefKernel(sp.form, rcell, sp.element.degree)
+        b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, np.zeros(prob.ndofs))
+        t0 = time.perf_counter()
+        k.run_threads(end, b, cores, start=start)
+        dt = time.perf_counter() - t0
+    else:
+        out = np.zeros(prob.ndofs)
+        t0 = time.perf_counter()
+        _cpu_assemble(prob, start, end, cores, out=out)
+        dt = time.perf_counter() - t0
+    return dt, F * (end - start), "reference" if use_ref else "port"
+
+
+CPU_PORT_TEXT = ("C restatement of the reference cell loop (oracle/fe_oracle.c, -O3 -ffast-math, "
+                 "OpenMP over cell chunks) where the reference has no code path (tets, hexes, "
+                 "mu/lambda, neo-Hookean); the reference's own generated vector-ext C "
+                 "(oracle/_ref) for C1")
+
+
+def cpu_measure(ops, budget_s=20.0):
+    """cpu_baseline of our arm: a bounded sample (the first cells, doubling
+    until ~budget/ops seconds) of every operator on all host cores."""
     cores = len(os.sched_getaffinity(0))
-    per = budget_s / len(ops_or_probs)
+    per = budget_s / len(ops)
     flop = tsum = 0.0
     kinds, desc = set(), []
-    for op in ops_or_probs:
-        prob = op["prob"]
-        F = op["F"]
-        sp = prob.spec
-        rcell = {"triangle": "tri", "quadrilateral": "quad"}.get(sp.cell.kind)
-        use_ref = rcell is not None and ref_c.available(sp.form, rcell, sp.element.degree)
-        P = oracle_problem(prob)
+    for op in ops:
         n = 1024
         while True:
             end = min(n, op["C"])
-            if use_ref:
-                k = ref_c.RefKernel(sp.form, rcell, sp.element.degree)
-                b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, np.zeros(prob.ndofs))
-                t0 = time.perf_counter()
-                k.run_threads(end, b, cores)
-                dt = time.perf_counter() - t0
-            else:
-                t0 = time.perf_counter()
-                _cpu_assemble(prob, end, cores)
-                dt = time.perf_counter() - t0
+            dt, fl, kind = cpu_run(op["prob"], op["F"], 0, end, cores)
             if dt > per / 3 or end >= op["C"]:
                 break
             n *= 2
-        flop += F * end
+        flop += fl
         tsum += dt
-        kinds.add("reference" if use_ref else "port")
-        desc.append(f"{op['name']}: first {end} cells")
+        kinds.add(kind)
+        desc.append(f"{op['name']}: {end}/{op['C']} cells")
     kind = "reference" if kinds == {"reference"} else "port"
-    src = ("reference-generated vector-ext C (oracle/_ref, fevec BENCH_FLAGS)" if kind == "reference"
-           else "C restatement of the reference cell loop (oracle/fe_oracle.c, -O3 -ffast-math, "
-                "OpenMP over cell chunks); the reference has no code path for this config")
     return {"value": round(flop / tsum / 1e9, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
-            "sample": f"{src}; " + ", ".join(desc), "seconds": round(tsum, 3)}
+            "sample": CPU_PORT_TEXT + "; first cells of each operator: " + ", ".join(desc),
+            "seconds": round(tsum, 3)}
 
 
-def run_e2e(ops, steps):
-    """Same metric through the public host API (numpy bindings ->
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_e2e_host_api(ops, steps):
+    """N = 1: the metric through the C-ABI host entry (numpy bindings ->
     GpuKernelHandle.__call__ -> fe_wrap_host): per step and operator, u is
-    uploaded from pinned host memory, applied, y is downloaded (y's zero
-    chunks are detected on the host and not uploaded)."""
+    uploaded from pinned host memory, applied, y downloaded (y's zero chunks
+    are detected on the host and not uploaded).  Afterwards the plans stay
+    bound to the host meshes (device applies would need bind() again)."""
     import torch
     import paper_1903_08243_b200 as fe
     hb = []
@@ -291,22 +417,47 @@ def run_e2e(ops, steps):
             t0 = time.perf_counter()
             op["h"](0, op["C"], b)
             t += time.perf_counter() - t0
-    for op, _ in hb:                 # restore the device binding
-        op["h"].rebind()
-    flop = sum(op["F"] * op["C"] for op in ops) * steps
-    return {"value": round(flop / t / 1e9, 3), "unit": "GFLOP/s",
-            # dat0 is zero every step (y = A u): the host entry detects its
-            # all-zero chunks while u uploads and does not upload them
-            "h2d_bytes_per_step": sum(8 * op["ndofs"] for op in ops),
-            "d2h_bytes_per_step": sum(8 * op["ndofs"] for op in ops), "steps": steps,
-            "path": "GpuKernelHandle(start, end, numpy bindings) -> fe_wrap_host, pinned host buffers; "
-                    "dat0 zeroed before each call (outside the timer), its zero chunks are scanned "
-                    "on the host inside the timer and not uploaded"}
+    return t, {"h2d_bytes_per_step": sum(8 * op["ndofs"] for op in ops),
+               "d2h_bytes_per_step": sum(8 * op["ndofs"] for op in ops),
+               "path": "GpuKernelHandle(start, end, numpy bindings) -> fe_wrap_host, pinned host "
+                       "buffers; dat0 zeroed before each call (outside the timer), its zero chunks "
+                       "are scanned on the host inside the timer and not uploaded"}
+
+
+def run_e2e_distributed(ops, steps, dev):
+    """N > 1: pinned host u -> device, the distributed apply (NCCL halo
+    sums), y -> pinned host, synchronised, per operator; wall clock per rank
+    (the max over ranks is taken by the caller)."""
+    import torch
+    hb = []
+    for op in ops:
+        hu = torch.empty(op["ndofs"], dtype=torch.float64, pin_memory=True)
+        hu.copy_(torch.from_numpy(op["prob"].u))
+        hy = torch.empty(op["ndofs"], dtype=torch.float64, pin_memory=True)
+        du, dy = torch.empty_like(op["u"]), torch.empty_like(op["y"])
+        hb.append((op, hu, hy, du, dy))
+    torch.cuda.synchronize()
+    t = 0.0
+    for it in range(steps + 1):
+        for op, hu, hy, du, dy in hb:
+            t0 = time.perf_counter()
+            du.copy_(hu, non_blocking=True)
+            op["run"](du, dy)
+            hy.copy_(dy, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            if it > 0:
+                t += time.perf_counter() - t0
+    return t, {"h2d_bytes_per_step": sum(8 * op["ndofs"] for op in ops),
+               "d2h_bytes_per_step": sum(8 * op["ndofs"] for op in ops),
+               "path": "per rank: pinned host u -> device copy, DistributedOperator.apply "
+                       "(fe_apply on the slab + NCCL halo sums), device -> pinned host y, "
+                       "synchronised; bytes summed over ranks; max over ranks"}
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
+    from paper_1903_08243_b200 import _lib
     from paper_1903_08243_b200.harness import L2Flusher, gpu_busy_wait
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -315,57 +466,90 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")            # communicator init in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
         dist.barrier()   # collective first: the communicator exists before any P2P batch
     names = WORKLOADS[args.config]
+    t_build = time.perf_counter()
     ops = build_ops(names, args.seed, dev, rank, world)
-    parity = parity_sample(ops) if rank == 0 else None
+    t_build = time.perf_counter() - t_build
+    parity = parity_sample(ops)
+    if world > 1:
+        t = torch.tensor([parity], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        parity = float(t.item())
     flush = L2Flusher(local)
     stream = torch.cuda.current_stream()
-    # rebuild the device binding after parity_sample's partial apply
-    for _ in range(args.warmup):
-        flush()
-        for op in ops:
+    token = torch.zeros(1, device=dev)
+
+    def step_ops(events=None):
+        for i, op in enumerate(ops):
+            flush()
+            if world > 1:
+                dist.all_reduce(token)           # device-side: ranks start each operator together
+            gpu_busy_wait()                      # host submission latency stays outside the events
+            if events is not None:
+                events[i][0].record(stream)
             op["run"](op["u"], op["y"])
+            if events is not None:
+                events[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step_ops()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    per_op = np.zeros(len(ops))
-    t_total = 0.0
+    lib = _lib.load()
+    times = np.zeros((args.steps, len(ops)))
+    launches0 = lib.fe_launch_count()
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush()
+        for s in range(args.steps):
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in ops]
-            gpu_busy_wait()              # host submission latency stays outside the events
-            for (e0, e1), op in zip(ev, ops):
-                e0.record(stream)
-                op["run"](op["u"], op["y"])
-                e1.record(stream)
+            step_ops(ev)
             clk.sample()                 # while this step is executing on the GPU
             ev[-1][1].synchronize()
-            ts = [e0.elapsed_time(e1) * 1e-3 for e0, e1 in ev]
-            per_op += ts
-            t_total += sum(ts)
+            times[s] = [e0.elapsed_time(e1) * 1e-3 for e0, e1 in ev]
+    launches = lib.fe_launch_count() - launches0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([t_total], device=dev)
+        t = torch.tensor(times, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total = float(t.item())
-    flop_step = sum(op["F"] * op["C"] for op in ops)
-    dofs_step = sum(op["ndofs"] for op in ops)
-    value = world * flop_step * args.steps / t_total / 1e9
+        times = t.cpu().numpy()
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    t_total = float(times.sum())
+    metas = [op_meta(n) for n in names]
+    flop_step = sum(m["F"] * m["cells"] for m in metas)
+    dofs_step = sum(m["dofs"] for m in metas)
+    value = flop_step * args.steps / t_total / 1e9
+    gathered = gathered_parity(ops, rank, world, dev, args.seed) if world > 1 else None
+    # e2e (max over ranks)
+    e2e_steps = max(3, min(args.steps, 10))
+    if world == 1:
+        t_e2e, e2e_info = run_e2e_host_api(ops, e2e_steps)
+    else:
+        t_e2e, e2e_info = run_e2e_distributed(ops, e2e_steps, dev)
+        t = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+        nb = torch.tensor([e2e_info["h2d_bytes_per_step"]], dtype=torch.int64, device=dev)
+        dist.all_reduce(nb)
+        e2e_info["h2d_bytes_per_step"] = e2e_info["d2h_bytes_per_step"] = int(nb.item())
     if rank == 0:
         peaks = measured_peaks()
-        e2e = run_e2e(ops, max(3, min(args.steps, 20)))
+        med = np.median(times, axis=0)
         dom = int(np.argmax([op["F"] * op["C"] for op in ops]))
-        t_dom = per_op[dom] / args.steps
-        achieved = ops[dom]["F"] * ops[dom]["C"] / t_dom / 1e12
+        achieved = ops[dom]["F"] * ops[dom]["C"] / med[dom] / 1e12
+        # per-operator roofline on this rank's slab (the slowest rank's time)
         troof = [max(op["F"] * op["C"] / (FP64_PEAK_TFLOPS * 1e12),
                      op["B"] * op["C"] / (peaks["hbm_gbs"] * 1e9)) for op in ops]
+        kern = {op["name"]: op["h"].info["kernel"] for op in ops}
         line = {
             "metric": METRIC,
             "value": round(value, 3),
@@ -375,44 +559,44 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(t_total / args.steps * 1e3, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic: seeded jittered structured mesh, u ~ U[-1,1] (BASELINE names no dataset)",
-            "config": {
-                "workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}",
-                "operators": names,
-                "cells_per_gpu": [op["C"] for op in ops],
-                "dofs_per_gpu": [op["ndofs"] for op in ops],
-                "seed": args.seed,
-                "l2": "inputs larger than L2 and L2 flushed (2x L2 write) between steps, outside the events",
-                "parallelism": (f"z-slab element partition over {world} GPUs, NCCL halo sums"
-                                if world > 1 else "1 GPU"),
-            },
-            "gdofs_per_s": round(world * dofs_step * args.steps / t_total / 1e9, 3),
-            "ms_per_operator": {op["name"]: round(per_op[i] / args.steps * 1e3, 4) for i, op in enumerate(ops)},
-            "roofline_frac_per_operator": {op["name"]: round(troof[i] / (per_op[i] / args.steps), 4)
+            "data": "synthetic: seeded jittered structured meshes, u ~ U[-1,1] (BASELINE names no dataset)",
+            "config": config_dict(args, world, names),
+            "gdofs_per_s": round(dofs_step * args.steps / t_total / 1e9, 3),
+            "ms_per_operator_median": {op["name"]: round(med[i] * 1e3, 4) for i, op in enumerate(ops)},
+            "ms_per_operator_mean": {op["name"]: round(times[:, i].mean() * 1e3, 4)
+                                     for i, op in enumerate(ops)},
+            "gflops_per_operator": {op["name"]: round(op["F"] * op["C"] / med[i] / 1e9, 1)
+                                    for i, op in enumerate(ops)},
+            "roofline_frac_per_operator": {op["name"]: round(troof[i] / med[i], 4)
                                            for i, op in enumerate(ops)},
-            "kernel_per_operator": {op["name"]: op["h"].info["kernel"] for op in ops},
+            "kernel_per_operator": kern,
             "step_roofline_frac": round(sum(troof) / (t_total / args.steps), 4),
             "parity_rel_l2_sample": parity,
+            "parity_gathered_rel_l2": gathered,
             "roofline": {
                 "bound": "fp64",
-                "kernel": ops[dom]["name"] + ":" + ops[dom]["h"].info["kernel"],
+                "kernel": ops[dom]["name"] + ":" + kern[ops[dom]["name"]],
                 "achieved": round(achieved, 4),
                 "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                "traffic": ncu_traffic(ops[dom]["name"] + ":" + ops[dom]["h"].info["kernel"]),
+                "traffic": ncu_traffic(ops[dom]["name"] + ":" + kern[ops[dom]["name"]]),
                 "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, one "
                                   "ncu --set full capture (profiles/traffic.json)",
                 "peak_source": "measured FP64 (DMMA) peak on this pool's B200s, profiles/r01_fp64_peaks.json "
                                "(MEASURED_PEAKS.json has no FP64 entry)",
                 "algorithmic_flop_per_launch": ops[dom]["F"] * ops[dom]["C"],
+                "time_basis": "median over steps of the max over ranks",
             },
-            "e2e": e2e,
-            "gpu_launches": len(ops) * args.steps,
+            "e2e": {"value": round(flop_step * e2e_steps / t_e2e / 1e9, 3), "unit": "GFLOP/s",
+                    "steps": e2e_steps, **e2e_info},
+            "gpu_launches": launches,
+            "gpu_launches_source": "fe_launch_count() difference around the timed region, summed over ranks",
             "clocks": clk.summary(),
+            "build_s": round(t_build, 1),
             "cpu_baseline": cpu_measure(ops) if world == 1 else None,
         }
         print(json.dumps(line), flush=True)
@@ -421,56 +605,80 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU implementation of the path on the
-    box's host cores (all of them), on this arm's config/metric/unit; each
-    step is a bounded sample of every operator."""
+    box's host cores (all of them), on this arm's config/metric/unit.  Step
+    s applies every operator over cell window s of its mesh (window =
+    ceil(C / K)), so the K timed steps together apply every operator to its
+    WHOLE BASELINE mesh exactly once; warm-up steps apply window 0."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    import paper_1903_08243_b200 as fe
     names = WORKLOADS[args.config]
-    ops = []
-    for name in names:
-        prob, _ = build_problem_for_rank(name, args.seed, 0, 1)
-        ops.append(dict(name=name, prob=prob, C=prob.mesh.ncells, ndofs=prob.ndofs,
-                        F=fe.flops_per_cell(prob.spec, prob.rule)))
-    # the whole --steps K --warmup W run stays near two minutes of CPU work
-    budget = max(0.4, 120.0 / max(1, args.steps + args.warmup))
-    vals = []
-    for it in range(args.warmup + args.steps):
-        r = cpu_measure(ops, budget_s=budget)
+    probs = [(build_problem_for_rank(n, args.seed, 0, 1), op_meta(n)["F"]) for n in names]
+    cores = len(os.sched_getaffinity(0))
+    K = args.steps
+    flop = secs = 0.0
+    kinds = set()
+    for it in range(args.warmup + K):
+        s = 0 if it < args.warmup else it - args.warmup
+        sf = st = 0.0
+        for prob, F in probs:
+            C = prob.mesh.ncells
+            w = -(-C // K)
+            a, b = min(C, s * w), min(C, (s + 1) * w)
+            if a >= b:
+                continue
+            dt, fl, kind = cpu_run(prob, F, a, b, cores)
+            sf += fl
+            st += dt
+            kinds.add(kind)
         if it >= args.warmup:
-            vals.append(r)
-    value = float(np.mean([v["value"] for v in vals]))
-    secs = float(np.mean([v["seconds"] for v in vals]))
-    last = vals[-1]
+            flop += sf
+            secs += st
+    value = flop / secs / 1e9
+    kind = "reference" if kinds == {"reference"} else "port"
+    sample = (CPU_PORT_TEXT + f"; step s applies cells [s*ceil(C/{K}), (s+1)*ceil(C/{K})) of every "
+              f"operator, so the {K} timed steps cover every full BASELINE mesh once")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(secs * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded jittered structured mesh, u ~ U[-1,1]",
-        "config": {"workload": f"{args.config}: {WORKLOAD_TEXT[args.config]}", "operators": names,
-                   "seed": args.seed},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": last["cores"],
-                         "kind": last["kind"], "sample": last["sample"]},
+        "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(secs / K * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded jittered structured meshes, u ~ U[-1,1] (BASELINE names no dataset)",
+        "config": config_dict(args, world, names),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 without torchrun: re-run this script as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="all", choices=sorted(WORKLOADS))
     ap.add_argument("--seed", type=int, default=0)
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     else:

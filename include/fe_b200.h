@@ -155,8 +155,14 @@ int fe_apply(const fe_plan* plan, int32_t start, int32_t end, double* dat0,
              uint32_t apply_flags, void* stream);
 
 /* Reference-order entry on DEVICE pointers: (start, end, dat0, dat1, dat2,
- * dat3, dat4, map0, map1).  Re-binds the mesh when dat1/map0/map1 differ
- * from the bound ones.  dat3/dat4 may be NULL. */
+ * dat3, dat4, map0, map1) -- the drop-in for wrap_<form>, which receives the
+ * mesh with every call and no sizes (codegen.py:375-394).  When dat1/map0/
+ * map1 differ from the bound buffers (or were bound as host pointers), the
+ * mesh is (re-)bound first: cells [0, end), nglobal = max(map0) + 1, nverts =
+ * max(vertex map) + 1, derived from the maps (a mesh bound implicitly this
+ * way is re-bound again when a later call passes a larger end).  A mesh bound
+ * explicitly by fe_plan_bind_mesh with the same buffers is used as is.
+ * dat3/dat4 may be NULL. */
 int fe_wrap(fe_plan* plan, int32_t start, int32_t end, double* dat0,
             const double* dat1, const double* dat2, const double* dat3,
             const double* dat4, const int32_t* map0, const int32_t* map1, void* stream);
@@ -167,7 +173,10 @@ int fe_wrap(fe_plan* plan, int32_t start, int32_t end, double* dat0,
  * the host: all-zero chunks (+0.0 / -0.0) are not uploaded, the others are
  * uploaded and accumulated on the device; each result chunk is downloaded as
  * soon as the last cell chunk scattering into it is done.  The mesh is
- * re-bound when dat1/map0/map1 differ from the bound host pointers. */
+ * (re-)bound exactly as in fe_wrap when dat1/map0/map1 differ from the bound
+ * HOST buffers.  [start, end) outside [0, ncells) -> FE_EINVAL before any
+ * copy is queued; on any error every copy of the call has completed before
+ * the function returns (nothing still reads dat2 or writes dat0). */
 int fe_wrap_host(fe_plan* plan, int32_t start, int32_t end, double* dat0,
                  const double* dat1, const double* dat2, const double* dat3,
                  const double* dat4, const int32_t* map0, const int32_t* map1);
@@ -183,6 +192,25 @@ int fe_plan_get_info(const fe_plan* plan, fe_plan_info* info);
  * dof (cost ~ ndof x apply). */
 int fe_diagonal(const fe_plan* plan, int32_t start, int32_t end, double* diag,
                 const double* coef0, const double* coef1, uint32_t apply_flags, void* stream);
+
+/* Thread safety: fe_apply / fe_wrap / fe_diagonal build their kernel
+ * parameter block per call, so concurrent calls on one plan from several
+ * host threads (different streams, disjoint dat0) are safe; binding
+ * (fe_plan_bind_mesh, or an implicit re-bind in fe_wrap*) and fe_wrap_host
+ * (which owns the plan's staging buffers) must not run concurrently with
+ * other calls on the same plan. */
+
+/* Diagnostics: y[i] = ln x[i] with the branch-free logarithm the
+ * hyperelastic kernels use (device pointers; exposes its special-value
+ * behaviour to tests: +inf -> +inf, +-0 -> -inf, x < 0 / NaN -> NaN,
+ * subnormals rescaled). */
+int fe_eval_log(const double* x, double* y, int64_t n, void* stream);
+
+/* Number of operator / diagonal kernels this library has launched in the
+ * process (fe_apply, fe_wrap*, fe_diagonal; not the bind-time layout
+ * kernels): bench.py's gpu_launches is the difference around its timed
+ * region. */
+int64_t fe_launch_count(void);
 
 void fe_plan_destroy(fe_plan* plan);
 

@@ -64,12 +64,17 @@ class RefKernel:
             args.append(buf.ctypes.data_as(ctypes.POINTER(t)))
         self.fn(*args)
 
-    def run_threads(self, ncells, bindings, threads):
-        """All cells on `threads` threads with private outputs; returns y."""
+    def run_threads(self, ncells, bindings, threads, start=0):
+        """Cells [start, ncells) on `threads` threads with private outputs
+        (chunk starts width-aligned relative to start, which must itself be
+        width-aligned); returns y."""
         w = self.width
-        chunk = -(-ncells // threads)
+        if start % w:
+            raise ValueError(f"start {start} is not a multiple of the SIMD width {w}")
+        n = ncells - start
+        chunk = -(-n // threads)
         chunk = -(-chunk // w) * w
-        cuts = list(range(0, ncells, chunk)) + [ncells]
+        cuts = list(range(start, ncells, chunk)) + [ncells]
         outs = [np.zeros_like(bindings["dat0"]) for _ in cuts[:-1]]
 
         def work(i):

@@ -64,6 +64,7 @@ class FeError(RuntimeError):
 EXPORTS = (
     "fe_abi_version", "fe_plan_create", "fe_plan_bind_mesh", "fe_apply", "fe_wrap",
     "fe_wrap_host", "fe_plan_get_info", "fe_plan_destroy", "fe_last_error", "fe_diagonal",
+    "fe_eval_log", "fe_launch_count",
 )
 
 _lib = None
@@ -92,6 +93,9 @@ def load():
     lib.fe_diagonal.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, ctypes.c_uint32, vp]
     lib.fe_wrap_host.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp]
     lib.fe_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+    lib.fe_eval_log.argtypes = [vp, vp, ctypes.c_int64, vp]
+    lib.fe_launch_count.restype = ctypes.c_int64
+    lib.fe_launch_count.argtypes = []
     lib.fe_plan_destroy.argtypes = [vp]
     lib.fe_plan_destroy.restype = None
     for name in ("fe_plan_create", "fe_plan_bind_mesh", "fe_apply", "fe_wrap",

@@ -68,10 +68,14 @@ FE_DEVICE double recip(double x) {
 // log() was 25% of C5's time).  x = 2^e m with m in [1/sqrt2, sqrt2),
 // ln m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, as an odd series in s
 // to s^23 (truncation < 2e-17 relative); e ln2 added with a two-part ln2.
-// A few ulp for positive normal x; NaN for x <= 0 or NaN (as the library).
-FE_DEVICE double fast_log(double x) {
+// A few ulp for positive finite x (subnormals are rescaled by 2^54 first);
+// +inf -> +inf, +-0 -> -inf, x < 0 or NaN -> NaN, as the library routine.
+// Branch-free: the special cases are selects.
+FE_DEVICE double fast_log(double x0) {
+  const bool sub = x0 < 2.2250738585072014e-308;            // subnormal (or <= 0: NaN/-inf below)
+  const double x = sub ? x0 * 18014398509481984.0 : x0;    // * 2^54
   const int hi = __double2hiint(x), lo = __double2loint(x);
-  int e = ((hi >> 20) & 0x7ff) - 1023;
+  int e = ((hi >> 20) & 0x7ff) - 1023 - (sub ? 54 : 0);
   double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);  // [1, 2)
   const bool big = m > 1.4142135623730951;
   m = big ? 0.5 * m : m;
@@ -94,7 +98,10 @@ FE_DEVICE double fast_log(double x) {
   const double r = fma(ts * z, p, ts);  // 2s (1 + z p)
   const double de = (double)e;
   const double res = fma(de, 6.93147180369123816490e-01, fma(de, 1.90821492927058770002e-10, r));
-  return x > 0.0 ? res : __longlong_as_double(0x7ff8000000000000LL);
+  const double special = x0 == 0.0 ? __longlong_as_double(0xfff0000000000000LL)     // -inf
+                         : x0 == __longlong_as_double(0x7ff0000000000000LL) ? x0    // +inf
+                                                                            : __longlong_as_double(0x7ff8000000000000LL);
+  return (x0 > 0.0 && x0 < __longlong_as_double(0x7ff0000000000000LL)) ? res : special;
 }
 
 // determinant and inverse of a DIM x DIM matrix stored row-major J[a][b]

@@ -5,6 +5,7 @@
 // (form, cell, degree, rule) -- here chosen from a registry of sm_100a
 // template instantiations instead of generated C -- plus the bound mesh in
 // the GPU layout (element-batched SoA maps, padded coordinates).
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -36,6 +37,8 @@ using namespace fe;
 
 namespace {
 thread_local std::string g_err;
+std::atomic<long long> g_launches{0};  // operator / diagonal kernel launches (fe_launch_count)
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -113,6 +116,7 @@ struct fe_plan {
   const void* b_map0 = nullptr;
   const void* b_map1 = nullptr;
   uint32_t b_flags = 0;
+  bool auto_bound = false;      // bound implicitly by fe_wrap/fe_wrap_host (cells [0, end) of that call)
   // host-entry staging
   cudaStream_t hstream = nullptr;
   cudaStream_t hstream2 = nullptr;
@@ -201,7 +205,7 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   k.p1 = p->params[1];
   int n = end - start;
   quad_kernel<FORM, DIM, NV, ND, NQ, AFFINE>
-      <<<(n + 127) / 128, 128, p->tables_bytes, s>>>(k);
+      <<<(n + 127) / 128, 128, p->tables_bytes, s>>>(k); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -241,7 +245,7 @@ int quad_diag(const fe_plan* cp, int32_t start, int32_t end, double* y, const do
     k.p0 = p->params[0];
     k.p1 = p->params[1];
     const int n = end - start;
-    quad_diag_kernel<FORM, DIM, NV, ND, NQ, AFFINE><<<(n + 127) / 128, 128, p->diag_tables_bytes, s>>>(k);
+    quad_diag_kernel<FORM, DIM, NV, ND, NQ, AFFINE><<<(n + 127) / 128, 128, p->diag_tables_bytes, s>>>(k); note_launch();
     CUDA_TRY(cudaGetLastError());
     return FE_OK;
   }
@@ -286,7 +290,8 @@ template <int FORM, int DIM, int NV, int ND, int NQ, bool AFF, int MINB = 1, int
 int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
               const double* c0, const double* c1, cudaStream_t s) {
   using P = QuadConstParams<NQ, ND, DIM, NV, form_needs_values(FORM), AFF>;
-  P* hp = static_cast<P*>(p->host_params);
+  P hpv = *static_cast<const P*>(p->host_params);  // per-launch copy: concurrent launches on one plan stay independent
+  P* hp = &hpv;
   hp->mesh = mesh_view(p);
   hp->start = start;
   hp->end = end;
@@ -297,7 +302,7 @@ int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -363,7 +368,8 @@ template <int FORM, int DIM, int NV, int ND, int NQ, int MINB, int UNR>
 int vtx_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                const double* c0, const double*, cudaStream_t s) {
   using P = VtxParams<NQ, ND, DIM, NV>;
-  P* hp = static_cast<P*>(p->host_params);
+  P hpv = *static_cast<const P*>(p->host_params);
+  P* hp = &hpv;
   hp->mesh = mesh_view(p);
   hp->start = start;
   hp->end = end;
@@ -374,7 +380,7 @@ int vtx_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const do
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_vtx_kernel<FORM, DIM, NV, ND, NQ, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp);
+  quad_vtx_kernel<FORM, DIM, NV, ND, NQ, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -455,7 +461,8 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
               const double*, const double*, cudaStream_t s) {
   constexpr int NM = et_nmats<FORM, DIM>();
   using P = ETParams<NM, ND>;
-  P* hp = static_cast<P*>(p->host_params);
+  P hpv = *static_cast<const P*>(p->host_params);
+  P* hp = &hpv;
   hp->mesh = mesh_view(p);
   hp->u = u;
   hp->y = y;
@@ -464,7 +471,7 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   int n = end - start;
   constexpr int G = affine_group(DIM, ND);
   const int nt = (n + G - 1) / G;
-  affine_et_kernel<FORM, DIM, ND, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
+  affine_et_kernel<FORM, DIM, ND, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -491,7 +498,8 @@ int etp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const do
   constexpr int NM = et_nmats<FORM, DIM>();
   using P = ETPatchParams<NM, ND>;
   if (!p->d_patch_off) return fail(FE_ENOMESH, "patch plan without patches");
-  P* hp = static_cast<P*>(p->host_params);
+  P hpv = *static_cast<const P*>(p->host_params);
+  P* hp = &hpv;
   hp->mesh = mesh_view(p);
   hp->patch.off = p->d_patch_off;
   hp->patch.dofs = p->d_patch_dofs;
@@ -502,7 +510,7 @@ int etp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const do
   hp->end = end;
   const int b0 = start / kPatchCells, b1 = (end - 1) / kPatchCells;
   const size_t smem = 2 * (size_t)p->patch_maxu * sizeof(double);
-  affine_et_patch_kernel<FORM, DIM, ND><<<b1 - b0 + 1, kPatchCells, smem, s>>>(*hp);
+  affine_et_patch_kernel<FORM, DIM, ND><<<b1 - b0 + 1, kPatchCells, smem, s>>>(*hp); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -558,7 +566,8 @@ template <int FORM, int DIM, int ND, int NQS>
 int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                  const double*, const double*, cudaStream_t s) {
   using P = SplitParams<NQS, ND, DIM>;
-  P* hp = static_cast<P*>(p->host_params);
+  P hpv = *static_cast<const P*>(p->host_params);
+  P* hp = &hpv;
   hp->mesh = mesh_view(p);
   hp->u = u;
   hp->y = y;
@@ -570,7 +579,7 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
     hp->start = a;
     hp->end = b;
     const int nt = (b - a + G - 1) / G;
-    affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp);
+    affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp); note_launch();
   };
   if constexpr (DIM == 3 && (ND == 4 || ND == 10)) {
     using PAT = MacroFor<ND>;
@@ -590,7 +599,7 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 128, 0);
             nb = std::min(nb, std::max(1, waves * sms * per_sm));
           }
-          kfn<<<nb, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1);
+          kfn<<<nb, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1); note_launch();
         };
         if constexpr (ND == 4) {
           if (p->p1_analytic)
@@ -672,7 +681,7 @@ int dmma_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_t s) {
   const int ngroups = (n + 8 * NT - 1) / (8 * NT);
   const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
   const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
-  dmma_et_kernel<FORM, DIM, ND, NT, MINB><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k);
+  dmma_et_kernel<FORM, DIM, ND, NT, MINB><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -780,7 +789,7 @@ int dmma_modal_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_
   const int ngroups = (n + 8 * NT - 1) / (8 * NT);
   const int need = (ngroups + BLK / 32 - 1) / (BLK / 32);
   const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
-  dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB, BLK><<<grid, BLK, p->tables_bytes, s>>>(k);
+  dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB, BLK><<<grid, BLK, p->tables_bytes, s>>>(k); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -867,7 +876,8 @@ template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                   const double* c0, const double* c1, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
-  TP* hp = static_cast<TP*>(p->host_params);
+  TP hpv = *static_cast<const TP*>(p->host_params);
+  TP* hp = &hpv;
   if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
   hp->mesh = mesh_view(p);
   hp->maplex = p->d_map_lex;
@@ -883,7 +893,7 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   const int cpb = p->cells_per_block;
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
-  tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT><<<grid, tensor_block<MINB>(), p->tables_bytes, s>>>(*hp);
+  tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT><<<grid, tensor_block<MINB>(), p->tables_bytes, s>>>(*hp); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -920,7 +930,8 @@ template <int P, int Q, int WARPS, int MINB, bool V1, int CU = 1>
 int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                  const double*, const double*, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
-  TP* hp = static_cast<TP*>(p->host_params);
+  TP hpv = *static_cast<const TP*>(p->host_params);
+  TP* hp = &hpv;
   if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
   hp->mesh = mesh_view(p);
   hp->maplex = p->d_map_lex;
@@ -937,6 +948,7 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
     plane1_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
   else
     plane_kernel<P, Q, WARPS, MINB, CU><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
+  note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -970,7 +982,8 @@ int hexq1_prepare(fe_plan* p) {
 int hexq1_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                  const double*, const double*, cudaStream_t s) {
   using TP = TensorParams<2, 2>;
-  TP* hp = static_cast<TP*>(p->host_params);
+  TP hpv = *static_cast<const TP*>(p->host_params);
+  TP* hp = &hpv;
   hp->mesh = mesh_view(p);
   hp->maplex = p->d_map_lex;
   hp->u = u;
@@ -981,10 +994,10 @@ int hexq1_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   const int n = end - start;
   const unsigned g = (n + 127) / 128;
   switch (p->dmma_cfg) {
-    case 1: hexq1_lap_kernel<1><<<g, 128, 0, s>>>(*hp); break;
-    case 2: hexq1_lap_kernel<2><<<g, 128, 0, s>>>(*hp); break;
-    case 4: hexq1_lap_kernel<4><<<g, 128, 0, s>>>(*hp); break;
-    default: hexq1_lap_kernel<3><<<g, 128, 0, s>>>(*hp); break;
+    case 1: hexq1_lap_kernel<1><<<g, 128, 0, s>>>(*hp); note_launch(); break;
+    case 2: hexq1_lap_kernel<2><<<g, 128, 0, s>>>(*hp); note_launch(); break;
+    case 4: hexq1_lap_kernel<4><<<g, 128, 0, s>>>(*hp); note_launch(); break;
+    default: hexq1_lap_kernel<3><<<g, 128, 0, s>>>(*hp); note_launch(); break;
   }
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
@@ -1008,7 +1021,8 @@ template <int FORM, int P, int Q, int MINB>
 int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
                 const double* c0, const double* c1, cudaStream_t s) {
   using TP = TensorParams<Q, P>;
-  TP* hp = static_cast<TP*>(p->host_params);
+  TP hpv = *static_cast<const TP*>(p->host_params);
+  TP* hp = &hpv;
   if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
   hp->mesh = mesh_view(p);
   hp->maplex = p->d_map_lex;
@@ -1019,7 +1033,7 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   hp->start = start;
   hp->end = end;
   const int64_t nt = 2 * (int64_t)(end - start);
-  pair_kernel<FORM, P, Q, MINB><<<(unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s>>>(*hp);
+  pair_kernel<FORM, P, Q, MINB><<<(unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s>>>(*hp); note_launch();
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -1412,6 +1426,77 @@ static int build_patches(fe_plan* p, const int32_t* map0, bool dev, cudaStream_t
   return FE_OK;
 }
 
+__global__ void k_eval_log(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fast_log(x[i]);
+}
+
+__global__ void k_max_i32(const int32_t* __restrict__ m, int64_t nrows, int rowlen, int ncols,
+                          int* __restrict__ out) {
+  int best = -1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows * ncols;
+       t += (int64_t)gridDim.x * blockDim.x)
+    best = max(best, m[(t / ncols) * rowlen + t % ncols]);
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best >= 0) atomicMax(out, best);
+}
+
+extern "C" int fe_plan_bind_mesh(fe_plan*, int32_t, int32_t, int64_t, const double*, const int32_t*,
+                                 const int32_t*, uint32_t, void*);
+
+// Largest entry of columns [0, ncols) of a row-major [nrows][rowlen] map.
+static int map_max(const int32_t* m, int64_t nrows, int rowlen, int ncols, bool dev, cudaStream_t s,
+                   int* result) {
+  *result = -1;
+  if (nrows <= 0) return FE_OK;
+  if (!dev) {
+    int best = -1;
+#pragma omp parallel for reduction(max : best) schedule(static)
+    for (int64_t r = 0; r < nrows; ++r)
+      for (int c = 0; c < ncols; ++c) best = std::max(best, m[r * rowlen + c]);
+    *result = best;
+    return FE_OK;
+  }
+  int* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(int)));
+  CUDA_TRY(cudaMemsetAsync(d, 0xff, sizeof(int), s));
+  k_max_i32<<<148 * 8, 256, 0, s>>>(m, nrows, rowlen, ncols, d);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(result, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(d);
+  return FE_OK;
+}
+
+// fe_wrap / fe_wrap_host: the reference's wrap_<form> takes the mesh with
+// every call and no sizes (codegen.py:375-394).  When dat1/map0/map1 (or the
+// pointer kind) differ from the bound ones -- or an implicitly bound mesh is
+// shorter than `end` -- the mesh is (re-)bound here: cells [0, end), nglobal
+// = max(map0) + 1, nverts = max(vertex map) + 1, derived from the maps.  A
+// mesh bound explicitly by fe_plan_bind_mesh with the same buffers is used
+// as is (the GPU layout is built once per mesh, not per apply).
+static int wrap_host_impl(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat2,
+                          const double* dat3, const double* dat4);
+
+static int wrap_bind(fe_plan* p, int32_t end, const double* dat1, const int32_t* map0,
+                     const int32_t* map1, bool dev, cudaStream_t s) {
+  const bool same = p->d_map && p->b_coords == dat1 && p->b_map0 == map0 && p->b_map1 == map1 &&
+                    (bool)(p->b_flags & FE_PTR_DEVICE) == dev;
+  if (same && !(p->auto_bound && end > p->ncells)) return FE_OK;
+  if (!dat1 || !map0) return fail(FE_EINVAL, "null dat1/map0");
+  if (end < 0) return fail(FE_EINVAL, "bad end %d", end);
+  int maxdof = -1, maxv = -1;
+  int rc = map_max(map0, end, p->nd, p->nd, dev, s, &maxdof);
+  if (!rc) rc = map1 ? map_max(map1, end, p->nv, p->nv, dev, s, &maxv) : map_max(map0, end, p->nd, p->nv, dev, s, &maxv);
+  if (rc) return rc;
+  if (end > 0 && (maxdof < 0 || maxv < 0)) return fail(FE_EINVAL, "map entry out of range");
+  rc = fe_plan_bind_mesh(p, end, std::max(1, maxv + 1), std::max(1, maxdof + 1), dat1, map0, map1,
+                         dev ? FE_PTR_DEVICE : FE_PTR_HOST, s);
+  if (rc) return rc;
+  p->auto_bound = true;
+  return FE_OK;
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1644,6 +1729,7 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
   p->b_map0 = map0;
   p->b_map1 = map1;
   p->b_flags = ptr_flags;
+  p->auto_bound = false;
   return FE_OK;
 }
 
@@ -1692,11 +1778,8 @@ int fe_wrap(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* 
             const double* dat2, const double* dat3, const double* dat4, const int32_t* map0,
             const int32_t* map1, void* stream) {
   if (!p) return fail(FE_EINVAL, "null plan");
-  if (!p->d_map || p->b_coords != dat1 || p->b_map0 != map0 || p->b_map1 != map1 ||
-      !(p->b_flags & FE_PTR_DEVICE))
-    return fail(FE_ENOMESH,
-                "fe_wrap: mesh buffers differ from the bound ones; call fe_plan_bind_mesh "
-                "(the GPU layout is built once per mesh, not per apply)");
+  int rc = wrap_bind(p, end, dat1, map0, map1, true, (cudaStream_t)stream);
+  if (rc) return rc;
   return fe_apply(p, start, end, dat0, dat2, dat3, dat4, FE_APPLY_ACCUMULATE, stream);
 }
 
@@ -1705,13 +1788,26 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
                  const int32_t* map0, const int32_t* map1) {
   if (!p) return fail(FE_EINVAL, "null plan");
   if (!p->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream, cudaStreamNonBlocking));
-  cudaStream_t s = p->hstream;
-  if (!p->d_map || p->b_coords != dat1 || p->b_map0 != map0 || p->b_map1 != map1 ||
-      (p->b_flags & FE_PTR_DEVICE)) {
-    return fail(FE_ENOMESH,
-                "fe_wrap_host: mesh buffers differ from the bound host buffers; call "
-                "fe_plan_bind_mesh with FE_PTR_HOST first");
+  int rc = wrap_bind(p, end, dat1, map0, map1, false, p->hstream);
+  if (rc) return rc;
+  if (start < 0 || end > p->ncells || start > end)
+    return fail(FE_EINVAL, "cell range [%d, %d) outside [0, %d)", start, end, p->ncells);
+  if (!dat0 || !dat2) return fail(FE_EINVAL, "null dat0/dat2");
+  rc = wrap_host_impl(p, start, end, dat0, dat2, dat3, dat4);
+  if (rc) {
+    // no copy may still read dat2 or write dat0 once the caller sees the error
+    for (cudaStream_t q : {p->hstream_u, p->hstream2, p->hstream_d, p->hstream})
+      if (q) cudaStreamSynchronize(q);
+    cudaGetLastError();
   }
+  return rc;
+}
+
+}  // extern "C"
+
+static int wrap_host_impl(fe_plan* p, int32_t start, int32_t end, double* dat0, const double* dat2,
+                          const double* dat3, const double* dat4) {
+  cudaStream_t s = p->hstream;
   const size_t n = (size_t)p->vs * p->nglobal;
   if (p->cap_u < n) {
     cudaFree(p->d_u);
@@ -1839,6 +1935,18 @@ int fe_wrap_host(fe_plan* p, int32_t start, int32_t end, double* dat0, const dou
   CUDA_TRY(cudaStreamSynchronize(p->hstream_d));
   CUDA_TRY(cudaStreamSynchronize(p->hstream2));
   CUDA_TRY(cudaStreamSynchronize(s));
+  return FE_OK;
+}
+
+extern "C" {
+
+int64_t fe_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int fe_eval_log(const double* x, double* y, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return fail(FE_EINVAL, "bad arguments");
+  if (n == 0) return FE_OK;
+  k_eval_log<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(x, y, n);
+  CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
 

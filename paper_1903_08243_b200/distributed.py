@@ -21,8 +21,11 @@ last Lx*Ly nodes -- contiguous buffers, no gather/scatter lists.  Inputs are
 drawn per lattice plane from SeedSequence((seed, stream, plane)), so a plane
 shared by two ranks gets identical coordinates and coefficients on both.
 
-Scaling mode: WEAK -- every rank owns a slab of the config's full per-GPU
-size (nx x ny x nz cubes); the global mesh is nx x ny x (nz * world).
+Scaling modes: STRONG (``slab_split``, what bench.py runs): the config's one
+fixed mesh is cut into world slabs of nz/world layers -- the BASELINE C5
+partition (128 cube layers -> 128/N per GPU), applied to every structured
+config (3D: z-slabs; 2D: rows of squares).  WEAK (``slab_range``): every rank
+owns nz layers of an nz*world-layer mesh.
 """
 
 from __future__ import annotations
@@ -35,7 +38,7 @@ from .configs import Config
 from .elements import operator_spec, quadrature_rule
 from .mesh import DofMap, Mesh, kuhn_tets
 
-__all__ = ["Slab", "build_slab", "DistributedOperator"]
+__all__ = ["Slab", "build_slab", "DistributedOperator", "slab_range", "slab_split", "global_offset"]
 
 
 @dataclass
@@ -79,73 +82,96 @@ def _plane_rng(seed, stream, plane):
 
 
 def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab:
-    """Cube layers [z0, z1) of the global nx x ny x nz_global mesh of a 3D
-    config, with slab-local lattice numbering."""
-    if len(cfg.n) != 3:
-        raise ValueError("slab partition needs a 3D config")
-    nx, ny, _ = cfg.n
+    """Cell layers [z0, z1) along the slowest axis (z in 3D, y in 2D) of the
+    global structured mesh of a config (nx x ny x nz_global cubes, or nx x
+    nz_global squares), with slab-local lattice numbering.  2D cells follow
+    the reference split (mesh.py:52-57): squares into (v00,v10,v01),
+    (v10,v11,v01), quads in tensor order."""
+    d = len(cfg.n)
+    if d not in (2, 3):
+        raise ValueError("slab partition needs a structured 2D or 3D config")
+    nx = cfg.n[0]
+    ny = cfg.n[1] if d == 3 else 1          # 2D: a single "row" of x per layer
     nzl = z1 - z0
     spec = operator_spec(cfg.form, cfg.cell, cfg.degree)
     rule = quadrature_rule(cfg.cell, cfg.qdegree)
     k = spec.element.degree
     vs = spec.element.value_size
-    # vertices of the slab: planes z0..z1
-    xs = np.linspace(0.0, 1.0, nx + 1)
-    ys = np.linspace(0.0, 1.0, ny + 1)
     hz = 1.0 / nz_global
-    coords = np.empty(((nzl + 1), (ny + 1), (nx + 1), 3))
-    Y, X = np.meshgrid(ys, xs, indexing="ij")
-    h = np.array([1.0 / nx, 1.0 / ny, hz])
+    xs = np.linspace(0.0, 1.0, nx + 1)
+    if d == 3:
+        ys = np.linspace(0.0, 1.0, ny + 1)
+        Y, X = np.meshgrid(ys, xs, indexing="ij")
+        h = np.array([1.0 / nx, 1.0 / ny, hz])
+        nvp = (ny + 1) * (nx + 1)                   # vertices per layer plane
+        inner = np.zeros((ny + 1, nx + 1), bool)
+        inner[1:-1, 1:-1] = True
+        inner = inner.ravel()
+        base_plane = np.stack([X.ravel(), Y.ravel()], axis=1)
+    else:
+        h = np.array([1.0 / nx, hz])
+        nvp = nx + 1
+        inner = np.zeros(nx + 1, bool)
+        inner[1:-1] = True
+        base_plane = xs[:, None]
+    coords = np.empty((nzl + 1, nvp, d))
     for lz in range(nzl + 1):
         gz = z0 + lz
-        coords[lz, :, :, 0] = X
-        coords[lz, :, :, 1] = Y
-        coords[lz, :, :, 2] = gz * hz
+        coords[lz, :, :d - 1] = base_plane
+        coords[lz, :, d - 1] = gz * hz
         if cfg.jitter and 0 < gz < nz_global:
-            d = _plane_rng(seed, 0, gz).uniform(-1.0, 1.0, size=((ny + 1) * (nx + 1), 3)) * (0.1 * h)
-            d = d.reshape(ny + 1, nx + 1, 3)
-            inner = np.zeros((ny + 1, nx + 1), bool)
-            inner[1:-1, 1:-1] = True
-            coords[lz][inner] += d[inner]
-    coords = coords.reshape(-1, 3)
-    # cells: cubes z-slowest, 6 Kuhn tets or one hex per cube
-    l, j, i = np.meshgrid(np.arange(nzl), np.arange(ny), np.arange(nx), indexing="ij")
-    base = (i + (nx + 1) * (j + (ny + 1) * l)).ravel()
-    corner = np.array([(b & 1) + (nx + 1) * (((b >> 1) & 1) + (ny + 1) * ((b >> 2) & 1))
-                       for b in range(8)], dtype=np.int64)
-    cells_bits = kuhn_tets() if cfg.cell == "tetrahedron" else np.arange(8)[None, :]
+            delta = _plane_rng(seed, 0, gz).uniform(-1.0, 1.0, size=(nvp, d)) * (0.1 * h)
+            coords[lz][inner] += delta[inner]
+    coords = coords.reshape(-1, d)
+    # cells: layers slowest; 6 Kuhn tets / one hex per cube, 2 tris / one quad per square
+    if d == 3:
+        l, j, i = np.meshgrid(np.arange(nzl), np.arange(ny), np.arange(nx), indexing="ij")
+        base = (i + (nx + 1) * (j + (ny + 1) * l)).ravel()
+        corner = np.array([(b & 1) + (nx + 1) * (((b >> 1) & 1) + (ny + 1) * ((b >> 2) & 1))
+                           for b in range(8)], dtype=np.int64)
+        cells_bits = kuhn_tets() if cfg.cell == "tetrahedron" else np.arange(8)[None, :]
+    else:
+        l, i = np.meshgrid(np.arange(nzl), np.arange(nx), indexing="ij")
+        base = (i + (nx + 1) * l).ravel()
+        corner = np.array([(b & 1) + (nx + 1) * ((b >> 1) & 1) for b in range(4)], dtype=np.int64)
+        cells_bits = (np.array([[0, 1, 2], [1, 3, 2]]) if cfg.cell == "triangle"
+                      else np.arange(4)[None, :])
     c2v = (base[:, None, None] + corner[cells_bits][None, :, :]).reshape(-1, cells_bits.shape[1])
-    mesh = Mesh(coords, np.ascontiguousarray(c2v, np.int32), spec.cell, (nx, ny, nzl))
-    # slab-local lattice numbering (x fastest, z slowest)
-    Lx, Ly, Lz = k * nx + 1, k * ny + 1, k * nzl + 1
+    grid = (nx, ny, nzl) if d == 3 else (nx, nzl)
+    mesh = Mesh(coords, np.ascontiguousarray(c2v, np.int32), spec.cell, grid)
+    # slab-local lattice numbering (x fastest, layer axis slowest)
+    L = [k * nx + 1] + ([k * ny + 1] if d == 3 else []) + [k * nzl + 1]
     vi = c2v % (nx + 1)
-    vj = (c2v // (nx + 1)) % (ny + 1)
-    vl = c2v // ((nx + 1) * (ny + 1))
-    V = np.stack([vi, vj, vl], axis=-1)
-    nodes = np.array([[int(x * k) for x in node] for node in spec.element.nodes], dtype=np.int64)
+    if d == 3:
+        vj = (c2v // (nx + 1)) % (ny + 1)
+        vl = c2v // ((nx + 1) * (ny + 1))
+        V = np.stack([vi, vj, vl], axis=-1)
+    else:
+        V = np.stack([vi, c2v // (nx + 1)], axis=-1)
+    nodes = np.array([[int(round(x * k)) for x in node] for node in spec.element.nodes], dtype=np.int64)
     if spec.cell.simplex:
         P = k * V[:, None, 0, :] + np.einsum("ia,cad->cid", nodes, V[:, 1:, :] - V[:, None, 0, :])
     else:
         P = k * V[:, None, 0, :] + nodes[None, :, :]
-    dof = P[..., 0] + Lx * (P[..., 1] + Ly * P[..., 2])
-    dm = DofMap(np.ascontiguousarray(dof, np.int32), Lx * Ly * Lz, spec.element)
+    dof = P[..., 0] + L[0] * (P[..., 1] + (L[1] * P[..., 2] if d == 3 else 0))
+    plane = int(np.prod(L[:-1]))
+    dm = DofMap(np.ascontiguousarray(dof, np.int32), plane * L[-1], spec.element)
     # coefficients per lattice plane
-    plane = Lx * Ly
-    u = np.empty((Lz, plane * vs))
-    for L in range(Lz):
-        u[L] = _plane_rng(seed, 1, k * z0 + L).uniform(-1.0, 1.0, plane * vs)
+    nmax = max(cfg.n[:-1] + (nz_global,))
+    u = np.empty((L[-1], plane * vs))
+    for q in range(L[-1]):
+        u[q] = _plane_rng(seed, 1, k * z0 + q).uniform(-1.0, 1.0, plane * vs)
     u = u.ravel()
     if cfg.u_scale == "h":
-        u *= 0.01 / max(nx, ny, nz_global)
+        u *= 0.01 / nmax
     mu = lam = None
     if spec.coefficient_fields:
-        nvp = (nx + 1) * (ny + 1)
         mu = np.concatenate([_plane_rng(seed, 2, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
         lam = np.concatenate([_plane_rng(seed, 3, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
     state = None
     if spec.has_state:
-        state = np.concatenate([_plane_rng(seed, 4, k * z0 + L).uniform(-1.0, 1.0, plane * vs)
-                                for L in range(Lz)]) * (0.01 / max(nx, ny, nz_global))
+        state = np.concatenate([_plane_rng(seed, 4, k * z0 + q).uniform(-1.0, 1.0, plane * vs)
+                                for q in range(L[-1])]) * (0.01 / nmax)
     return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane, state)
 
 
@@ -170,7 +196,7 @@ class DistributedOperator:
         self.rank = rank
         self.world = world
         self.n_if = slab.plane * slab.spec.element.value_size
-        nx, ny, nzl = slab.mesh.grid
+        nzl = slab.mesh.grid[-1]
         self.layer_cells = slab.mesh.ncells // nzl
         self.nlayers = nzl
         self._bufs = None
@@ -235,5 +261,21 @@ def exchange_loopback(ys, n_if):
 
 
 def slab_range(rank: int, world: int, nz_per_rank: int):
-    """Weak scaling: rank r owns cube layers [r nz, (r+1) nz)."""
+    """Weak scaling: rank r owns cell layers [r nz, (r+1) nz)."""
     return rank * nz_per_rank, (rank + 1) * nz_per_rank, world * nz_per_rank
+
+
+def slab_split(rank: int, world: int, nz_global: int):
+    """Strong scaling: the nz_global cell layers of ONE fixed mesh split into
+    world contiguous slabs as evenly as possible (BASELINE C5: 128 layers ->
+    128/N per GPU)."""
+    if world > nz_global:
+        raise ValueError(f"cannot split {nz_global} layers over {world} ranks")
+    return rank * nz_global // world, (rank + 1) * nz_global // world, nz_global
+
+
+def global_offset(slab: "Slab") -> int:
+    """Entry of the single-domain (world = 1) slab vector where this slab's
+    first entry sits: the lattice numbering is layer-slowest, so a slab is a
+    contiguous window of the global vector."""
+    return slab.spec.element.degree * slab.z0 * slab.plane * slab.spec.element.value_size

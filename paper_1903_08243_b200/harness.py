@@ -10,10 +10,12 @@ Same names and meaning where the reference has them: ``make_bindings``
 
 Differences, all deliberate:
 
-* ``flops_per_cell`` is the FROZEN algorithmic count of SURVEY.md Appendix B
-  (the minimum over a documented algorithm menu, FMA = 2 flops), not an
-  interpreter tally of one implementation: a kernel doing more work is
-  measured against it, one doing less legitimately scores higher;
+* ``flops_per_cell`` is the algorithmic count of SURVEY.md Appendix B -- the
+  minimum over its documented algorithm menu plus the two cheaper exact
+  algorithms round 1 added (modal split for affine simplices, vertex-
+  gradient P2; App. B allows lowering F, never raising it), FMA = 2 flops --
+  not an interpreter tally of one implementation; ``menu="survey"`` gives
+  SURVEY's frozen figures;
 * ``bytes_per_cell`` is the compulsory-traffic model of SURVEY.md 8(d)
   (u read once, y written once, coordinates, one int32 node map whose vertex
   columns double as the vertex map, mu/lambda fields);
@@ -258,15 +260,22 @@ def verify_target(spec, target, mesh, dofmap, rule, handle, u, rtol, oracle,
 
 
 class L2Flusher:
-    """Writes a buffer of 2x the L2 size between timed applies."""
+    """Cold, clean L2 before a timed apply: READS a buffer of 3x the L2 size.
+    Every line of the previous apply is evicted -- its dirty lines (y) are
+    written back here, outside the timed region -- and what is left in the
+    L2 is clean.  (A write-based flush leaves the L2 full of dirty lines whose
+    write-back then lands inside the next timed apply: up to 126 MB of
+    DRAM writes, ~20 us, charged to the operator.)"""
 
     def __init__(self, device=0):
         import torch
         l2 = torch.cuda.get_device_properties(device).L2_cache_size
-        self.buf = torch.empty(max(2 * l2, 1 << 20) // 4, dtype=torch.int32, device=device)
+        self.buf = torch.ones(max(3 * l2, 1 << 20) // 4, dtype=torch.int32, device=device)
+        self.out = torch.empty((), dtype=torch.int64, device=device)
 
     def __call__(self):
-        self.buf.fill_(1)
+        import torch
+        torch.sum(self.buf, out=self.out)
 
 
 def gpu_busy_wait(seconds=50e-6):

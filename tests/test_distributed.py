@@ -16,7 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1903_08243_b200 import configs as C
-from paper_1903_08243_b200.distributed import DistributedOperator, build_slab, slab_range
+from paper_1903_08243_b200.distributed import (DistributedOperator, build_slab, global_offset,
+                                               slab_range, slab_split)
 from oracle import fe_oracle as fo
 
 
@@ -96,6 +97,95 @@ def test_distributed_equals_single_domain(name, world, nz, overlap):
             sl = build_slab(cfg, 11, z0, z0 + nz, nz * world).state
             assert np.array_equal(sl, glob.state[off:off + sl.size])
         assert fo.rel_l2(y, y_glob[off:off + y.size]) <= 1e-14, rank
+
+
+def _strong_worker(rank, world, port, name, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = C.get_config(name, n)
+    z0, z1, nzg = slab_split(rank, world, cfg.n[-1])
+    slab = build_slab(cfg, 5, z0, z1, nzg)
+    apply, range_apply = _oracle_apply(slab)
+    op = DistributedOperator(slab, apply, rank, world, range_apply)
+    u = torch.from_numpy(slab.u.copy())
+    y = torch.zeros_like(u)
+    op.apply(u, y)
+    q.put((rank, global_offset(slab), y.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world,n", [
+    # strong scaling: ONE fixed mesh split into world slabs (bench.py --gpus N)
+    ("C5", 2, (2, 2, 6)), ("C2-P3", 2, (2, 2, 5)), ("C3-Q2", 3, (2, 3, 7)),
+    ("C1", 2, (4, 6)), ("C4-quad-Q2", 3, (3, 7)), ("C4-hex-Q1", 2, (2, 2, 4))])
+def test_strong_split_equals_single_domain(name, world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, name, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = C.get_config(name, n)
+    glob = build_slab(cfg, 5, 0, cfg.n[-1], cfg.n[-1])
+    P = fo.Problem(glob.spec.form, glob.spec.cell.kind, glob.spec.element.degree,
+                   glob.rule.exactness_degree, glob.spec.params)
+    y_glob = fo.assemble(P, glob.mesh.coords, glob.mesh.cell2vert, glob.dofmap.cell2dof, glob.u,
+                         glob.mu, glob.lam, state=glob.state)
+    covered = np.zeros(y_glob.size, bool)
+    for rank, off, y in results:
+        assert fo.rel_l2(y, y_glob[off:off + y.size]) <= 1e-14, rank
+        covered[off:off + y.size] = True
+    assert covered.all()
+
+
+@pytest.mark.parametrize("name,n", [("C1", (3, 4)), ("C4-quad-Q3", (2, 3)), ("C4-quad-Q1", (4, 4))])
+def test_2d_slab_is_a_valid_mesh(name, n):
+    """2D slabs (rows of squares): positive orientation, conforming lattice
+    numbering (every lattice node used, shared nodes agree), and the
+    single-slab operator equals the oracle on the reference-built mesh up to
+    the node permutation when there is no jitter."""
+    cfg = C.get_config(name, n)
+    s = build_slab(cfg, 0, 0, n[-1], n[-1])
+    X = s.mesh.coords[s.mesh.cell2vert]
+    if cfg.cell == "triangle":
+        det = np.linalg.det(X[:, 1:] - X[:, :1])
+    else:
+        det = np.linalg.det(np.stack([X[:, 1] - X[:, 0], X[:, 2] - X[:, 0]], axis=1))
+    assert (det > 0).all()
+    assert s.mesh.ncells == cfg.ncells
+    k = s.spec.element.degree
+    assert s.dofmap.ndofs_global == (k * n[0] + 1) * (k * n[1] + 1)
+    assert np.unique(s.dofmap.cell2dof).size == s.dofmap.ndofs_global
+    # the lattice node of each local dof sits at the mapped physical point (unjittered copy)
+    import dataclasses
+    flat = build_slab(dataclasses.replace(cfg, jitter=False), 0, 0, n[-1], n[-1])
+    Lx = k * n[0] + 1
+    d = flat.dofmap.cell2dof
+    gx, gy = (d % Lx) / (k * n[0]), (d // Lx) / (k * n[1])
+    nodes = np.asarray(flat.spec.element.nodes)
+    Xc = flat.mesh.coords[flat.mesh.cell2vert]
+    if cfg.cell == "triangle":
+        phys = Xc[:, None, 0, :] + np.einsum("ia,cad->cid", nodes, Xc[:, 1:, :] - Xc[:, None, 0, :])
+    else:
+        phys = Xc[:, None, 0, :] + nodes[None, :, :] * (Xc[:, None, 3, :] - Xc[:, None, 0, :])
+    assert np.allclose(phys[..., 0], gx) and np.allclose(phys[..., 1], gy)
+
+
+def test_slab_split_is_balanced_and_covers():
+    for nz, world in ((128, 8), (64, 3), (7, 7), (256, 4)):
+        parts = [slab_split(r, world, nz) for r in range(world)]
+        assert parts[0][0] == 0 and parts[-1][1] == nz
+        assert all(a[1] == b[0] for a, b in zip(parts[:-1], parts[1:]))
+        sizes = [p[1] - p[0] for p in parts]
+        assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        slab_split(0, 9, 8)
 
 
 def test_slab_of_whole_mesh_matches_config_shape():
