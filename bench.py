@@ -209,7 +209,7 @@ def build_problem_for_rank(name, seed, rank, world):
     """This rank's slab of the config's fixed mesh (strong scaling; the
     whole mesh at world = 1), slab-local lattice numbering."""
     from paper_1903_08243_b200 import configs as C
-    from paper_1903_08243_b200.distributed import build_slab, slab_split
+    from paper_1903_08243_b200.distributed import build_slab, global_dof_index, slab_split
     cfg = C.get_config(name)
     return build_slab(cfg, seed, *slab_split(rank, world, cfg.n[-1]))
 
@@ -291,7 +291,7 @@ def gathered_parity(ops, rank, world, dev, seed):
     import torch.distributed as dist
     import paper_1903_08243_b200 as fe
     from oracle import fe_oracle as fo
-    from paper_1903_08243_b200.distributed import build_slab, slab_split
+    from paper_1903_08243_b200.distributed import build_slab, global_dof_index, slab_split
     worst = 0.0
     for op in ops:
         sizes = torch.zeros(world, dtype=torch.int64, device=dev)
@@ -318,9 +318,8 @@ def gathered_parity(ops, rank, world, dev, seed):
         yg = torch.zeros(glob.ndofs, dtype=torch.float64, device=dev)
         g.apply(torch.tensor(glob.u, device=dev), yg, coef=coef, overwrite=True)
         for r in range(world):
-            off = glob.spec.element.degree * slab_split(r, world, cfg.n[-1])[0] * glob.plane \
-                * glob.spec.element.value_size
-            ref = yg[off:off + ys[r].numel()]
+            sl = build_slab(cfg, seed, *slab_split(r, world, cfg.n[-1]))
+            ref = yg[torch.as_tensor(global_dof_index(sl), device=dev)]
             worst = max(worst, float(torch.linalg.norm(ys[r] - ref) / torch.linalg.norm(ref)))
         del g, yg
     out = torch.tensor([worst], device=dev)
@@ -334,9 +333,12 @@ def gathered_parity(ops, rank, world, dev, seed):
 
 
 def cpu_run(prob, F, start, end, cores):
-    """One timed CPU pass over cells [start, end) of an operator: the
-    reference's own generated C (oracle/_ref, vector-ext w8) where the
-    reference supports the config, else the C restatement of its loop."""
+    """One timed CPU pass over cells [start, end) of an operator on `cores`
+    threads: the reference's own generated vector-ext C (oracle/_ref) where
+    the reference supports the config (C1), else the SIMD-batched port of
+    its cell loop (oracle/fe_cpu_port.cpp: per-(form, degree, rule)
+    specialised, cross-element vectorised, the paper's technique)."""
+    from oracle import fe_cpu_port as fcp
     from oracle import ref_c
     import paper_1903_08243_b200 as fe
     sp = prob.spec
@@ -349,17 +351,22 @@ def cpu_run(prob, F, start, end, cores):
         k.run_threads(end, b, cores, start=start)
         dt = time.perf_counter() - t0
     else:
+        P = oracle_problem(prob)
         out = np.zeros(prob.ndofs)
         t0 = time.perf_counter()
-        _cpu_assemble(prob, start, end, cores, out=out)
+        fcp.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                     prob.mu, prob.lam, start, end, threads=cores, out=out,
+                     state=getattr(prob, "state", None))
         dt = time.perf_counter() - t0
     return dt, F * (end - start), "reference" if use_ref else "port"
 
 
-CPU_PORT_TEXT = ("C restatement of the reference cell loop (oracle/fe_oracle.c, -O3 -ffast-math, "
-                 "OpenMP over cell chunks) where the reference has no code path (tets, hexes, "
-                 "mu/lambda, neo-Hookean); the reference's own generated vector-ext C "
-                 "(oracle/_ref) for C1")
+CPU_PORT_TEXT = ("SIMD-batched port of the reference cell loop (oracle/fe_cpu_port.cpp: the reference's "
+                 "quadrature-loop local kernel specialised per (form, degree, rule) with compile-time "
+                 "sizes, cross-element vectorised 8 cells per AVX-512 vector as the paper does, OpenMP "
+                 "over cell chunks) where the reference has no code path (tets, hexes, mu/lambda, "
+                 "neo-Hookean); the reference's own generated vector-ext C (oracle/_ref, its "
+                 "BENCH_FLAGS) for C1")
 
 
 def cpu_measure(ops, budget_s=20.0):
@@ -631,7 +638,7 @@ def run_reference(args):
         sf = st = 0.0
         for prob, F in probs:
             C = prob.mesh.ncells
-            w = -(-C // K)
+            w = -(-(-(-C // K)) // 8) * 8          # ceil(C/K), a multiple of the SIMD width
             a, b = min(C, s * w), min(C, (s + 1) * w)
             if a >= b:
                 continue
@@ -644,8 +651,8 @@ def run_reference(args):
             secs += st
     value = flop / secs / 1e9
     kind = "reference" if kinds == {"reference"} else "port"
-    sample = (CPU_PORT_TEXT + f"; step s applies cells [s*ceil(C/{K}), (s+1)*ceil(C/{K})) of every "
-              f"operator, so the {K} timed steps cover every full BASELINE mesh once")
+    sample = (CPU_PORT_TEXT + f"; step s applies cells [s*w, (s+1)*w), w = ceil(C/{K}) rounded up to 8, of "
+              f"every operator, so the {K} timed steps cover every full BASELINE mesh once")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup,

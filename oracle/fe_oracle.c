@@ -28,7 +28,7 @@
 #endif
 
 enum { MASS = 0, HELMHOLTZ = 1, LAPLACIAN = 2, ELASTICITY = 3, LAPLACIAN_SCALAR = 4,
-       ELASTICITY_LAME = 5, NEOHOOKEAN = 6 };
+       ELASTICITY_LAME = 5, NEOHOOKEAN = 6, NEOHOOKEAN_TANGENT = 7 };
 
 #define MAXD 3
 
@@ -63,7 +63,7 @@ typedef struct {
 
 /* local kernel of one cell: A[nd*vs] from X[nv][dim], w[nd*vs] */
 static void local_kernel(const problem* P, const double* X, const double* w, const double* muv,
-                         const double* lamv, double* A) {
+                         const double* lamv, const double* w0, double* A) {
   const int d = P->dim, nd = P->nd, vs = P->vs, nv = P->nv;
   double J[MAXD][MAXD], Ji[MAXD][MAXD], absdet = 0.0;
   memset(A, 0, sizeof(double) * nd * vs);
@@ -121,6 +121,37 @@ static void local_kernel(const problem* P, const double* X, const double* w, con
         double ll = P->p1 * log(Jf);
         for (int c = 0; c < d; ++c)
           for (int a = 0; a < d; ++a) T[c][a] = P->p0 * (F[c][a] - Fi[a][c]) + ll * Fi[a][c];
+      } else if (P->form == NEOHOOKEAN_TANGENT) {
+        /* dP = mu dF + (mu - lam ln J) F^-T dF^T F^-T + lam tr(F^-1 dF) F^-T
+         * at F = I + grad u0 (oracle/fe_oracle.py _local, neohookean_tangent) */
+        double g0[MAXD][MAXD] = {{0}}, F[MAXD][MAXD], Fi[MAXD][MAXD];
+        for (int i = 0; i < nd; ++i)
+          for (int c = 0; c < vs; ++c)
+            for (int b = 0; b < d; ++b) g0[c][b] += dp[i * d + b] * w0[i * vs + c];
+        for (int c = 0; c < d; ++c)
+          for (int a = 0; a < d; ++a) {
+            double s = 0.0;
+            for (int b = 0; b < d; ++b) s += Ji[b][a] * g0[c][b];
+            F[c][a] = s + (c == a ? 1.0 : 0.0);
+          }
+        double Jf = det_inv(d, F, Fi);
+        double tr = 0.0;                        /* tr(F^-1 dF) */
+        for (int a = 0; a < d; ++a)
+          for (int c = 0; c < d; ++c) tr += Fi[a][c] * G[c][a];
+        double M[MAXD][MAXD];                   /* dF^T F^-T: M[a][e] = sum_c dF[c][a] Fi[e][c] */
+        for (int a = 0; a < d; ++a)
+          for (int e = 0; e < d; ++e) {
+            double s = 0.0;
+            for (int c = 0; c < d; ++c) s += G[c][a] * Fi[e][c];
+            M[a][e] = s;
+          }
+        const double cA = P->p0 - P->p1 * log(Jf);
+        for (int c = 0; c < d; ++c)
+          for (int a = 0; a < d; ++a) {
+            double s = 0.0;                     /* (F^-T M)[c][a] = sum_b Fi[b][c] M[b][a] */
+            for (int b = 0; b < d; ++b) s += Fi[b][c] * M[b][a];
+            T[c][a] = P->p0 * G[c][a] + cA * s + P->p1 * tr * Fi[a][c];
+          }
       } else {
         for (int c = 0; c < vs; ++c)
           for (int a = 0; a < d; ++a) T[c][a] = G[c][a];
@@ -143,17 +174,23 @@ static void local_kernel(const problem* P, const double* X, const double* w, con
   }
 }
 
+/* mu: the vertex field mu (elasticity_lame) or the state u0, a dof field
+ * in the layout of u (neohookean_tangent, as the GPU ABI's coef0) */
 static void gather(const problem* P, int64_t n, const double* coords, const double* u,
                    const int32_t* map0, const int32_t* map1, const double* mu, const double* lam,
-                   double* X, double* w, double* muv, double* lamv) {
+                   double* X, double* w, double* muv, double* lamv, double* w0) {
   const int d = P->dim, nd = P->nd, vs = P->vs, nv = P->nv;
+  const int state = P->form == NEOHOOKEAN_TANGENT;
   for (int v = 0; v < nv; ++v) {
     int vid = map1[n * nv + v];
     for (int a = 0; a < d; ++a) X[v * d + a] = coords[(int64_t)vid * d + a];
-    if (mu) { muv[v] = mu[vid]; lamv[v] = lam[vid]; }
+    if (mu && !state) { muv[v] = mu[vid]; lamv[v] = lam[vid]; }
   }
   for (int i = 0; i < nd; ++i)
-    for (int c = 0; c < vs; ++c) w[i * vs + c] = u[(int64_t)vs * map0[n * nd + i] + c];
+    for (int c = 0; c < vs; ++c) {
+      w[i * vs + c] = u[(int64_t)vs * map0[n * nd + i] + c];
+      if (state) w0[i * vs + c] = mu[(int64_t)vs * map0[n * nd + i] + c];
+    }
 }
 
 /* single-threaded wrap_<form> restatement: y += sum over [start,end) */
@@ -165,14 +202,16 @@ void fe_oracle_apply(int form, int dim, int nv, int nd, int vs, int nq, int affi
   problem P = {form, dim, nv, nd, vs, nq, affine, qw, phi, dphi, gphi, gdphi, p0, p1};
   double X[8 * MAXD], muv[8], lamv[8];
   double* w = malloc(sizeof(double) * nd * vs);
+  double* w0 = malloc(sizeof(double) * nd * vs);
   double* A = malloc(sizeof(double) * nd * vs);
   for (int64_t n = start; n < end; ++n) {
-    gather(&P, n, coords, u, map0, map1, mu, lam, X, w, muv, lamv);
-    local_kernel(&P, X, w, muv, lamv, A);
+    gather(&P, n, coords, u, map0, map1, mu, lam, X, w, muv, lamv, w0);
+    local_kernel(&P, X, w, muv, lamv, w0, A);
     for (int j = 0; j < nd; ++j)
       for (int c = 0; c < vs; ++c) y[(int64_t)vs * map0[n * nd + j] + c] += A[j * vs + c];
   }
   free(w);
+  free(w0);
   free(A);
 }
 
@@ -190,12 +229,14 @@ void fe_oracle_apply_mt(int form, int dim, int nv, int nd, int vs, int nq, int a
   {
     double X[8 * MAXD], muv[8], lamv[8];
     double* w = malloc(sizeof(double) * L);
+    double* w0 = malloc(sizeof(double) * L);
 #pragma omp for schedule(static)
     for (int64_t c = start; c < end; ++c) {
-      gather(&P, c, coords, u, map0, map1, mu, lam, X, w, muv, lamv);
-      local_kernel(&P, X, w, muv, lamv, buf + (c - start) * L);
+      gather(&P, c, coords, u, map0, map1, mu, lam, X, w, muv, lamv, w0);
+      local_kernel(&P, X, w, muv, lamv, w0, buf + (c - start) * L);
     }
     free(w);
+    free(w0);
   }
   for (int64_t c = start; c < end; ++c) {
     const double* A = buf + (c - start) * L;

@@ -13,7 +13,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "liboracle.so")
 FORMS = {"mass": 0, "helmholtz": 1, "laplacian": 2, "elasticity": 3, "laplacian_scalar": 4,
-         "elasticity_lame": 5, "neohookean": 6}
+         "elasticity_lame": 5, "neohookean": 6, "neohookean_tangent": 7}
 _lib = None
 
 
@@ -33,8 +33,9 @@ def _p(a, t=ctypes.c_double):
 
 
 def assemble(P, coords, cell2vert, cell2dof, u, mu=None, lam=None, start=0, end=None,
-             threads=1, out=None):
-    """Same contract as fe_oracle.assemble, computed by the C loop."""
+             threads=1, out=None, state=None):
+    """Same contract as fe_oracle.assemble, computed by the C loop
+    (``state``: the linearisation point u0 of neohookean_tangent)."""
     lib = load()
     coords = np.ascontiguousarray(coords, np.float64)
     c2v = np.ascontiguousarray(cell2vert, np.int32)
@@ -46,6 +47,10 @@ def assemble(P, coords, cell2vert, cell2dof, u, mu=None, lam=None, start=0, end=
     if mu is not None:
         mu = np.ascontiguousarray(mu, np.float64)
         lam = np.ascontiguousarray(lam, np.float64)
+    if P.form == "neohookean_tangent":
+        if state is None:
+            raise ValueError("neohookean_tangent needs the state u0")
+        mu, lam = np.ascontiguousarray(state, np.float64), None   # passed as the dof field mu
     affine = 1 if P.kind in ("triangle", "tetrahedron") else 0
     p0, p1 = (P.params + (0.0, 0.0))[:2] if P.params else (0.0, 0.0)
     args = [FORMS[P.form], P.d, P.nv, P.nd, P.vs, len(P.qw), affine] + [_p(t) for t in tabs] + [

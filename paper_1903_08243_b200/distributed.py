@@ -15,11 +15,15 @@ group per apply).  Both neighbours end with the fully summed interface
 values, so the distributed y restricted to each slab equals the
 single-domain y (partition independence, reference test_reference.py:72-89).
 
-Slab-local numbering: nodes of the k-refined lattice in lexicographic order
-(x fastest, z slowest), so the bottom/top interface planes are the first and
-last Lx*Ly nodes -- contiguous buffers, no gather/scatter lists.  Inputs are
-drawn per lattice plane from SeedSequence((seed, stream, plane)), so a plane
-shared by two ranks gets identical coordinates and coefficients on both.
+Slab-local numbering: nodes of the k-refined lattice, vertex points first
+(dof id = vertex id, as the reference numbers them, mesh.py:95 -- the
+kernels then read no separate vertex map), then the other lattice points,
+both lexicographic (x fastest, z slowest).  An interface plane is therefore
+two contiguous blocks (its vertex points at the start/end of the vertex
+section, its other points at the start/end of the rest): no gather lists.
+Inputs are drawn per lattice plane from SeedSequence((seed, stream, plane)),
+so a plane shared by two ranks gets identical coordinates and coefficients
+on both.
 
 Scaling modes: STRONG (``slab_split``, what bench.py runs): the config's one
 fixed mesh is cut into world slabs of nz/world layers -- the BASELINE C5
@@ -38,7 +42,7 @@ from .configs import Config
 from .elements import operator_spec, quadrature_rule
 from .mesh import DofMap, Mesh, kuhn_tets
 
-__all__ = ["Slab", "build_slab", "DistributedOperator", "slab_range", "slab_split", "global_offset"]
+__all__ = ["Slab", "build_slab", "DistributedOperator", "slab_range", "slab_split", "global_dof_index", "exchange_loopback", "vertex_first_ids"]
 
 
 @dataclass
@@ -56,6 +60,21 @@ class Slab:
     nz_global: int
     plane: int         # nodes per lattice plane (Lx * Ly)
     state: np.ndarray = None   # u0 of a linearised form (C6), per-plane seeded like u
+    nvert: int = 0             # vertices of the slab (= vertex dofs, numbered first)
+    nvp: int = 0               # vertices per layer plane
+    global_index: np.ndarray = None   # single-domain scalar dof id of every slab dof
+
+    def interface_ranges(self, side: str):
+        """Scalar-dof ranges [a, b) of the interface node plane at the bottom
+        (``"below"``) or top (``"above"``) of the slab: its vertex points
+        (a block of the vertex section) and its other lattice points (a
+        block of the rest), both in lexicographic order on either side of
+        the interface."""
+        n = self.dofmap.ndofs_global
+        rest = self.plane - self.nvp          # non-vertex points of a vertex plane
+        if side == "below":
+            return [(0, self.nvp), (self.nvert, self.nvert + rest)]
+        return [(self.nvert - self.nvp, self.nvert), (n - rest, n)]
 
     def coef(self):
         if self.mu is not None:
@@ -79,6 +98,36 @@ class Slab:
 
 def _plane_rng(seed, stream, plane):
     return np.random.default_rng(np.random.SeedSequence([seed, stream, plane]))
+
+
+def vertex_first_ids(P, ncells_per_axis, k):
+    """Dof id of lattice points P[..., d] on the k-refined lattice of an
+    n_0 x ... x n_{d-1} structured mesh: vertex points (all coordinates
+    multiples of k) first with id = vertex id, then the other points in
+    lexicographic order (x fastest) -- mesh.py _lattice_numbering, 2D or 3D."""
+    d = len(ncells_per_axis)
+    nv1 = [n + 1 for n in ncells_per_axis]
+    Lk = [k * n + 1 for n in ncells_per_axis]
+    cdiv = lambda a: -(-a // k)
+    lin = np.zeros(P.shape[:-1], dtype=np.int64)
+    vid = np.zeros(P.shape[:-1], dtype=np.int64)
+    before = np.zeros(P.shape[:-1], dtype=np.int64)
+    is_vertex = np.ones(P.shape[:-1], dtype=bool)
+    stride_l, stride_v = 1, 1
+    for a in range(d):
+        lin += P[..., a] * stride_l
+        vid += (P[..., a] // k) * stride_v
+        stride_l *= Lk[a]
+        stride_v *= nv1[a]
+    # vertex points strictly before P in lexicographic order (slowest axis first)
+    on_vertex_rows = np.ones(P.shape[:-1], dtype=bool)
+    for a in range(d - 1, -1, -1):
+        below = int(np.prod(nv1[:a])) if a > 0 else 1
+        before += np.where(on_vertex_rows, cdiv(P[..., a]) * below, 0)
+        on_vertex_rows &= P[..., a] % k == 0
+        is_vertex &= P[..., a] % k == 0
+    nverts = int(np.prod(nv1))
+    return np.where(is_vertex, vid, nverts + lin - before)
 
 
 def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab:
@@ -139,8 +188,12 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
     c2v = (base[:, None, None] + corner[cells_bits][None, :, :]).reshape(-1, cells_bits.shape[1])
     grid = (nx, ny, nzl) if d == 3 else (nx, nzl)
     mesh = Mesh(coords, np.ascontiguousarray(c2v, np.int32), spec.cell, grid)
-    # slab-local lattice numbering (x fastest, layer axis slowest)
-    L = [k * nx + 1] + ([k * ny + 1] if d == 3 else []) + [k * nzl + 1]
+    # slab-local numbering: lattice points, VERTEX POINTS FIRST (dof id =
+    # vertex id, so map0[:, :nv] is the vertex map -- reference mesh.py:95,
+    # no separate vertex-map traffic), then the other lattice points, both
+    # lexicographic (x fastest, layer axis slowest)
+    nper = (nx, ny, nzl) if d == 3 else (nx, nzl)
+    L = [k * n + 1 for n in nper]
     vi = c2v % (nx + 1)
     if d == 3:
         vj = (c2v // (nx + 1)) % (ny + 1)
@@ -153,15 +206,29 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
         P = k * V[:, None, 0, :] + np.einsum("ia,cad->cid", nodes, V[:, 1:, :] - V[:, None, 0, :])
     else:
         P = k * V[:, None, 0, :] + nodes[None, :, :]
-    dof = P[..., 0] + L[0] * (P[..., 1] + (L[1] * P[..., 2] if d == 3 else 0))
+    dof = vertex_first_ids(P, nper, k)
     plane = int(np.prod(L[:-1]))
-    dm = DofMap(np.ascontiguousarray(dof, np.int32), plane * L[-1], spec.element)
-    # coefficients per lattice plane
+    nlat = plane * L[-1]
+    dm = DofMap(np.ascontiguousarray(dof, np.int32), nlat, spec.element)
+    # single-domain (world = 1) id of every slab dof: the same numbering on
+    # the whole mesh, lattice points shifted by k z0 layers
+    Pg = P.copy()
+    Pg[..., -1] += k * z0
+    gid = vertex_first_ids(Pg, tuple(nper[:-1]) + (nz_global,), k)
+    global_index = np.empty(nlat, dtype=np.int64)
+    global_index[dof.ravel()] = gid.ravel()
+    # lattice value arrays (u, state) are drawn per lattice plane; permute
+    # them into the vertex-first numbering
+    lat = np.empty(nlat, dtype=np.int64)                      # lexicographic id of each dof
+    lin = P[..., 0] + L[0] * (P[..., 1] + (L[1] * P[..., 2] if d == 3 else 0))
+    lat[dof.ravel()] = lin.ravel()
+    # coefficients per lattice plane (seeded per global plane, so a plane two
+    # slabs share gets identical values on both)
     nmax = max(cfg.n[:-1] + (nz_global,))
-    u = np.empty((L[-1], plane * vs))
+    ulat = np.empty((L[-1], plane * vs))
     for q in range(L[-1]):
-        u[q] = _plane_rng(seed, 1, k * z0 + q).uniform(-1.0, 1.0, plane * vs)
-    u = u.ravel()
+        ulat[q] = _plane_rng(seed, 1, k * z0 + q).uniform(-1.0, 1.0, plane * vs)
+    u = ulat.reshape(nlat, vs)[lat].ravel()
     if cfg.u_scale == "h":
         u *= 0.01 / nmax
     mu = lam = None
@@ -170,9 +237,12 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
         lam = np.concatenate([_plane_rng(seed, 3, z0 + lz).uniform(0.5, 2.0, nvp) for lz in range(nzl + 1)])
     state = None
     if spec.has_state:
-        state = np.concatenate([_plane_rng(seed, 4, k * z0 + q).uniform(-1.0, 1.0, plane * vs)
-                                for q in range(L[-1])]) * (0.01 / nmax)
-    return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane, state)
+        slat = np.concatenate([_plane_rng(seed, 4, k * z0 + q).uniform(-1.0, 1.0, plane * vs)
+                               for q in range(L[-1])])
+        state = slat.reshape(nlat, vs)[lat].ravel() * (0.01 / nmax)
+    nvert = (nzl + 1) * nvp
+    return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane, state,
+                nvert, nvp, global_index)
 
 
 class DistributedOperator:
@@ -195,7 +265,10 @@ class DistributedOperator:
         self.range_apply = range_apply
         self.rank = rank
         self.world = world
-        self.n_if = slab.plane * slab.spec.element.value_size
+        vs = slab.spec.element.value_size
+        self.ranges = {side: [(vs * a, vs * b) for a, b in slab.interface_ranges(side)]
+                       for side in ("below", "above")}
+        self.n_if = sum(b - a for a, b in self.ranges["below"])
         nzl = slab.mesh.grid[-1]
         self.layer_cells = slab.mesh.ncells // nzl
         self.nlayers = nzl
@@ -204,32 +277,42 @@ class DistributedOperator:
     def _buffers(self, y):
         import torch
         if self._bufs is None or self._bufs[0].device != y.device:
-            self._bufs = (torch.empty(self.n_if, dtype=y.dtype, device=y.device),
-                          torch.empty(self.n_if, dtype=y.dtype, device=y.device))
+            self._bufs = tuple(torch.empty(self.n_if, dtype=y.dtype, device=y.device) for _ in range(4))
         return self._bufs
+
+    def _pack(self, y, side, out):
+        o = 0
+        for a, b in self.ranges[side]:
+            out[o:o + b - a] = y[a:b]
+            o += b - a
+        return out
+
+    def _unpack_add(self, y, side, buf):
+        o = 0
+        for a, b in self.ranges[side]:
+            y[a:b] += buf[o:o + b - a]
+            o += b - a
 
     def _start_exchange(self, y):
         import torch.distributed as dist
-        n = self.n_if
-        below, above = self._buffers(y)
+        below, above, send_b, send_a = self._buffers(y)
         ops = []
         if self.slab.has_below:
-            ops.append(dist.P2POp(dist.isend, y[:n], self.rank - 1))
+            ops.append(dist.P2POp(dist.isend, self._pack(y, "below", send_b), self.rank - 1))
             ops.append(dist.P2POp(dist.irecv, below, self.rank - 1))
         if self.slab.has_above:
-            ops.append(dist.P2POp(dist.isend, y[-n:], self.rank + 1))
+            ops.append(dist.P2POp(dist.isend, self._pack(y, "above", send_a), self.rank + 1))
             ops.append(dist.P2POp(dist.irecv, above, self.rank + 1))
         return dist.batch_isend_irecv(ops) if ops else []
 
     def _finish_exchange(self, y, works):
         for w in works:
             w.wait()
-        n = self.n_if
-        below, above = self._bufs if self._bufs else (None, None)
+        below, above = (self._bufs[0], self._bufs[1]) if self._bufs else (None, None)
         if self.slab.has_below:
-            y[:n] += below
+            self._unpack_add(y, "below", below)
         if self.slab.has_above:
-            y[-n:] += above
+            self._unpack_add(y, "above", above)
 
     def exchange(self, y):
         """Sum the interface planes with the neighbours (in place)."""
@@ -250,14 +333,16 @@ class DistributedOperator:
         return y
 
 
-def exchange_loopback(ys, n_if):
+def exchange_loopback(ys, slabs):
     """In-process equivalent of DistributedOperator.exchange for a list of
     consecutive slabs' y vectors (one process driving several slabs, e.g. on
     one GPU): both neighbours of every interface end with the sum."""
-    for lo, hi in zip(ys[:-1], ys[1:]):
-        s = lo[-n_if:] + hi[:n_if]
-        lo[-n_if:] = s
-        hi[:n_if] = s
+    for (lo, slo), (hi, shi) in zip(zip(ys[:-1], slabs[:-1]), zip(ys[1:], slabs[1:])):
+        vs = slo.spec.element.value_size
+        for (a0, a1), (b0, b1) in zip(slo.interface_ranges("above"), shi.interface_ranges("below")):
+            s = lo[vs * a0:vs * a1] + hi[vs * b0:vs * b1]
+            lo[vs * a0:vs * a1] = s
+            hi[vs * b0:vs * b1] = s
 
 
 def slab_range(rank: int, world: int, nz_per_rank: int):
@@ -274,8 +359,10 @@ def slab_split(rank: int, world: int, nz_global: int):
     return rank * nz_global // world, (rank + 1) * nz_global // world, nz_global
 
 
-def global_offset(slab: "Slab") -> int:
-    """Entry of the single-domain (world = 1) slab vector where this slab's
-    first entry sits: the lattice numbering is layer-slowest, so a slab is a
-    contiguous window of the global vector."""
-    return slab.spec.element.degree * slab.z0 * slab.plane * slab.spec.element.value_size
+def global_dof_index(slab: "Slab"):
+    """Entries of the single-domain (world = 1) vector that this slab's
+    vector holds, in slab order (value size included): y_slab = y_glob[idx]
+    after the halo sums (partition independence)."""
+    vs = slab.spec.element.value_size
+    g = slab.global_index
+    return (vs * g[:, None] + np.arange(vs)[None, :]).ravel()

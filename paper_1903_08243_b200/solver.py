@@ -93,13 +93,16 @@ class SlabDot:
     rank), all-reduced over ``torch.distributed``."""
 
     def __init__(self, slab, rank: int, world: int):
-        self.n_if = slab.plane * slab.spec.element.value_size
-        self.skip = self.n_if if (slab.has_below and world > 1) else 0
+        vs = slab.spec.element.value_size
+        self.skip = ([(vs * a, vs * b) for a, b in slab.interface_ranges("below")]
+                     if (slab.has_below and world > 1) else [])
         self.world = world
 
     def __call__(self, a, b):
         import torch.distributed as dist
-        s = (a[self.skip:] * b[self.skip:]).sum()
+        s = (a * b).sum()
+        for lo, hi in self.skip:                 # the lower rank owns the shared plane
+            s = s - (a[lo:hi] * b[lo:hi]).sum()
         if self.world > 1:
             dist.all_reduce(s)
         return s

@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1903_08243_b200 import configs as C
-from paper_1903_08243_b200.distributed import (DistributedOperator, build_slab, global_offset,
+from paper_1903_08243_b200.distributed import (DistributedOperator, build_slab, global_dof_index,
                                                slab_range, slab_split)
 from oracle import fe_oracle as fo
 
@@ -61,7 +61,8 @@ def _worker(rank, world, port, name, nz, q, overlap=False):
     u = torch.from_numpy(slab.u.copy())
     y = torch.zeros_like(u)
     op.apply(u, y)
-    q.put((rank, z0, y.numpy().copy(), slab.u.copy()))
+    st = None if slab.state is None else slab.state.copy()
+    q.put((rank, global_dof_index(slab), y.numpy().copy(), slab.u.copy(), st))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -88,15 +89,11 @@ def test_distributed_equals_single_domain(name, world, nz, overlap):
                    glob.rule.exactness_degree, glob.spec.params)
     y_glob = fo.assemble(P, glob.mesh.coords, glob.mesh.cell2vert, glob.dofmap.cell2dof, glob.u,
                          glob.mu, glob.lam, state=glob.state)
-    k = glob.spec.element.degree
-    per_plane = glob.plane * glob.spec.element.value_size
-    for rank, z0, y, u in results:
-        off = k * z0 * per_plane
-        assert np.array_equal(u, glob.u[off:off + u.size])          # consistent inputs
+    for rank, idx, y, u, st in results:
+        assert np.array_equal(u, glob.u[idx])                       # consistent inputs
         if glob.state is not None:                                  # (and state planes)
-            sl = build_slab(cfg, 11, z0, z0 + nz, nz * world).state
-            assert np.array_equal(sl, glob.state[off:off + sl.size])
-        assert fo.rel_l2(y, y_glob[off:off + y.size]) <= 1e-14, rank
+            assert np.array_equal(st, glob.state[idx])
+        assert fo.rel_l2(y, y_glob[idx]) <= 1e-14, rank
 
 
 def _strong_worker(rank, world, port, name, n, q):
@@ -111,7 +108,7 @@ def _strong_worker(rank, world, port, name, n, q):
     u = torch.from_numpy(slab.u.copy())
     y = torch.zeros_like(u)
     op.apply(u, y)
-    q.put((rank, global_offset(slab), y.numpy().copy()))
+    q.put((rank, global_dof_index(slab), y.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -138,9 +135,9 @@ def test_strong_split_equals_single_domain(name, world, n):
     y_glob = fo.assemble(P, glob.mesh.coords, glob.mesh.cell2vert, glob.dofmap.cell2dof, glob.u,
                          glob.mu, glob.lam, state=glob.state)
     covered = np.zeros(y_glob.size, bool)
-    for rank, off, y in results:
-        assert fo.rel_l2(y, y_glob[off:off + y.size]) <= 1e-14, rank
-        covered[off:off + y.size] = True
+    for rank, idx, y in results:
+        assert fo.rel_l2(y, y_glob[idx]) <= 1e-14, rank
+        covered[idx] = True
     assert covered.all()
 
 
@@ -165,9 +162,17 @@ def test_2d_slab_is_a_valid_mesh(name, n):
     # the lattice node of each local dof sits at the mapped physical point (unjittered copy)
     import dataclasses
     flat = build_slab(dataclasses.replace(cfg, jitter=False), 0, 0, n[-1], n[-1])
-    Lx = k * n[0] + 1
+    from paper_1903_08243_b200.distributed import vertex_first_ids
+    Lx, Ly = k * n[0] + 1, k * n[1] + 1
+    J, I = np.meshgrid(np.arange(Ly), np.arange(Lx), indexing="ij")
+    pts = np.stack([I.ravel(), J.ravel()], axis=-1)
+    ids = vertex_first_ids(pts, n, k)
+    assert np.array_equal(np.sort(ids), np.arange(Lx * Ly))          # a permutation of the lattice
+    lat = np.empty((Lx * Ly, 2), np.int64)
+    lat[ids] = pts
     d = flat.dofmap.cell2dof
-    gx, gy = (d % Lx) / (k * n[0]), (d // Lx) / (k * n[1])
+    gx, gy = lat[d, 0] / (k * n[0]), lat[d, 1] / (k * n[1])
+    assert np.array_equal(d[:, :flat.spec.cell.nvertices], flat.mesh.cell2vert)   # vertex dofs first
     nodes = np.asarray(flat.spec.element.nodes)
     Xc = flat.mesh.coords[flat.mesh.cell2vert]
     if cfg.cell == "triangle":
@@ -200,9 +205,25 @@ def test_slab_of_whole_mesh_matches_config_shape():
 
 
 def test_loopback_exchange_matches_distributed_semantics():
+    """Three slabs in one process: after exchange_loopback both copies of
+    every interface node hold the sum, every other entry is untouched."""
     from paper_1903_08243_b200.distributed import exchange_loopback
-    a, b, c = torch.arange(6.0), torch.arange(6.0) + 10, torch.arange(6.0) + 20
-    exchange_loopback([a, b, c], 2)
-    assert a.tolist() == [0, 1, 2, 3, 14, 16]
-    assert b.tolist() == [14, 16, 12, 13, 34, 36]
-    assert c.tolist() == [34, 36, 22, 23, 24, 25]
+    cfg = C.get_config("C2-P2", (2, 2, 3))
+    slabs = [build_slab(cfg, 0, *slab_split(r, 3, 3)) for r in range(3)]
+    ys = [torch.arange(s.ndofs, dtype=torch.float64) + 1000 * r for r, s in enumerate(slabs)]
+    before = [y.clone() for y in ys]
+    exchange_loopback(ys, slabs)
+    for r, (s, y, y0) in enumerate(zip(slabs, ys, before)):
+        touched = np.zeros(s.ndofs, bool)
+        for side, nb in (("below", r - 1), ("above", r + 1)):
+            if not 0 <= nb < 3:
+                continue
+            other = "above" if side == "below" else "below"
+            for (a, b), (c, d) in zip(s.interface_ranges(side), slabs[nb].interface_ranges(other)):
+                assert torch.equal(y[a:b], y0[a:b] + before[nb][c:d])
+                touched[a:b] = True
+        assert torch.equal(y[~torch.from_numpy(touched)], y0[~torch.from_numpy(touched)])
+    # interface nodes sit at the same physical points on both sides
+    for lo, hi in zip(slabs[:-1], slabs[1:]):
+        for (a, b), (c, d) in zip(lo.interface_ranges("above"), hi.interface_ranges("below")):
+            assert np.array_equal(lo.global_index[a:b], hi.global_index[c:d])

@@ -8,7 +8,7 @@ import pytest
 
 import paper_1903_08243_b200 as fe
 from paper_1903_08243_b200 import configs as C
-from paper_1903_08243_b200.distributed import build_slab, exchange_loopback, slab_range
+from paper_1903_08243_b200.distributed import build_slab, exchange_loopback, global_dof_index, slab_range
 from oracle import fe_oracle as fo
 
 pytestmark = pytest.mark.gpu
@@ -45,16 +45,13 @@ def test_slabs_on_gpu_equal_single_domain(name, world, nz, split):
             h.apply(u, y, coef=coef, overwrite=True)
         ys.append(y)
         slabs.append(s)
-    exchange_loopback(ys, slabs[0].plane * slabs[0].spec.element.value_size)
+    exchange_loopback(ys, slabs)
     torch.cuda.synchronize()
     glob = build_slab(cfg, 9, 0, nz * world, nz * world)
     P = fo.Problem(glob.spec.form, glob.spec.cell.kind, glob.spec.element.degree,
                    glob.rule.exactness_degree, glob.spec.params)
     yg = fo.assemble(P, glob.mesh.coords, glob.mesh.cell2vert, glob.dofmap.cell2dof, glob.u,
                      glob.mu, glob.lam)
-    k = glob.spec.element.degree
-    per_plane = glob.plane * glob.spec.element.value_size
     for s, y in zip(slabs, ys):
-        off = k * s.z0 * per_plane
         y = y.cpu().numpy()
-        assert fo.rel_l2(y, yg[off:off + y.size]) <= 1e-12
+        assert fo.rel_l2(y, yg[global_dof_index(s)]) <= 1e-12
