@@ -332,7 +332,7 @@ def gathered_parity(ops, rank, world, dev, seed):
 # ---------------------------------------------------------------------------
 
 
-def cpu_run(prob, F, start, end, cores):
+def cpu_run(prob, F, start, end, cores, out=None):
     """One timed CPU pass over cells [start, end) of an operator on `cores`
     threads: the reference's own generated vector-ext C (oracle/_ref) where
     the reference supports the config (C1), else the SIMD-batched port of
@@ -352,7 +352,8 @@ def cpu_run(prob, F, start, end, cores):
         dt = time.perf_counter() - t0
     else:
         P = oracle_problem(prob)
-        out = np.zeros(prob.ndofs)
+        if out is None:
+            out = np.zeros(prob.ndofs)
         t0 = time.perf_counter()
         fcp.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
                      prob.mu, prob.lam, start, end, threads=cores, out=out,
@@ -378,9 +379,11 @@ def cpu_measure(ops, budget_s=20.0):
     kinds, desc = set(), []
     for op in ops:
         n = 1024
+        out = np.zeros(op["ndofs"])
+        out.fill(0.0)                        # pages mapped outside the timer
         while True:
             end = min(n, op["C"])
-            dt, fl, kind = cpu_run(op["prob"], op["F"], 0, end, cores)
+            dt, fl, kind = cpu_run(op["prob"], op["F"], 0, end, cores, out)
             if dt > per / 3 or end >= op["C"]:
                 break
             n *= 2
@@ -629,6 +632,9 @@ def run_reference(args):
         return
     names = WORKLOADS[args.config]
     probs = [(build_problem_for_rank(n, args.seed, 0, 1), op_meta(n)["F"]) for n in names]
+    outs = [np.zeros(p.ndofs) for p, _ in probs]
+    for o in outs:
+        o.fill(0.0)                          # pages mapped outside the timer
     cores = len(os.sched_getaffinity(0))
     K = args.steps
     flop = secs = 0.0
@@ -636,13 +642,13 @@ def run_reference(args):
     for it in range(args.warmup + K):
         s = 0 if it < args.warmup else it - args.warmup
         sf = st = 0.0
-        for prob, F in probs:
+        for (prob, F), out in zip(probs, outs):
             C = prob.mesh.ncells
             w = -(-(-(-C // K)) // 8) * 8          # ceil(C/K), a multiple of the SIMD width
             a, b = min(C, s * w), min(C, (s + 1) * w)
             if a >= b:
                 continue
-            dt, fl, kind = cpu_run(prob, F, a, b, cores)
+            dt, fl, kind = cpu_run(prob, F, a, b, cores, out)
             sf += fl
             st += dt
             kinds.add(kind)

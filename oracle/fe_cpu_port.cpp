@@ -319,7 +319,11 @@ int fe_cpu_apply(int form, int dim, int nv, int nd, int vs, int nq, int affine, 
   cut[T_] = end;
   for (int t = 1; t < T_; ++t) cut[t] = std::min(end, std::max(cut[t], cut[t - 1]));
   std::vector<int64_t> lo(T_), hi(T_);
-  std::vector<std::vector<double>> buf(T_);
+  // per-thread window buffers, kept across calls (their pages stay mapped:
+  // a windowed caller is not charged for page faults every call); one
+  // caller at a time
+  static std::vector<std::vector<double>> buf;
+  if ((int)buf.size() < T_) buf.resize(T_);
 #pragma omp parallel num_threads(T_)
   {
     int t = 0;
@@ -335,7 +339,8 @@ int fe_cpu_apply(int form, int dim, int nv, int nd, int vs, int nq, int affine, 
     if (b > a) {
       lo[t] = (int64_t)vs * mn;
       hi[t] = (int64_t)vs * mx + vs;
-      buf[t].assign(hi[t] - lo[t], 0.0);
+      if ((int64_t)buf[t].size() < hi[t] - lo[t]) buf[t].resize(hi[t] - lo[t]);
+      std::fill(buf[t].begin(), buf[t].begin() + (hi[t] - lo[t]), 0.0);
       for (int64_t c = a; c < b; c += W)
         e->fn(T, Mv, c, (int)std::min<int64_t>(W, b - c), buf[t].data(), lo[t]);
     } else {

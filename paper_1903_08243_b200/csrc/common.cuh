@@ -173,6 +173,12 @@ FE_DEVICE double det_adj(const double (&J)[DIM][DIM], double (&A)[DIM][DIM]) {
   }
 }
 
+// Programmatic dependent launch: an overwrite apply zero-fills y with a
+// kernel that lets the operator kernel start early (its prologue gathers and
+// first cells overlap the fill); every operator kernel calls this before its
+// first write to y.  A no-op when the kernel was not launched as a dependent.
+FE_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // y[idx] += v.  The global scatter P_e^T: FP64 RED at L2 (REDG.E.ADD.F64).
 FE_DEVICE void scatter_add(double* y, int64_t idx, double v) { atomicAdd(y + idx, v); }
 

@@ -99,6 +99,7 @@ FE_DEVICE void group_scatter(double* __restrict__ y, const int (&dof)[G][ND], do
             yv[r2][i2] += yv[r][i];
             dup[r][i] = true;
           }
+  griddep_wait();
 #pragma unroll
   for (int r = 0; r < G; ++r)
 #pragma unroll
@@ -451,6 +452,7 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
 #pragma unroll
     for (int i = 0; i < ND; ++i) yl[PAT::at(t, i)] += yt[i];
   }
+  griddep_wait();
 #pragma unroll
   for (int k = 0; k < NU; ++k) scatter_add(p.y, dof[k], yl[k]);
   }
@@ -529,6 +531,7 @@ affine_et_patch_kernel(const __grid_constant__ ETPatchParams<et_nmats<FORM, DIM>
     }
   }
   __syncthreads();
+  griddep_wait();
   for (int k = threadIdx.x; k < nu; k += kPatchCells) {
     const double v = sacc[k];
     if (v != 0.0) scatter_add(p.y, __ldg(p.patch.dofs + off + k), v);

@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256, MINB) dmma_et_kernel(DmmaParams p) {
       }
     }
     // scatter: acc[mt][nt][e] = Y[row = 8 mt + r][cell = base + 8 nt + 2 c4 + e]
+    griddep_wait();
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(BLK, MINB) dmma_modal_kernel(DmmaParams p) {
           dmma884(acc[mt][nt], a, s < NSTEP ? acc1[nt][s / 2][s % 2] : ureg[nt][s - NSTEP]);
       }
     }
+    griddep_wait();
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll

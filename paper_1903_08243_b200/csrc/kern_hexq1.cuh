@@ -163,6 +163,7 @@ hexq1_lap_kernel(const __grid_constant__ TensorParams<2, 2> p) {
       }
     }
   }
+  griddep_wait();
 #pragma unroll
   for (int k = 0; k < 2; ++k)
 #pragma unroll

@@ -136,6 +136,7 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
       for (int i = 0; i < P; ++i) y[j][i] = fma(p.B[b][j], Z0[i], fma(p.D[b][j], Z1[i], y[j][i]));
   }
+  griddep_wait();
 #pragma unroll
   for (int j = 0; j < P; ++j)
 #pragma unroll

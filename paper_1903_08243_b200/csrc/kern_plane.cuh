@@ -342,6 +342,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     }
     if (jt) {
       const int32_t* sM = sM0 + ((it % 3) * TPW + T) * MS;
+      griddep_wait();
 #pragma unroll
       for (int k = 0; k < P; ++k)
 #pragma unroll

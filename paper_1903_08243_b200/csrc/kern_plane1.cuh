@@ -383,6 +383,7 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           for (int i = 0; i < P; ++i) Zb[i][c] = fma(p.D[a][i], w, Zb[i][c]);
         }
       // y[i, j, k] = sum_c B[c][k] Zb[i][c]; scatter
+      griddep_wait();
 #pragma unroll
       for (int k = 0; k < P; ++k)
 #pragma unroll

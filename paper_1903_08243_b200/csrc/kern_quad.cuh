@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(128) quad_kernel(QuadParams p) {
       }
     }
   }
+  griddep_wait();
 #pragma unroll
   for (int j = 0; j < ND; ++j)
 #pragma unroll
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(128) quad_diag_kernel(QuadParams p) {
           for (int b = 0; b < DIM; ++b) acc += s_dphi[(q * ND + i) * DIM + b] * cg[c][b];
         }
       }
+      griddep_wait();
       scatter_add(p.y, (int64_t)VS * dof + c, acc);
     }
   }
@@ -599,6 +601,7 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
         A[j][c] = acc;
       }
   }
+  griddep_wait();
 #pragma unroll
   for (int j = 0; j < ND; ++j)
 #pragma unroll
@@ -706,6 +709,7 @@ quad_vtx_kernel(const __grid_constant__ VtxParams<NQ, ND, DIM, NV> p) {
 #pragma unroll
         for (int b = 0; b < DIM; ++b) S[v][c][b] = fma(p.gphi[q][v], cg[c][b], S[v][c][b]);
   }
+  griddep_wait();
 #pragma unroll
   for (int j = 0; j < ND; ++j)
 #pragma unroll

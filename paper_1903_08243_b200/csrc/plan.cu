@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <vector>
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 
@@ -39,6 +40,34 @@ namespace {
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};  // operator / diagonal kernel launches (fe_launch_count)
 inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Set by fe_apply right after it queued the PDL zero-fill of y (overwrite
+// applies): the NEXT operator launch on this thread is a programmatic
+// dependent of the fill -- its CTAs start while the fill runs, and every
+// operator kernel waits (griddep_wait, common.cuh) before its first write
+// to y.  Later launches of the same apply are ordinary stream launches.
+thread_local bool g_pdl_next = false;
+
+template <typename... KArgs, typename... Args>
+void launch_op(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  if (g_pdl_next) {
+    g_pdl_next = false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  } else {
+    k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+  }
+  note_launch();
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -204,8 +233,7 @@ int quad_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   k.p0 = p->params[0];
   k.p1 = p->params[1];
   int n = end - start;
-  quad_kernel<FORM, DIM, NV, ND, NQ, AFFINE>
-      <<<(n + 127) / 128, 128, p->tables_bytes, s>>>(k); note_launch();
+  launch_op(quad_kernel<FORM, DIM, NV, ND, NQ, AFFINE>, (n + 127) / 128, 128, p->tables_bytes, s, k);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -245,7 +273,7 @@ int quad_diag(const fe_plan* cp, int32_t start, int32_t end, double* y, const do
     k.p0 = p->params[0];
     k.p1 = p->params[1];
     const int n = end - start;
-    quad_diag_kernel<FORM, DIM, NV, ND, NQ, AFFINE><<<(n + 127) / 128, 128, p->diag_tables_bytes, s>>>(k); note_launch();
+    launch_op(quad_diag_kernel<FORM, DIM, NV, ND, NQ, AFFINE>, (n + 127) / 128, 128, p->diag_tables_bytes, s, k);
     CUDA_TRY(cudaGetLastError());
     return FE_OK;
   }
@@ -302,7 +330,7 @@ int qc_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp); note_launch();
+  launch_op(quad_const_kernel<FORM, DIM, NV, ND, NQ, AFF, MINB, UNR>, (n + 127) / 128, 128, 0, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -380,7 +408,7 @@ int vtx_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const do
   hp->p0 = p->params[0];
   hp->p1 = p->params[1];
   const int n = end - start;
-  quad_vtx_kernel<FORM, DIM, NV, ND, NQ, MINB, UNR><<<(n + 127) / 128, 128, 0, s>>>(*hp); note_launch();
+  launch_op(quad_vtx_kernel<FORM, DIM, NV, ND, NQ, MINB, UNR>, (n + 127) / 128, 128, 0, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -471,7 +499,7 @@ int et_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const dou
   int n = end - start;
   constexpr int G = affine_group(DIM, ND);
   const int nt = (n + G - 1) / G;
-  affine_et_kernel<FORM, DIM, ND, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp); note_launch();
+  launch_op(affine_et_kernel<FORM, DIM, ND, G>, (nt + 127) / 128, 128, 0, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -510,7 +538,7 @@ int etp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const do
   hp->end = end;
   const int b0 = start / kPatchCells, b1 = (end - 1) / kPatchCells;
   const size_t smem = 2 * (size_t)p->patch_maxu * sizeof(double);
-  affine_et_patch_kernel<FORM, DIM, ND><<<b1 - b0 + 1, kPatchCells, smem, s>>>(*hp); note_launch();
+  launch_op(affine_et_patch_kernel<FORM, DIM, ND>, b1 - b0 + 1, kPatchCells, smem, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -579,7 +607,7 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
     hp->start = a;
     hp->end = b;
     const int nt = (b - a + G - 1) / G;
-    affine_split_kernel<FORM, DIM, ND, NQS, G><<<(nt + 127) / 128, 128, 0, s>>>(*hp); note_launch();
+    launch_op(affine_split_kernel<FORM, DIM, ND, NQS, G>, (nt + 127) / 128, 128, 0, s, *hp);
   };
   if constexpr (DIM == 3 && (ND == 4 || ND == 10)) {
     using PAT = MacroFor<ND>;
@@ -599,7 +627,7 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 128, 0);
             nb = std::min(nb, std::max(1, waves * sms * per_sm));
           }
-          kfn<<<nb, 128, 0, s>>>(*hp, p->d_macro, p->macro_stride, m0, m1); note_launch();
+          launch_op(kfn, nb, 128, 0, s, *hp, p->d_macro, p->macro_stride, m0, m1);
         };
         if constexpr (ND == 4) {
           if (p->p1_analytic)
@@ -681,7 +709,7 @@ int dmma_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_t s) {
   const int ngroups = (n + 8 * NT - 1) / (8 * NT);
   const int need = (ngroups + kDmmaBlock / 32 - 1) / (kDmmaBlock / 32);
   const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
-  dmma_et_kernel<FORM, DIM, ND, NT, MINB><<<grid, kDmmaBlock, p->tables_bytes, s>>>(k); note_launch();
+  launch_op(dmma_et_kernel<FORM, DIM, ND, NT, MINB>, grid, kDmmaBlock, p->tables_bytes, s, k);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -789,7 +817,7 @@ int dmma_modal_run(const fe_plan* p, const DmmaParams& k, int32_t n, cudaStream_
   const int ngroups = (n + 8 * NT - 1) / (8 * NT);
   const int need = (ngroups + BLK / 32 - 1) / (BLK / 32);
   const int grid = need < p->persistent_ctas ? need : p->persistent_ctas;
-  dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB, BLK><<<grid, BLK, p->tables_bytes, s>>>(k); note_launch();
+  launch_op(dmma_modal_kernel<FORM, DIM, ND, NMODE, NT, MINB, BLK>, grid, BLK, p->tables_bytes, s, k);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -893,7 +921,7 @@ int tensor_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const
   const int cpb = p->cells_per_block;
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
-  tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT><<<grid, tensor_block<MINB>(), p->tables_bytes, s>>>(*hp); note_launch();
+  launch_op(tensor_kernel<FORM, DIM, P, Q, MINB, DIRECT>, grid, tensor_block<MINB>(), p->tables_bytes, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -945,10 +973,9 @@ int plane_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   const int nbatch = (n + cpb - 1) / cpb;
   const int grid = nbatch < p->persistent_ctas ? nbatch : p->persistent_ctas;
   if constexpr (V1)
-    plane1_kernel<P, Q, WARPS, MINB><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
+    launch_op(plane1_kernel<P, Q, WARPS, MINB>, grid, WARPS * 32, p->tables_bytes, s, *hp);
   else
-    plane_kernel<P, Q, WARPS, MINB, CU><<<grid, WARPS * 32, p->tables_bytes, s>>>(*hp);
-  note_launch();
+    launch_op(plane_kernel<P, Q, WARPS, MINB, CU>, grid, WARPS * 32, p->tables_bytes, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -994,10 +1021,10 @@ int hexq1_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   const int n = end - start;
   const unsigned g = (n + 127) / 128;
   switch (p->dmma_cfg) {
-    case 1: hexq1_lap_kernel<1><<<g, 128, 0, s>>>(*hp); note_launch(); break;
-    case 2: hexq1_lap_kernel<2><<<g, 128, 0, s>>>(*hp); note_launch(); break;
-    case 4: hexq1_lap_kernel<4><<<g, 128, 0, s>>>(*hp); note_launch(); break;
-    default: hexq1_lap_kernel<3><<<g, 128, 0, s>>>(*hp); note_launch(); break;
+    case 1: launch_op(hexq1_lap_kernel<1>, g, 128, 0, s, *hp); break;
+    case 2: launch_op(hexq1_lap_kernel<2>, g, 128, 0, s, *hp); break;
+    case 4: launch_op(hexq1_lap_kernel<4>, g, 128, 0, s, *hp); break;
+    default: launch_op(hexq1_lap_kernel<3>, g, 128, 0, s, *hp); break;
   }
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
@@ -1033,7 +1060,7 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   hp->start = start;
   hp->end = end;
   const int64_t nt = 2 * (int64_t)(end - start);
-  pair_kernel<FORM, P, Q, MINB><<<(unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s>>>(*hp); note_launch();
+  launch_op(pair_kernel<FORM, P, Q, MINB>, (unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s, *hp);
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -1216,6 +1243,17 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rm, const int32_t* __
   int64_t c = t / nd;
   int l = (int)(t % nd);
   out[t] = rm[c * nd + perm[l]];
+}
+
+// Zero-fill of y for an overwrite apply; lets the operator kernel launch
+// as soon as every fill CTA is resident (griddepcontrol.launch_dependents).
+__global__ void __launch_bounds__(256) k_zero_pdl(double* __restrict__ y, int64_t n) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  double2* y2 = reinterpret_cast<double2*>(y);
+  const int64_t n2 = n / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+    y2[i] = make_double2(0.0, 0.0);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) y[n - 1] = 0.0;
 }
 
 __global__ void k_add(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
@@ -1745,10 +1783,23 @@ int fe_apply(const fe_plan* p, int32_t start, int32_t end, double* y, const doub
   if (p->form == FE_FORM_NEOHOOKEAN_TANGENT && !c0)
     return fail(FE_EINVAL, "neohookean_tangent needs the state u (coef0)");
   cudaStream_t s = (cudaStream_t)stream;
-  if (apply_flags & FE_APPLY_OVERWRITE)
-    CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)p->vs * p->nglobal * sizeof(double), s));
+  const int64_t ny = (int64_t)p->vs * p->nglobal;
+  if ((apply_flags & FE_APPLY_OVERWRITE) && (end == start || (reinterpret_cast<uintptr_t>(y) & 15) ||
+                                              getenv("FE_NO_PDL"))) {
+    CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)ny * sizeof(double), s));
+  } else if (apply_flags & FE_APPLY_OVERWRITE) {
+    // zero-fill as a kernel the operator launch depends on programmatically:
+    // the operator's prologue (map/u/coordinate gathers, first cells)
+    // overlaps the fill instead of queueing behind it
+    const int64_t blocks = std::min<int64_t>((ny / 2 + 255) / 256, 148 * 4);
+    k_zero_pdl<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, s>>>(y, ny);
+    CUDA_TRY(cudaGetLastError());
+    g_pdl_next = true;
+  }
   if (end == start) return FE_OK;
-  return p->var->launch(p, start, end, y, u, c0, c1, s);
+  const int rc = p->var->launch(p, start, end, y, u, c0, c1, s);
+  g_pdl_next = false;
+  return rc;
 }
 
 int fe_diagonal(const fe_plan* p, int32_t start, int32_t end, double* diag, const double* c0,

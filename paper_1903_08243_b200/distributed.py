@@ -130,6 +130,20 @@ def vertex_first_ids(P, ncells_per_axis, k):
     return np.where(is_vertex, vid, nverts + lin - before)
 
 
+def vertex_first_table(L, k):
+    """``vertex_first_ids`` for every point of a lattice with L[a] points per
+    axis (x fastest), indexed by the lexicographic id: vertex points ranked
+    among vertex points, the others after them ranked among the others."""
+    flags = [np.arange(n) % k == 0 for n in L]
+    isv = flags[-1]
+    for f in flags[-2::-1]:
+        isv = (isv[:, None] & f[None, :]).ravel()
+    cv = np.cumsum(isv, dtype=np.int64)
+    nv = int(cv[-1])
+    lin = np.arange(isv.size, dtype=np.int64)
+    return np.where(isv, cv - 1, nv + lin - cv)
+
+
 def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab:
     """Cell layers [z0, z1) along the slowest axis (z in 3D, y in 2D) of the
     global structured mesh of a config (nx x ny x nz_global cubes, or nx x
@@ -194,34 +208,33 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
     # lexicographic (x fastest, layer axis slowest)
     nper = (nx, ny, nzl) if d == 3 else (nx, nzl)
     L = [k * n + 1 for n in nper]
-    vi = c2v % (nx + 1)
-    if d == 3:
-        vj = (c2v // (nx + 1)) % (ny + 1)
-        vl = c2v // ((nx + 1) * (ny + 1))
-        V = np.stack([vi, vj, vl], axis=-1)
-    else:
-        V = np.stack([vi, c2v // (nx + 1)], axis=-1)
+    strides = np.cumprod([1] + L[:-1])                       # lexicographic lattice strides
     nodes = np.array([[int(round(x * k)) for x in node] for node in spec.element.nodes], dtype=np.int64)
+    # lattice offsets of every local node for each cell type of a cube/square
+    # (a cell = cube origin + type), then broadcast over the cubes
+    cbits = np.array([[(b >> a) & 1 for a in range(d)] for b in range(2 ** d)], dtype=np.int64)
+    Vt = cbits[cells_bits]                                   # [types][nv][d]
     if spec.cell.simplex:
-        P = k * V[:, None, 0, :] + np.einsum("ia,cad->cid", nodes, V[:, 1:, :] - V[:, None, 0, :])
+        off = k * Vt[:, None, 0, :] + np.einsum("ia,tad->tid", nodes, Vt[:, 1:, :] - Vt[:, None, 0, :])
     else:
-        P = k * V[:, None, 0, :] + nodes[None, :, :]
-    dof = vertex_first_ids(P, nper, k)
+        off = k * Vt[:, None, 0, :] + nodes[None, :, :]
+    off_lin = off @ strides                                  # [types][nd]
+    origin = np.stack([i.ravel(), (j.ravel() if d == 3 else l.ravel())] + ([l.ravel()] if d == 3 else []),
+                      axis=1).astype(np.int64)               # cube origins, cell order
+    lin = ((k * origin) @ strides)[:, None, None] + off_lin[None, :, :]
+    lin = lin.reshape(-1, nodes.shape[0])                    # [ncells][nd] lexicographic lattice ids
+    table = vertex_first_table(L, k)
+    dof = table[lin]
     plane = int(np.prod(L[:-1]))
     nlat = plane * L[-1]
     dm = DofMap(np.ascontiguousarray(dof, np.int32), nlat, spec.element)
+    lat = np.empty(nlat, dtype=np.int64)                     # lexicographic id of each dof
+    lat[table] = np.arange(nlat, dtype=np.int64)
     # single-domain (world = 1) id of every slab dof: the same numbering on
-    # the whole mesh, lattice points shifted by k z0 layers
-    Pg = P.copy()
-    Pg[..., -1] += k * z0
-    gid = vertex_first_ids(Pg, tuple(nper[:-1]) + (nz_global,), k)
-    global_index = np.empty(nlat, dtype=np.int64)
-    global_index[dof.ravel()] = gid.ravel()
-    # lattice value arrays (u, state) are drawn per lattice plane; permute
-    # them into the vertex-first numbering
-    lat = np.empty(nlat, dtype=np.int64)                      # lexicographic id of each dof
-    lin = P[..., 0] + L[0] * (P[..., 1] + (L[1] * P[..., 2] if d == 3 else 0))
-    lat[dof.ravel()] = lin.ravel()
+    # the whole mesh; a slab's lattice points are the global ones shifted by
+    # k z0 layers
+    gtable = vertex_first_table(L[:-1] + [k * nz_global + 1], k)
+    global_index = gtable[lat + k * z0 * plane]
     # coefficients per lattice plane (seeded per global plane, so a plane two
     # slabs share gets identical values on both)
     nmax = max(cfg.n[:-1] + (nz_global,))

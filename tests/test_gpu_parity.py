@@ -209,15 +209,19 @@ def test_gpu_on_slab_numbering_with_separate_vertex_map(name):
 
 
 def test_missing_vertex_map_with_non_vertex_numbering_is_rejected():
+    """Without map1 the plan takes map0[:, :nv] as the vertex map; a dof
+    numbering whose vertex columns are not vertex ids must be rejected
+    (out-of-range coordinate index), not read out of bounds."""
     import torch
-    from paper_1903_08243_b200.distributed import build_slab
-    s = build_slab(C.get_config("C2-P2", (3, 2, 2)), 5, 0, 2, 2)
-    h = handle_for(s.spec, s.rule)
+    prob = C.build_problem(C.get_config("C2-P2", (3, 2, 2)), 5)
+    perm = np.random.default_rng(0).permutation(prob.dofmap.ndofs_global)   # vertex dofs not first
+    c2d = perm[np.asarray(prob.dofmap.cell2dof)].astype(np.int32)
+    assert c2d[:, :4].max() >= prob.mesh.nvertices
+    h = handle_for(prob.spec, prob.rule)
     dev = torch.device("cuda")
     with pytest.raises(fe.jit.KernelError, match="out of range"):
-        h.bind(torch.tensor(np.asarray(s.mesh.coords).ravel(), device=dev),
-               torch.tensor(np.asarray(s.dofmap.cell2dof, np.int32).ravel(), device=dev), None,
-               nglobal=s.dofmap.ndofs_global)
+        h.bind(torch.tensor(np.asarray(prob.mesh.coords).ravel(), device=dev),
+               torch.tensor(c2d.ravel(), device=dev), None, nglobal=prob.dofmap.ndofs_global)
 
 
 def test_tangent_needs_the_state():
