@@ -619,6 +619,10 @@ quad_const_kernel(const __grid_constant__ QuadConstParams<NQ, ND, DIM, NV, form_
 // the 10 nodes once per cell.  Exact (not an approximation): lambda_v are the
 // P1 barycentric functions, the same gphi table the geometry uses.
 // ---------------------------------------------------------------------------
+#ifndef FE_VTX_PHYS
+#define FE_VTX_PHYS 1   // hyperelastic forms: physical vertex gradients / moments (0: reference-gradient loop)
+#endif
+
 template <int NQ, int ND, int DIM, int NV>
 struct VtxParams {
   MeshView mesh;
@@ -683,6 +687,114 @@ quad_vtx_kernel(const __grid_constant__ VtxParams<NQ, ND, DIM, NV> p) {
     for (int c = 0; c < VS; ++c)
 #pragma unroll
       for (int b = 0; b < DIM; ++b) S[v][c][b] = 0.0;
+#if FE_VTX_PHYS
+  // physical vertex gradients H_v = G_v J^-1 once per cell (affine: J^-1 is
+  // constant, so grad u(x_q) = sum_v lambda_v(x_q) H_v exactly); the flux is
+  // accumulated as physical vertex moments sum_q lambda_v tw P_q and mapped
+  // by J^-T once per cell.  Per point this drops the two 3x3x3 products
+  // grad_ref -> grad_phys and P -> P J^-T of the reference quadrature loop.
+  if constexpr (FORM == FE_FORM_NEOHOOKEAN || FORM == FE_FORM_NEOHOOKEAN_TANGENT) {
+    static_assert(VS == DIM, "vector form");
+    auto to_phys = [&](double (&Gr)[NV][VS][DIM]) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int c = 0; c < VS; ++c) {
+          double h[DIM];
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) t = fma(Gr[v][c][b], Ji[b][a], t);
+            h[a] = t;
+          }
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) Gr[v][c][a] = h[a];
+        }
+    };
+    to_phys(Gv);
+    if constexpr (STATE) to_phys(G0v);
+    const double mu = p.p0, lam = p.p1;
+#pragma unroll UNR
+    for (int q = 0; q < NQ; ++q) {
+      const double tw = p.qw[q] * absdet;
+      double G[DIM][DIM], F[DIM][DIM], A[DIM][DIM], T[DIM][DIM];
+#pragma unroll
+      for (int c = 0; c < DIM; ++c)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double t = 0.0, t0 = 0.0;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            t = fma(p.gphi[q][v], Gv[v][c][a], t);
+            if constexpr (STATE) t0 = fma(p.gphi[q][v], G0v[v][c][a], t0);
+          }
+          G[c][a] = t;
+          F[c][a] = (STATE ? t0 : t) + (c == a ? 1.0 : 0.0);
+        }
+      const double Jf = det_adj<DIM>(F, A);
+      const double m = tw * mu;
+      if constexpr (FORM == FE_FORM_NEOHOOKEAN) {
+        // P = mu G + mu I + (lambda ln J - mu) F^-T, F^-T[c][a] = A[a][c] / J
+        const double sc = tw * (lam * FE_LOG(Jf) - mu) * recip<true>(Jf);
+#pragma unroll
+        for (int c = 0; c < DIM; ++c)
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) T[c][a] = fma(m, G[c][a], sc * A[a][c]) + (c == a ? m : 0.0);
+      } else {
+        // dP = mu dF + (mu - lambda ln J) F^-T dF^T F^-T + lambda tr(F^-1 dF) F^-T
+        // (pointwise<>, NEOHOOKEAN_TANGENT), dF = G, M = A dF
+        const double r = recip<true>(Jf);
+        double M[DIM][DIM], tr = 0.0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int b = 0; b < DIM; ++b) {
+            double t = 0.0;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) t = fma(A[a][c], G[c][b], t);
+            M[a][b] = t;
+            if (a == b) tr += t;
+          }
+        const double r2 = tw * r * r;
+        const double c2 = (mu - lam * FE_LOG(Jf)) * r2;
+        const double l2 = lam * tr * r2;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c)
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) t = fma(M[a][b], A[b][c], t);
+            T[c][a] = fma(m, G[c][a], fma(c2, t, l2 * A[a][c]));
+          }
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int c = 0; c < DIM; ++c)
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) S[v][c][a] = fma(p.gphi[q][v], T[c][a], S[v][c][a]);
+    }
+    // physical moments -> reference: S_v J^-T
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) {
+        double h[DIM];
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int a = 0; a < DIM; ++a) t = fma(Ji[b][a], S[v][c][a], t);
+          h[b] = t;
+        }
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) S[v][c][b] = h[b];
+      }
+  } else
+#endif
+  {
 #pragma unroll UNR
   for (int q = 0; q < NQ; ++q) {
     const double tw = p.qw[q] * absdet;
@@ -708,6 +820,7 @@ quad_vtx_kernel(const __grid_constant__ VtxParams<NQ, ND, DIM, NV> p) {
       for (int c = 0; c < VS; ++c)
 #pragma unroll
         for (int b = 0; b < DIM; ++b) S[v][c][b] = fma(p.gphi[q][v], cg[c][b], S[v][c][b]);
+  }
   }
   griddep_wait();
 #pragma unroll

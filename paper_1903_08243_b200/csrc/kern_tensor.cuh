@@ -138,8 +138,7 @@ struct TensorLayout {
   static constexpr int X = O2 + R2;
   static constexpr int MU = X + NV * DIM;
   static constexpr int LAM = MU + NV;
-  static constexpr int MAPI = LAM + NV;                  // the cell's dof ids (int32, ND of them)
-  static constexpr int raw = MAPI + (ND + 1) / 2;
+  static constexpr int raw = LAM + NV;
   static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
@@ -178,7 +177,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
   // ---- prefetch pipeline: map indices two batches ahead, data one ahead ----
   constexpr int RX = L::RX, RM = L::RM;
-  int pf_map[RU], pf_mapd[RU];   // map of the batch two ahead / of the data in flight
+  int pf_map[RU];
   double pf_u[RU][VS];
   double pf_x[RX], pf_m[RM], pf_l[RM];
   auto cell_of = [&](int batch) { return p.start + batch * CPB + team; };
@@ -195,12 +194,10 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     const int c = cell_of(batch);
     const bool ok = in_team && batch < nbatch && c < p.end;
 #pragma unroll
-    for (int r = 0; r < RU; ++r) {
-      pf_mapd[r] = pf_map[r];
+    for (int r = 0; r < RU; ++r)
 #pragma unroll
       for (int k = 0; k < VS; ++k)
         pf_u[r][k] = pf_map[r] >= 0 ? __ldg(p.u + (int64_t)VS * pf_map[r] + k) : 0.0;
-    }
 #pragma unroll
     for (int r = 0; r < RX; ++r) {
       const int e = t + r * TS;
@@ -223,17 +220,14 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       }
     }
   };
-  int32_t* sMap = reinterpret_cast<int32_t*>(sm + L::MAPI);
   auto park = [&]() {  // prefetched registers -> this team's shared memory
     if (!in_team) return;
 #pragma unroll
     for (int r = 0; r < RU; ++r) {
       const int idx = t + r * TS;
-      if (idx < ND) {
+      if (idx < ND)
 #pragma unroll
         for (int k = 0; k < VS; ++k) sU[k * ND + idx] = pf_u[r][k];
-        sMap[idx] = pf_mapd[r];  // kept for the scatter: no dependent global load there
-      }
     }
 #pragma unroll
     for (int r = 0; r < RX; ++r)
@@ -516,6 +510,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
     // ---- transposed chain and scatter, one component at a time ------------
     griddep_wait();   // y zero-filled by the preceding kernel (PDL overwrite path)
+    const int32_t* mrow = p.maplex + (int64_t)cell * ND;
 #pragma unroll
     for (int comp = 0; comp < VS; ++comp) {
       if constexpr (DIM == 3) {
@@ -578,7 +573,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               double s = 0.0;
 #pragma unroll
               for (int c = 0; c < Q; ++c) s = fma(p.B[c][k], w1[c], s);
-              scatter_add(p.y, (int64_t)VS * sMap[k * P * P + t] + comp, s);
+              scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
             }
           }
           team_sync();
@@ -641,7 +636,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
                 s = fma(p.B[c][k], w1[c], s);
                 s = fma(p.D[c][k], w2[c], s);
               }
-              scatter_add(p.y, (int64_t)VS * sMap[k * P * P + t] + comp, s);
+              scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
             }
           }
           team_sync();
@@ -678,7 +673,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               s = fma(p.B[b][j], a0[b], s);
               s = fma(p.D[b][j], a1[b], s);
             }
-            scatter_add(p.y, (int64_t)VS * sMap[j * P + i] + comp, s);
+            scatter_add(p.y, (int64_t)VS * __ldg(mrow + j * P + i) + comp, s);
           }
         }
         team_sync();
