@@ -407,7 +407,7 @@ FE_DEVICE void p1_simplex_compute(const double (&X)[DIM + 1][DIM], const double 
 }
 
 #ifndef FE_MACRO_MINB
-#define FE_MACRO_MINB 1
+#define FE_MACRO_MINB 3   // 165 registers, no spill: C2-P1 21.5 -> 19.4 us (profiles/r02/ab_macro_minb.txt)
 #endif
 template <int FORM, int DIM, int ND, int NQS, class PAT, bool ANALYTIC = false>
 __global__ void __launch_bounds__(128, FE_MACRO_MINB)

@@ -1103,7 +1103,7 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define FE_VTX_MINB 1
 #endif
 #ifndef FE_VTX_UNR
-#define FE_VTX_UNR 2   // measured with the fast log: C5 5.62 ms at 1, 5.17 at 2, 5.34 at 3 (profiles/r01/sweep_c5unr.txt)
+#define FE_VTX_UNR 3   // physical-gradient kernel: C5 5.29 ms at 1 and 2, 5.11 at 3 (profiles/r02/vtx_variants.log)
 #endif
 #ifndef FE_VTX_TUNR
 #define FE_VTX_TUNR 1

@@ -14,6 +14,11 @@ caller side of the hot path -- the reference has no solver at all).
   weighted 0 and the local sums are all-reduced over NCCL (gloo on CPU).
 * :func:`jacobi` -- inverse operator diagonal (``GpuKernelHandle.diagonal``,
   fe_diagonal), interface entries summed across ranks like the action.
+* :func:`newton` -- Newton's method for the hyperelastic residual
+  F(u) = 0 (``neohookean``, C5) with Dirichlet constraints: every step is
+  one residual apply and a CG solve with the tangent action K(u)
+  (``neohookean_tangent``, C6) -- the caller side the two
+  operators exist for.
 
 Symmetric positive definite forms: mass, Helmholtz, Lame elasticity (with
 constraints), the neo-Hookean tangent near a stable state.
@@ -23,7 +28,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-__all__ = ["cg", "CGInfo", "SlabDot", "jacobi"]
+__all__ = ["cg", "CGInfo", "SlabDot", "jacobi", "newton", "NewtonInfo"]
 
 
 @dataclass
@@ -116,3 +121,62 @@ def jacobi(diag, op=None):
     if op is not None and op.world > 1:
         op.exchange(diag)
     return 1.0 / diag
+
+
+@dataclass
+class NewtonInfo:
+    iterations: int = 0
+    converged: bool = False
+    residuals: list = field(default_factory=list)     # ||F(u)|| (free dofs) after each step, [0] initial
+    cg_iterations: list = field(default_factory=list)
+
+
+def newton(residual, tangent, u, free=None, rtol=1e-10, atol=0.0, maxiter=20, cg_rtol=1e-12,
+           cg_maxiter=2000, precond=None, dot=None):
+    """Solve F(u) = 0 on the free dofs, Dirichlet values kept where
+    ``free`` == 0 (a 0/1 tensor like u; None: all free).
+
+    ``residual(u, r)`` overwrites r with F(u); ``tangent(u)`` returns the
+    action ``apply(du, y)`` of K(u) = dF/du (overwrite).  Each step solves
+    the constrained system  [free K free + (1 - free)] du = -free F(u)  by
+    CG (symmetric: K is, near a stable state) and updates u in place.
+    ``precond(u)`` may return a CG preconditioner for K(u) (e.g. Jacobi from
+    fe_diagonal at the state).  Returns (u, NewtonInfo)."""
+    import torch
+    dot = dot or _local_dot
+    one = None if free is None else (1.0 - free)
+    r = torch.empty_like(u)
+    info = NewtonInfo()
+
+    def res_norm():
+        residual(u, r)
+        if free is not None:
+            r.mul_(free)
+        return float(torch.sqrt(dot(r, r)))
+
+    r0 = res_norm()
+    info.residuals.append(r0)
+    tol = max(atol, rtol * r0)
+    if r0 <= tol:
+        info.converged = True
+        return u, info
+    for it in range(1, maxiter + 1):
+        K = tangent(u)
+        if free is None:
+            A = K
+        else:
+            def A(x, y, K=K):
+                K(x * free, y)
+                y.mul_(free).add_(one * x)
+        rhs = -r
+        du, ci = cg(A, rhs, rtol=cg_rtol, maxiter=cg_maxiter,
+                    precond=None if precond is None else precond(u), dot=dot)
+        info.cg_iterations.append(ci.iterations)
+        u.add_(du)
+        rn = res_norm()
+        info.residuals.append(rn)
+        info.iterations = it
+        if rn <= tol:
+            info.converged = True
+            break
+    return u, info

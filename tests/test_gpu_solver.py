@@ -75,3 +75,33 @@ def test_cg_recovers_manufactured_solution(name, n, precond):
     x, info = cg(A, b, rtol=1e-12, maxiter=2000, precond=M)
     assert info.converged, info.residuals[-3:]
     assert float((x - u).abs().max()) <= 1e-7 * float(u.abs().max())
+
+
+@pytest.mark.parametrize("n", [2, 8])
+def test_gpu_newton_neohookean_residual_and_tangent(n):
+    """Newton on the B200: the C5 residual kernel and the C6 tangent kernel
+    inside solver.newton (CG per step), Dirichlet data u = A x on the cube
+    boundary -> the exact homogeneous deformation at every node."""
+    import torch
+    from paper_1903_08243_b200.solver import newton
+    from test_solver import newton_problem
+    s, exact, free = newton_problem(n)
+    dev = torch.device("cuda")
+    hr = fe.compile_and_load(fe.emit_for(fe.operator_spec("neohookean", "tetrahedron", 2), fe.Target(), s.rule))
+    ht = fe.compile_and_load(fe.emit_for(fe.operator_spec("neohookean_tangent", "tetrahedron", 2), fe.Target(),
+                                         s.rule))
+    mesh = (torch.tensor(np.asarray(s.mesh.coords).ravel(), device=dev),
+            torch.tensor(np.asarray(s.dofmap.cell2dof, np.int32).ravel(), device=dev),
+            torch.tensor(np.asarray(s.mesh.cell2vert, np.int32).ravel(), device=dev))
+    for h in (hr, ht):
+        h.bind(*mesh, nglobal=s.dofmap.ndofs_global)
+    residual = lambda u, r: hr.apply(u, r, overwrite=True)
+    tangent = lambda u0: (lambda du, y: ht.apply(du, y, coef=(u0, None), overwrite=True))
+    fr = torch.tensor(free, device=dev)
+    u = torch.tensor(exact * (1.0 - free), device=dev)
+    u, info = newton(residual, tangent, u, free=fr, rtol=1e-12, maxiter=10, cg_rtol=1e-13)
+    assert info.converged, info.residuals
+    assert info.iterations <= 8
+    rel = np.array(info.residuals) / info.residuals[0]
+    assert rel[-1] <= 1e-12 and rel[-2] <= 1e-5          # quadratic tail
+    assert float((u.cpu() - torch.tensor(exact)).abs().max()) <= 1e-11

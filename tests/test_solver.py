@@ -91,3 +91,53 @@ def test_distributed_cg_equals_single_domain(name):
     for rank, its, conv, err in res:
         assert conv and err < 1e-8, (rank, err)
         assert abs(its - info1.iterations) <= 1, (its, info1.iterations)   # same Krylov sequence
+
+
+def _node_coords(slab):
+    """Physical position of every scalar dof (affine simplices: the nodes'
+    reference coordinates mapped by each cell's vertices)."""
+    X = slab.mesh.coords[slab.mesh.cell2vert]                       # [c][4][3]
+    ref = np.array(slab.spec.element.nodes, float)                   # [nd][3]
+    pts = X[:, None, 0, :] + np.einsum("ia,cad->cid", ref, X[:, 1:, :] - X[:, None, 0, :])
+    out = np.empty((slab.dofmap.ndofs_global, 3))
+    out[np.asarray(slab.dofmap.cell2dof).ravel()] = pts.reshape(-1, 3)
+    return out
+
+
+def newton_problem(n=2):
+    """Neo-Hookean P2 on the C5 mesh family, Dirichlet data u = A x on the
+    cube's boundary: the homogeneous deformation x -> (I + A) x is an exact
+    equilibrium (no body force) and P2 interpolates it exactly, so Newton
+    must land on u = A x at every node."""
+    cfg = C.get_config("C5", (n, n, n))
+    s = build_slab(cfg, 0, 0, n, n)
+    xyz = _node_coords(s)
+    A = np.array([[0.02, -0.01, 0.005], [0.01, 0.03, -0.02], [-0.015, 0.0, 0.01]])
+    exact = (xyz @ A.T).ravel()
+    on_bnd = np.any((np.abs(xyz) < 1e-12) | (np.abs(xyz - 1.0) < 1e-12), axis=1)
+    free = np.repeat(~on_bnd, 3).astype(float)
+    return s, exact, free
+
+
+def test_newton_recovers_homogeneous_deformation():
+    from paper_1903_08243_b200.solver import newton
+    s, exact, free = newton_problem(2)
+    Pr = fo.Problem("neohookean", "tetrahedron", 2, 4)
+    Pt = fo.Problem("neohookean_tangent", "tetrahedron", 2, 4)
+    geo = (s.mesh.coords, s.mesh.cell2vert, s.dofmap.cell2dof)
+
+    def residual(u, r):
+        r.copy_(torch.from_numpy(fo.assemble(Pr, *geo, u.numpy())))
+
+    def tangent(u0):
+        st = u0.numpy().copy()
+        return lambda du, y: y.copy_(torch.from_numpy(fo.assemble(Pt, *geo, du.numpy(), state=st)))
+
+    u = torch.from_numpy(exact * (1.0 - free))          # boundary data, interior 0
+    u, info = newton(residual, tangent, u, free=torch.from_numpy(free), rtol=1e-13, maxiter=8)
+    assert info.converged, info.residuals
+    assert info.iterations <= 5
+    # quadratic convergence: each step squares the (relative) residual
+    rel = np.array(info.residuals) / info.residuals[0]
+    assert rel[2] <= 10 * rel[1] ** 2 + 1e-14
+    assert np.abs(u.numpy() - exact).max() <= 1e-12
