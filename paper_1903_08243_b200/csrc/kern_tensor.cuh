@@ -145,10 +145,14 @@ struct TensorLayout {
 // MINB: CTAs per SM the register allocation must allow, chosen per variant
 // from measurements (profiles/r01/sweep_minb2.jsonl): 1 or 2 with 256-thread
 // CTAs, 3 with 128-thread CTAs (<= 170 registers, 12 warps per SM)
-template <int MINB> constexpr int tensor_block() { return MINB >= 3 ? 128 : 256; }
+// MINB >= 100 encodes a CTA size of MINB threads at 2 CTAs per SM (e.g.
+// 192: 5 teams of 36 at Q = 6 with a 170-register budget instead of 7 teams
+// and 128 registers + spills)
+template <int MINB> constexpr int tensor_block() { return MINB >= 100 ? MINB : (MINB >= 3 ? 128 : 256); }
+template <int MINB> constexpr int tensor_minb() { return MINB >= 100 ? 2 : MINB; }
 
 template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
-__global__ void __launch_bounds__(tensor_block<MINB>(), MINB)
+__global__ void __launch_bounds__(tensor_block<MINB>(), tensor_minb<MINB>())
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);
@@ -687,19 +691,28 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
 }  // namespace fe
 
+#ifndef FE_TK_Q5_MINB
+#define FE_TK_Q5_MINB 2
+#endif
+#ifndef FE_TK_Q6_MINB
+#define FE_TK_Q6_MINB 2
+#endif
+#ifndef FE_TK_EQ2_MINB
+#define FE_TK_EQ2_MINB 192   // 192-thread CTAs, 168 registers: C4-hex-Q2 0.504 -> 0.466 ms (profiles/r02/ab_tensor_blocks.txt)
+#endif
 // registry hook (plan.cu): TV(form, cell, dim, degree, P, Q, MINB[, DIRECT])
 #define FE_TENSOR_VARIANTS                                                                   \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 2, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 3, 2),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 4, 2),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 2),                             \
-  TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, 2),                            \
-  TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, 2),                            \
+  TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, FE_TK_Q5_MINB),                \
+  TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, FE_TK_Q6_MINB),                \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                             \
   TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 2),                              \
-  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 2),                              \
+  TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, FE_TK_EQ2_MINB),                 \
   TV(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                              \
   TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                                   \
   TV(FE_FORM_NEOHOOKEAN, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                                   \
