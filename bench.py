@@ -423,7 +423,7 @@ def run_e2e_host_api(ops, steps):
     # full-duplex PCIe link -- the reference's "concurrent calls on disjoint
     # dat0"
     from concurrent.futures import ThreadPoolExecutor
-    nthr = int(os.environ.get("FE_E2E_THREADS", "4"))
+    nthr = int(os.environ.get("FE_E2E_THREADS", "8"))
     pool = ThreadPoolExecutor(nthr) if nthr > 1 else None
 
     def call(ob):

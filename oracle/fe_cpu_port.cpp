@@ -20,8 +20,9 @@
  *    scatter-add stay per lane and sequential within a batch
  *    (transforms.py:428,483); peeled remainder cells run as a masked batch;
  *  - threads (SURVEY.md 8d CPU-baseline protocol): contiguous cell chunks,
- *    each scattering into a private window [lo, hi] of y (the dofs its cells
- *    touch), windows then summed into y in parallel over dof ranges.
+ *    each scattering into two private windows of y (the dofs its cells'
+ *    vertex columns touch, and the others'), windows then summed into y in
+ *    parallel over dof ranges.
  *
  * Numerically it is the oracle's algorithm (oracle/fe_oracle.c) in a
  * different order; tests/test_cpu_port.py pins it to the oracle at 1e-13.
@@ -101,7 +102,8 @@ inline vd det_inv(const vd (&J)[D][D], vd (&Ji)[D][D]) {
 /* One batch of W cells [c, c + n), n <= W (lanes >= n replicate cell c and
  * are not scattered). */
 template <int FORM, int D, int NV, int ND, int VS, int NQ, bool AFF>
-void batch(const Tables& T, const Mesh& M, int64_t c, int n, double* ybuf, int64_t lo) {
+void batch(const Tables& T, const Mesh& M, int64_t c, int n, double* ybv, int64_t lov, double* ybr,
+           int64_t lor) {
   constexpr bool VALS = FORM == MASS || FORM == HELMHOLTZ;
   constexpr bool GRADS = FORM != MASS;
   constexpr bool STATE = FORM == NEOHOOKEAN_TANGENT;
@@ -236,15 +238,18 @@ void batch(const Tables& T, const Mesh& M, int64_t c, int n, double* ybuf, int64
         A[j][k] += acc;
       }
   }
-  // scatter-add P^T (sequential over lanes, as the reference)
+  // scatter-add P^T (sequential over lanes, as the reference) into the
+  // thread's two windows: vertex columns (j < NV) and the others
   for (int l = 0; l < n; ++l) {
     const int32_t* dm = M.map0 + cell[l] * ND;
-    for (int j = 0; j < ND; ++j)
-      for (int k = 0; k < VS; ++k) ybuf[(int64_t)VS * dm[j] + k - lo] += A[j][k][l];
+    for (int j = 0; j < ND; ++j) {
+      double* yb = j < NV ? ybv - lov : ybr - lor;
+      for (int k = 0; k < VS; ++k) yb[(int64_t)VS * dm[j] + k] += A[j][k][l];
+    }
   }
 }
 
-typedef void (*BatchFn)(const Tables&, const Mesh&, int64_t, int, double*, int64_t);
+typedef void (*BatchFn)(const Tables&, const Mesh&, int64_t, int, double*, int64_t, double*, int64_t);
 
 struct Entry {
   int form, dim, nv, nd, vs, nq;
@@ -318,12 +323,14 @@ int fe_cpu_apply(int form, int dim, int nv, int nd, int vs, int nq, int affine, 
   cut[0] = start;
   cut[T_] = end;
   for (int t = 1; t < T_; ++t) cut[t] = std::min(end, std::max(cut[t], cut[t - 1]));
-  std::vector<int64_t> lo(T_), hi(T_);
-  // per-thread window buffers, kept across calls (their pages stay mapped:
-  // a windowed caller is not charged for page faults every call); one
-  // caller at a time
+  // per thread TWO windows of y: the dofs of its cells' vertex columns
+  // (j < nv) and of the other columns -- with the vertex dofs numbered first
+  // (the reference's convention, mesh.py:95) the two bands are far apart in
+  // y and one window would span it all.  Window buffers are kept across
+  // calls (their pages stay mapped); one caller at a time.
+  std::vector<int64_t> lo(2 * T_), hi(2 * T_);
   static std::vector<std::vector<double>> buf;
-  if ((int)buf.size() < T_) buf.resize(T_);
+  if ((int)buf.size() < 2 * T_) buf.resize(2 * T_);
 #pragma omp parallel num_threads(T_)
   {
     int t = 0;
@@ -331,31 +338,38 @@ int fe_cpu_apply(int form, int dim, int nv, int nd, int vs, int nq, int affine, 
     t = omp_get_thread_num();
 #endif
     int64_t a = cut[t], b = cut[t + 1];
-    int32_t mn = INT32_MAX, mx = -1;
-    for (int64_t i = a * nd; i < b * nd; ++i) {
-      mn = std::min(mn, map0[i]);
-      mx = std::max(mx, map0[i]);
+    int32_t mn[2] = {INT32_MAX, INT32_MAX}, mx[2] = {-1, -1};
+    for (int64_t c = a; c < b; ++c)
+      for (int j = 0; j < nd; ++j) {
+        const int w = j < nv ? 0 : 1;
+        const int32_t d = map0[c * nd + j];
+        mn[w] = std::min(mn[w], d);
+        mx[w] = std::max(mx[w], d);
+      }
+    for (int w = 0; w < 2; ++w) {
+      const int i = 2 * t + w;
+      if (mx[w] >= 0) {
+        lo[i] = (int64_t)vs * mn[w];
+        hi[i] = (int64_t)vs * mx[w] + vs;
+      } else {
+        lo[i] = hi[i] = 0;
+      }
+      if ((int64_t)buf[i].size() < std::max<int64_t>(1, hi[i] - lo[i])) buf[i].resize(std::max<int64_t>(1, hi[i] - lo[i]));
+      std::fill(buf[i].begin(), buf[i].begin() + (hi[i] - lo[i]), 0.0);
     }
-    if (b > a) {
-      lo[t] = (int64_t)vs * mn;
-      hi[t] = (int64_t)vs * mx + vs;
-      if ((int64_t)buf[t].size() < hi[t] - lo[t]) buf[t].resize(hi[t] - lo[t]);
-      std::fill(buf[t].begin(), buf[t].begin() + (hi[t] - lo[t]), 0.0);
-      for (int64_t c = a; c < b; c += W)
-        e->fn(T, Mv, c, (int)std::min<int64_t>(W, b - c), buf[t].data(), lo[t]);
-    } else {
-      lo[t] = hi[t] = 0;
-    }
+    for (int64_t c = a; c < b; c += W)
+      e->fn(T, Mv, c, (int)std::min<int64_t>(W, b - c), buf[2 * t].data(), lo[2 * t], buf[2 * t + 1].data(),
+            lo[2 * t + 1]);
   }
   // windows -> y, in parallel over dof ranges
   const int R = std::max(1, nthreads);
 #pragma omp parallel for num_threads(R) schedule(static)
   for (int r = 0; r < R; ++r) {
     const int64_t r0 = ny * r / R, r1 = ny * (r + 1) / R;
-    for (int t = 0; t < T_; ++t) {
-      const int64_t a = std::max(r0, lo[t]), b = std::min(r1, hi[t]);
-      const double* s = buf[t].data() - lo[t];
-      for (int64_t i = a; i < b; ++i) y[i] += s[i];
+    for (int i = 0; i < 2 * T_; ++i) {
+      const int64_t a = std::max(r0, lo[i]), b = std::min(r1, hi[i]);
+      const double* s = buf[i].data() - lo[i];
+      for (int64_t k = a; k < b; ++k) y[k] += s[k];
     }
   }
   return 0;

@@ -97,6 +97,10 @@ constexpr int pick_inner(int lo, int nr, int ns, int rstep) {
 }
 constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
 
+#ifndef FE_TK_ASYNC
+#define FE_TK_ASYNC 0   // 1: cp.async gather pipeline (no prefetch registers)
+#endif
+
 // DIRECT: use the direct algorithm even when p == q (measured faster at
 // Q5/Q6, where the collocation stages' cross-pencil Dc reads, 2 q^4 shared
 // loads per component, outweigh its 25% flop saving)
@@ -138,7 +142,17 @@ struct TensorLayout {
   static constexpr int X = O2 + R2;
   static constexpr int MU = X + NV * DIM;
   static constexpr int LAM = MU + NV;
-  static constexpr int raw = LAM + NV;
+  // FE_TK_ASYNC: second data buffer (u, coordinates, mu/lambda) and two
+  // map-row buffers (ND dof ids + NV vertex ids, int32) for the cp.async
+  // gather pipeline
+  static constexpr int MBW = (ND + NV + 1) / 2;            // map buffer width in doubles
+  static constexpr int UA = LAM + NV;
+  static constexpr int XA = UA + VS * ND;
+  static constexpr int MUA = XA + NV * DIM;
+  static constexpr int LAMA = MUA + NV;
+  static constexpr int MB0 = LAMA + NV;
+  static constexpr int MB1 = MB0 + MBW;
+  static constexpr int raw = FE_TK_ASYNC ? MB1 + MBW : LAM + NV;
   static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
@@ -171,10 +185,12 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     else __syncthreads();
   };
   double* sm = smem_all + (in_team ? team : 0) * L::size;
-  double* sU = sm + L::U;
+  double* sU = sm + L::U;              // the data buffers of the batch being computed
   double* s1 = sm + L::O1;
   double* s2 = sm + L::O2;
   double* sX = sm + L::X;
+  double* sMU = sm + L::MU;
+  double* sLAM = sm + L::LAM;
   const int64_t cs = p.mesh.nc_stride;
   const int ncell = p.end - p.start;
   const int nbatch = (ncell + CPB - 1) / CPB;
@@ -240,25 +256,107 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
       for (int r = 0; r < RM; ++r)
         if (t + r * TS < NV) {
-          sm[L::MU + t + r * TS] = pf_m[r];
-          sm[L::LAM + t + r * TS] = pf_l[r];
+          sMU[t + r * TS] = pf_m[r];
+          sLAM[t + r * TS] = pf_l[r];
         }
     }
   };
 
-  int batch = blockIdx.x;
-  load_map(batch);
-  load_data(batch);
-  park();
-  load_map(batch + gridDim.x);
-  team_sync();
+  // ---- FE_TK_ASYNC: the same pipeline through cp.async (LDGSTS) straight
+  // into shared memory -- map rows + vertex ids two batches ahead, u /
+  // coordinates / mu, lambda one ahead, double-buffered -- so no prefetched
+  // value occupies a register during the compute
+  int32_t* const mbuf0 = reinterpret_cast<int32_t*>(sm + L::MB0);
+  int32_t* const mbuf1 = reinterpret_cast<int32_t*>(sm + L::MB1);
+  auto issue_maps = [&](int batch, int32_t* mb) {
+    if (!in_team) return;
+    const int c = cell_of(batch);
+    const bool ok = batch < nbatch && c < p.end;
+    for (int idx = t; idx < ND + NV; idx += TS) {
+      if (!ok) mb[idx] = -1;
+      else if (idx < ND) cp_async4(mb + idx, p.maplex + (int64_t)c * ND + idx);
+      else cp_async4(mb + idx, p.mesh.vmap + (idx - ND) * cs + c);
+    }
+  };
+  auto issue_data = [&](const int32_t* mb, int par) {
+    if (!in_team) return;
+    double* du = sm + (par ? L::UA : L::U);
+    double* dx = sm + (par ? L::XA : L::X);
+#pragma unroll
+    for (int r = 0; r < RU; ++r) {
+      const int idx = t + r * TS;
+      if (idx < ND) {
+        const int m = mb[idx];
+#pragma unroll
+        for (int k = 0; k < VS; ++k) cp_async8_zfill(du + k * ND + idx, p.u + (m >= 0 ? (int64_t)VS * m + k : 0), m >= 0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RX; ++r) {
+      const int e = t + r * TS;
+      if (e < NV * DIM) {
+        const int vid = mb[ND + e / DIM];
+        cp_async8_zfill(dx + e, p.mesh.coords + (vid >= 0 ? (int64_t)vid * CStride<DIM>::value + e % DIM : 0), vid >= 0);
+      }
+    }
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+      double* dm = sm + (par ? L::MUA : L::MU);
+      double* dl = sm + (par ? L::LAMA : L::LAM);
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const int v = t + r * TS;
+        if (v < NV) {
+          const int vid = mb[ND + v];
+          cp_async8_zfill(dm + v, p.mu + (vid >= 0 ? vid : 0), vid >= 0);
+          cp_async8_zfill(dl + v, p.lam + (vid >= 0 ? vid : 0), vid >= 0);
+        }
+      }
+    }
+  };
+  auto select_buffers = [&](int par) {
+    sU = sm + (par ? L::UA : L::U);
+    sX = sm + (par ? L::XA : L::X);
+    sMU = sm + (par ? L::MUA : L::MU);
+    sLAM = sm + (par ? L::LAMA : L::LAM);
+  };
 
-  for (; batch < nbatch; batch += gridDim.x) {
+  int batch = blockIdx.x;
+  if constexpr (FE_TK_ASYNC) {
+    issue_maps(batch, mbuf0);
+    cp_commit();
+    cp_wait_group<0>();
+    team_sync();
+    issue_data(mbuf0, 0);
+    cp_commit();
+    issue_maps(batch + gridDim.x, mbuf1);
+    cp_commit();
+    cp_wait_group<1>();                  // data of the first batch
+    team_sync();
+  } else {
+    load_map(batch);
+    load_data(batch);
+    park();
+    load_map(batch + gridDim.x);
+    team_sync();
+  }
+
+  for (int it = 0; batch < nbatch; batch += gridDim.x, ++it) {
     const int cell = cell_of(batch);
     const bool active = in_team && cell < p.end;
-    // issue the next batch's gathers now; they land while this batch computes
-    load_data(batch + gridDim.x);
-    load_map(batch + 2 * gridDim.x);
+    if constexpr (FE_TK_ASYNC) {
+      cp_wait_group<0>();                // map rows of the next batch
+      team_sync();
+      const int par = it & 1;
+      select_buffers(par);
+      issue_data(par ? mbuf0 : mbuf1, par ^ 1);   // next batch's data, other buffer
+      cp_commit();
+      issue_maps(batch + 2 * gridDim.x, par ? mbuf1 : mbuf0);
+      cp_commit();
+    } else {
+      // issue the next batch's gathers now; they land while this batch computes
+      load_data(batch + gridDim.x);
+      load_map(batch + 2 * gridDim.x);
+    }
 
     // ---- forward: reference gradients at the points of this thread's x-pencil
     double g[VS][DIM][Q];
@@ -466,8 +564,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         for (int v = 0; v < NV; ++v) {
           const int vx = v & 1, vy = (v >> 1) & 1, vz = v >> 2;
           const double wgt = DIM == 3 ? Ly[vy] * Lz[vz] : Ly[vy];
-          mx[vx] += wgt * sm[L::MU + v];
-          lx[vx] += wgt * sm[L::LAM + v];
+          mx[vx] += wgt * sMU[v];
+          lx[vx] += wgt * sLAM[v];
         }
         m0 = mx[0]; dm = mx[1] - mx[0];
         l0 = lx[0]; dl = lx[1] - lx[0];
@@ -684,7 +782,11 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       }
     }
     // the next batch's data (loads issued at the top of this iteration)
-    park();
+    if constexpr (FE_TK_ASYNC) {
+      cp_wait_group<1>();
+    } else {
+      park();
+    }
     team_sync();
   }
 }
