@@ -104,7 +104,7 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 // DIRECT: use the direct algorithm even when p == q (measured faster at
 // Q5/Q6, where the collocation stages' cross-pencil Dc reads, 2 q^4 shared
 // loads per component, outweigh its 25% flop saving)
-template <int DIM, int P, int Q, int VS, bool DIRECT = false, int BLOCK_ = 256>
+template <int DIM, int P, int Q, int VS, bool DIRECT = false, int BLOCK_ = 256, bool ASYNC = false>
 struct TensorLayout {
   static constexpr int BLOCK = BLOCK_;                       // threads per CTA
   static constexpr int TS = DIM == 3 ? Q * Q : Q;          // threads per cell (team)
@@ -152,7 +152,7 @@ struct TensorLayout {
   static constexpr int LAMA = MUA + NV;
   static constexpr int MB0 = LAMA + NV;
   static constexpr int MB1 = MB0 + MBW;
-  static constexpr int raw = FE_TK_ASYNC ? MB1 + MBW : LAM + NV;
+  static constexpr int raw = ASYNC ? MB1 + MBW : LAM + NV;
   static constexpr int size = raw + ((TS - raw) % 16 + 16) % 16;  // team stride == TS (mod 16)
 };
 
@@ -162,15 +162,23 @@ struct TensorLayout {
 // MINB >= 100 encodes a CTA size of MINB threads at 2 CTAs per SM (e.g.
 // 192: 5 teams of 36 at Q = 6 with a 170-register budget instead of 7 teams
 // and 128 registers + spills)
-template <int MINB> constexpr int tensor_block() { return MINB >= 100 ? MINB : (MINB >= 3 ? 128 : 256); }
-template <int MINB> constexpr int tensor_minb() { return MINB >= 100 ? 2 : MINB; }
+// MINB >= 1000: the same with the cp.async gather pipeline (FE_TK_ASYNC
+// per variant: C3-Q5 0.38 -> 0.45 of its roof; slower where its extra
+// shared memory costs occupancy, profiles/r02/ab_tensor_async.txt)
+template <int MINB> constexpr bool tensor_async() { return MINB >= 1000 || FE_TK_ASYNC; }
+template <int MINB> constexpr int tensor_block() {
+  constexpr int m = MINB % 1000;
+  return m >= 100 ? m : (m >= 3 ? 128 : 256);
+}
+template <int MINB> constexpr int tensor_minb() { return MINB % 1000 >= 100 ? 2 : MINB % 1000; }
 
 template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(tensor_block<MINB>(), tensor_minb<MINB>())
 tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   static_assert(Q >= P, "team layout assumes Q >= P");
   constexpr int VS = form_vs(FORM, DIM);
-  using L = TensorLayout<DIM, P, Q, VS, DIRECT, tensor_block<MINB>()>;
+  constexpr bool ASYNC = tensor_async<MINB>();
+  using L = TensorLayout<DIM, P, Q, VS, DIRECT, tensor_block<MINB>(), ASYNC>;
   constexpr int TS = L::TS, CPB = L::CPB, ND = L::ND, NV = L::NV, RU = L::RU;
   constexpr bool COLLOC = L::COLLOC;
   constexpr int QQ = Q * Q;
@@ -321,7 +329,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   };
 
   int batch = blockIdx.x;
-  if constexpr (FE_TK_ASYNC) {
+  if constexpr (ASYNC) {
     issue_maps(batch, mbuf0);
     cp_commit();
     cp_wait_group<0>();
@@ -343,7 +351,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   for (int it = 0; batch < nbatch; batch += gridDim.x, ++it) {
     const int cell = cell_of(batch);
     const bool active = in_team && cell < p.end;
-    if constexpr (FE_TK_ASYNC) {
+    if constexpr (ASYNC) {
       cp_wait_group<0>();                // map rows of the next batch
       team_sync();
       const int par = it & 1;
@@ -782,7 +790,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       }
     }
     // the next batch's data (loads issued at the top of this iteration)
-    if constexpr (FE_TK_ASYNC) {
+    if constexpr (ASYNC) {
       cp_wait_group<1>();
     } else {
       park();
@@ -794,7 +802,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 }  // namespace fe
 
 #ifndef FE_TK_Q5_MINB
-#define FE_TK_Q5_MINB 2
+#define FE_TK_Q5_MINB 1002   // 256-thread CTAs, 2 per SM, cp.async gather
 #endif
 #ifndef FE_TK_Q6_MINB
 #define FE_TK_Q6_MINB 2

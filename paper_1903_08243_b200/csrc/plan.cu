@@ -877,7 +877,7 @@ int fill_tensor_tables(const fe_plan* p, TensorParams<Q, P>* hp) {
 template <int FORM, int DIM, int P, int Q, int MINB, bool DIRECT>
 int tensor_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
-  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT, tensor_block<MINB>()>;
+  using SM = TensorLayout<DIM, P, Q, form_vs(FORM, DIM), DIRECT, tensor_block<MINB>(), tensor_async<MINB>()>;
   static_assert(sizeof(TP) <= 32000, "parameter block too large");
   TP* hp = new TP();
   if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
@@ -1304,7 +1304,11 @@ __global__ void k_chunk_maxdof(const int32_t* __restrict__ rm, int nc, int nd, c
   const int c = (int)(t / nd);
   int k = 0;
   while (k + 1 < nchunk && c >= bounds[k + 1]) ++k;
-  atomicMax(out + k, rm[t]);
+  // one atomic per warp and chunk (126M same-address atomics at C5 otherwise:
+  // 0.68 s of bind time in the ncu launch list, profiles/r02/launches_r2k.csv)
+  const unsigned grp = __match_any_sync(__activemask(), k);
+  const int m = __reduce_max_sync(grp, rm[t]);
+  if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicMax(out + k, m);
 }
 
 __global__ void k_check_range(const int32_t* __restrict__ m, int64_t n, int64_t hi, int* flag) {
