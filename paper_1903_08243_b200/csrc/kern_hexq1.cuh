@@ -176,4 +176,165 @@ hexq1_lap_kernel(const __grid_constant__ TensorParams<2, 2> p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Thread-per-cell sum-factorised scalar Laplacian for Q2 hexahedra on the
+// 3x3x3 Gauss rule (C3-Q2), collocation form (12 q^4 MACs):
+//   interpolate u to the Gauss points with three B contractions (in
+//   registers), then per point differentiate with the collocation matrix Dc
+//   along the three lines through it (9 MACs), apply the adjugate-form flux
+//   and accumulate its Dc^T contributions into a point-space output (9 MACs);
+//   three B^T contractions bring that back to the 27 dofs.
+// The whole cell lives in one thread's registers (27 point values + 27
+// outputs + the 21 monomial map coefficients): no shared memory, no barriers,
+// no shuffles -- the team kernels spend ~45% of their issue slots on those
+// (plane_t at Q = 3: FP64 pipe 53% active, profiles/r01/ncu13_summaries.txt).
+// All 24 table entries (B, Dc, x, w) stay resident in uniform registers.
+// ---------------------------------------------------------------------------
+struct HexQ2Params {
+  MeshView mesh;
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  int32_t start, end;
+  int32_t lex[27];      // local dof of tensor node n = i + 3 j + 9 k
+  double B[3][3], Dc[3][3], x[3], w[3];
+};
+
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+hexq2_lap_kernel(const __grid_constant__ HexQ2Params p) {
+  constexpr int Q = 3;
+  const int cell = p.start + blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  double uq[Q][Q][Q];  // [k][j][i] dof values, then [c][b][a] point values
+#pragma unroll
+  for (int n = 0; n < 27; ++n)
+    uq[n / 9][(n / 3) % 3][n % 3] = __ldg(p.u + __ldg(p.mesh.map + p.lex[n] * cs + cell));
+  double cf[7][3];
+  {
+    double X[8][3];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) load_vertex<3>(p.mesh.coords, __ldg(p.mesh.vmap + v * cs + cell), X[v]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      cf[0][d] = X[1][d] - X[0][d];                       // xi
+      cf[1][d] = X[2][d] - X[0][d];                       // eta
+      cf[2][d] = X[4][d] - X[0][d];                       // zeta
+      cf[3][d] = (X[3][d] - X[2][d]) - cf[0][d];          // xi eta
+      cf[4][d] = (X[5][d] - X[4][d]) - cf[0][d];          // xi zeta
+      cf[5][d] = (X[6][d] - X[4][d]) - cf[1][d];          // eta zeta
+      cf[6][d] = ((X[7][d] - X[6][d]) - (X[5][d] - X[4][d])) - (X[3][d] - X[2][d]) + cf[0][d];
+    }
+  }
+  // ---- u at the Gauss points: B along x, y, z --------------------------------
+#pragma unroll
+  for (int k = 0; k < Q; ++k)
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const double v0 = uq[k][j][0], v1 = uq[k][j][1], v2 = uq[k][j][2];
+#pragma unroll
+      for (int a = 0; a < Q; ++a) uq[k][j][a] = fma(p.B[a][2], v2, fma(p.B[a][1], v1, p.B[a][0] * v0));
+    }
+#pragma unroll
+  for (int k = 0; k < Q; ++k)
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      const double v0 = uq[k][0][a], v1 = uq[k][1][a], v2 = uq[k][2][a];
+#pragma unroll
+      for (int b = 0; b < Q; ++b) uq[k][b][a] = fma(p.B[b][2], v2, fma(p.B[b][1], v1, p.B[b][0] * v0));
+    }
+#pragma unroll
+  for (int b = 0; b < Q; ++b)
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      const double v0 = uq[0][b][a], v1 = uq[1][b][a], v2 = uq[2][b][a];
+#pragma unroll
+      for (int c = 0; c < Q; ++c) uq[c][b][a] = fma(p.B[c][2], v2, fma(p.B[c][1], v1, p.B[c][0] * v0));
+    }
+  // ---- points: gradient, flux, transposed collocation derivative --------------
+  double out[Q][Q][Q];
+#pragma unroll
+  for (int n = 0; n < 27; ++n) out[n / 9][(n / 3) % 3][n % 3] = 0.0;
+#pragma unroll
+  for (int c = 0; c < Q; ++c) {
+    const double zeta = p.x[c];
+    double A0[3], A1[3], B0[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      A0[d] = fma(zeta, cf[4][d], cf[0][d]);   // dx/dxi   = A0 + eta A1
+      A1[d] = fma(zeta, cf[6][d], cf[3][d]);   // dx/deta  = B0 + xi A1
+      B0[d] = fma(zeta, cf[5][d], cf[1][d]);
+    }
+#pragma unroll
+    for (int b = 0; b < Q; ++b) {
+      const double eta = p.x[b], wbc = p.w[b] * p.w[c];
+      double Jx[3], C0[3], C1[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        Jx[d] = fma(eta, A1[d], A0[d]);
+        C0[d] = fma(eta, cf[5][d], cf[2][d]);  // dx/dzeta = C0 + xi C1
+        C1[d] = fma(eta, cf[6][d], cf[4][d]);
+      }
+#pragma unroll
+      for (int a = 0; a < Q; ++a) {
+        const double xi = p.x[a];
+        double J[3][3], A[3][3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          J[d][0] = Jx[d];
+          J[d][1] = fma(xi, A1[d], B0[d]);
+          J[d][2] = fma(xi, C1[d], C0[d]);
+        }
+        const double det = det_adj<3>(J, A);
+        const double s = (p.w[a] * wbc) * rcp(fabs(det));
+        double g[3];
+        g[0] = fma(p.Dc[a][2], uq[c][b][2], fma(p.Dc[a][1], uq[c][b][1], p.Dc[a][0] * uq[c][b][0]));
+        g[1] = fma(p.Dc[b][2], uq[c][2][a], fma(p.Dc[b][1], uq[c][1][a], p.Dc[b][0] * uq[c][0][a]));
+        g[2] = fma(p.Dc[c][2], uq[2][b][a], fma(p.Dc[c][1], uq[1][b][a], p.Dc[c][0] * uq[0][b][a]));
+        double t[3], f[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) t[e] = s * fma(A[2][e], g[2], fma(A[1][e], g[1], A[0][e] * g[0]));
+#pragma unroll
+        for (int r = 0; r < 3; ++r) f[r] = fma(A[r][2], t[2], fma(A[r][1], t[1], A[r][0] * t[0]));
+#pragma unroll
+        for (int e = 0; e < Q; ++e) {
+          out[c][b][e] = fma(p.Dc[a][e], f[0], out[c][b][e]);
+          out[c][e][a] = fma(p.Dc[b][e], f[1], out[c][e][a]);
+          out[e][b][a] = fma(p.Dc[c][e], f[2], out[e][b][a]);
+        }
+      }
+    }
+  }
+  // ---- back to the dofs: B^T along z, y, x ------------------------------------
+#pragma unroll
+  for (int b = 0; b < Q; ++b)
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      const double v0 = out[0][b][a], v1 = out[1][b][a], v2 = out[2][b][a];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) out[k][b][a] = fma(p.B[2][k], v2, fma(p.B[1][k], v1, p.B[0][k] * v0));
+    }
+#pragma unroll
+  for (int k = 0; k < Q; ++k)
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      const double v0 = out[k][0][a], v1 = out[k][1][a], v2 = out[k][2][a];
+#pragma unroll
+      for (int j = 0; j < Q; ++j) out[k][j][a] = fma(p.B[2][j], v2, fma(p.B[1][j], v1, p.B[0][j] * v0));
+    }
+  griddep_wait();
+#pragma unroll
+  for (int k = 0; k < Q; ++k)
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const double v0 = out[k][j][0], v1 = out[k][j][1], v2 = out[k][j][2];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const double r = fma(p.B[2][i], v2, fma(p.B[1][i], v1, p.B[0][i] * v0));
+        scatter_add(p.y, __ldg(p.mesh.map + p.lex[i + 3 * j + 9 * k] * cs + cell), r);
+      }
+    }
+}
+
 }  // namespace fe

@@ -143,6 +143,216 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     for (int i = 0; i < P; ++i) scatter_add(p.y, 2 * (int64_t)dof[j * P + i] + c, y[j][i]);
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined variant (round 2): the same arithmetic in PERSISTENT warps with
+// the indirect gather P_e u taken off the critical path.  pair_kernel above
+// issues map -> u loads and only then computes, with 8 warps per SM (255
+// registers) to cover ~1.5 us of dependent DRAM latency per cell (ncu: FP64
+// pipe 52% active).  Here every warp walks batches of 16 cells and keeps
+// three stages in flight through cp.async (LDGSTS), all warp-local (no CTA
+// barrier anywhere):
+//   batch n+2: dof-id row + vertex ids          -> map ring (3 buffers)
+//   batch n+1: u (own component), coordinates,
+//              mu / lambda at the 4 vertices    -> data ring (2 buffers)
+//   batch n  : compute from shared memory (u is re-read per point row: one
+//              conflict-free LDS.64 per ~17 FP64 instructions) and scatter
+//              with the ids still parked in the map ring.
+// Neither the dof ids (P^2 registers) nor u (2 P^2 registers) live in
+// registers any more.
+// ---------------------------------------------------------------------------
+template <int P>
+struct PairPipeLayout {
+  static constexpr int NDS = P * P;
+  static constexpr int MR = NDS + 4;              // dof ids + vertex ids per cell
+  static constexpr int MRS = MR | 1;              // odd stride: conflict-free id reads across cells
+  static constexpr int MAP_INTS = 16 * MRS;       // one map buffer (16 cells)
+  static constexpr int MAP_DOUBLES = (3 * MAP_INTS + 1) / 2;
+  static constexpr int U = 0;                     // [NDS][32] own-component dof values
+  static constexpr int X = U + NDS * 32;          // [4][16] double2 vertex coordinates
+  static constexpr int MU = X + 4 * 16 * 2;       // [4][16]
+  static constexpr int LAM = MU + 4 * 16;         // [4][16]
+  static constexpr int DATA = LAM + 4 * 16;       // one data buffer
+  static constexpr int WARP_DOUBLES = ((2 * DATA + MAP_DOUBLES) + 1) & ~1;
+};
+
+template <int FORM, int P, int Q, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
+pair_pipe_kernel(const __grid_constant__ TensorParams<Q, P> p) {
+  static_assert(FORM == FE_FORM_ELASTICITY_LAME || FORM == FE_FORM_ELASTICITY, "2D elasticity forms");
+  using L = PairPipeLayout<P>;
+  constexpr int NDS = L::NDS, MR = L::MR, MRS = L::MRS;
+  constexpr bool LAME = FORM == FE_FORM_ELASTICITY_LAME;
+  extern __shared__ double smem_all[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane & 1, slot = lane >> 1;
+  double* const sw = smem_all + warp * L::WARP_DOUBLES;
+  int32_t* const smap = reinterpret_cast<int32_t*>(sw + 2 * L::DATA);
+  const int64_t cs = p.mesh.nc_stride;
+  const int ncell = p.end - p.start;
+  const int nbatch = (ncell + 15) / 16;
+  const int wstride = gridDim.x * WARPS;
+  // The 1D tables are mirror-symmetric (nodes and points symmetric about 1/2,
+  // verified at plan time): B[q][i] = B[Q-1-q][P-1-i], D[q][i] = -D[Q-1-q][P-1-i].
+  // Reading only the lower half keeps every table entry of the loop resident
+  // in uniform registers (sm_100a feeds constant operands through ~80 URs; the
+  // full tables do not fit and ptxas then parks them in vector registers and
+  // moves them back with R2UR inside the loop).
+  auto TB = [&](int q, int i) { return 2 * q < Q ? p.B[q][i] : p.B[Q - 1 - q][P - 1 - i]; };
+  auto TD = [&](int q, int i) { return 2 * q < Q ? p.D[q][i] : -p.D[Q - 1 - q][P - 1 - i]; };
+  auto TX = [&](int q) { return 2 * q < Q ? p.x[q] : 1.0 - p.x[Q - 1 - q]; };
+  auto TW = [&](int q) { return 2 * q < Q ? p.w[q] : p.w[Q - 1 - q]; };
+
+  auto issue_maps = [&](int batch, int mb) {
+    const int cell = p.start + batch * 16 + slot;
+    if (batch >= nbatch || cell >= p.end) return;
+    int32_t* dst = smap + mb * L::MAP_INTS + slot * MRS;
+    const int32_t* mrow = p.maplex + (int64_t)cell * NDS;
+#pragma unroll
+    for (int e = c; e < MR; e += 2) {
+      if (e < NDS) cp_async4(dst + e, mrow + e);
+      else cp_async4(dst + e, p.mesh.vmap + (e - NDS) * cs + cell);
+    }
+  };
+  auto issue_data = [&](int batch, int mb, int db) {
+    const int cell = p.start + batch * 16 + slot;
+    if (batch >= nbatch || cell >= p.end) return;
+    const int32_t* ids = smap + mb * L::MAP_INTS + slot * MRS;
+    double* d = sw + db * L::DATA;
+#pragma unroll
+    for (int e = 0; e < NDS; ++e) cp_async8(d + L::U + e * 32 + lane, p.u + 2 * (int64_t)ids[e] + c);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int v = 2 * c + k;
+      const int vid = ids[NDS + v];
+      cp_async16(d + L::X + (v * 16 + slot) * 2, p.mesh.coords + 2 * (int64_t)vid);
+      if constexpr (LAME) {
+        cp_async8(d + L::MU + v * 16 + slot, p.mu + vid);
+        cp_async8(d + L::LAM + v * 16 + slot, p.lam + vid);
+      }
+    }
+  };
+
+  int batch = blockIdx.x * WARPS + warp;
+  issue_maps(batch, 0);
+  cp_commit();
+  issue_maps(batch + wstride, 1);
+  cp_commit();
+  cp_wait_group<1>();
+  __syncwarp();
+  issue_data(batch, 0, 0);
+  cp_commit();
+  int m0 = 0;  // map buffer of the current batch (ring of 3)
+  int d0 = 0;  // data buffer of the current batch (ring of 2)
+#pragma unroll 1
+  for (; batch < nbatch; batch += wstride) {
+    const int m1 = m0 == 2 ? 0 : m0 + 1, m2 = m1 == 2 ? 0 : m1 + 1;
+    issue_maps(batch + 2 * wstride, m2);
+    cp_commit();
+    cp_wait_group<1>();        // data of this batch and ids of the next have landed
+    __syncwarp();
+    issue_data(batch + wstride, m1, d0 ^ 1);
+    cp_commit();
+
+    const int cell = p.start + batch * 16 + slot;
+    const bool active = cell < p.end;
+    const unsigned live = __ballot_sync(0xffffffffu, active);
+    if (active) {
+      const double* d = sw + d0 * L::DATA;
+      const double* su = d + L::U + lane;
+      double X[4][2], mv[4], lv[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double2 xv = *reinterpret_cast<const double2*>(d + L::X + (v * 16 + slot) * 2);
+        X[v][0] = xv.x;
+        X[v][1] = xv.y;
+        if constexpr (LAME) {
+          mv[v] = d[L::MU + v * 16 + slot];
+          lv[v] = d[L::LAM + v * 16 + slot];
+        } else {
+          mv[v] = 0.5;
+          lv[v] = 0.0;
+        }
+      }
+      double j1[2], d1[2];
+#pragma unroll
+      for (int dd = 0; dd < 2; ++dd) {
+        j1[dd] = X[2][dd] - X[0][dd];
+        d1[dd] = (X[3][dd] - X[1][dd]) - j1[dd];
+      }
+      double y[P][P];
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int i = 0; i < P; ++i) y[j][i] = 0.0;
+
+#pragma unroll
+      for (int b = 0; b < Q; ++b) {
+        const double eta = TX(b), le = 1.0 - eta, wb = TW(b);
+        double Y0[P], Y1[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) Y0[i] = Y1[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j)
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const double uv = su[(j * P + i) * 32];
+            Y0[i] = fma(TB(b, j), uv, Y0[i]);
+            Y1[i] = fma(TD(b, j), uv, Y1[i]);
+          }
+        double J0[2];
+#pragma unroll
+        for (int dd = 0; dd < 2; ++dd) J0[dd] = (X[1][dd] - X[0][dd]) * le + (X[3][dd] - X[2][dd]) * eta;
+        const double det0 = J0[0] * j1[1] - j1[0] * J0[1], ddet = J0[0] * d1[1] - d1[0] * J0[1];
+        const double mm0 = mv[0] * le + mv[2] * eta, dm = mv[1] * le + mv[3] * eta - mm0;
+        const double l0 = lv[0] * le + lv[2] * eta, dl = lv[1] * le + lv[3] * eta - l0;
+        double Z0[P], Z1[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) Z0[i] = Z1[i] = 0.0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          const double xi = TX(a);
+          double gx = 0.0, gy = 0.0;
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            gx = fma(TD(a, i), Y0[i], gx);
+            gy = fma(TB(a, i), Y1[i], gy);
+          }
+          const double J01 = fma(xi, d1[0], j1[0]), J11 = fma(xi, d1[1], j1[1]);
+          const double det = fma(xi, ddet, det0);
+          const double sc = (TW(a) * wb) * recip<(P <= 4)>(fabs(det));
+          const double mu = sc * fma(xi, dm, mm0), lam = sc * fma(xi, dl, l0);
+          const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
+          const double o0 = __shfl_xor_sync(live, g0, 1), o1 = __shfl_xor_sync(live, g1, 1);
+          const double tr = c ? (g1 + o0) : (g0 + o1);
+          const double s0 = g0 + (c ? o1 : g0), s1 = g1 + (c ? g1 : o0);
+          const double t0 = fma(mu, s0, c ? 0.0 : lam * tr), t1 = fma(mu, s1, c ? lam * tr : 0.0);
+          const double f0 = t0 * J11 - t1 * J01, f1 = t1 * J0[0] - t0 * J0[1];
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            Z0[i] = fma(TD(a, i), f0, Z0[i]);
+            Z1[i] = fma(TB(a, i), f1, Z1[i]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j)
+#pragma unroll
+          for (int i = 0; i < P; ++i) y[j][i] = fma(TB(b, j), Z0[i], fma(TD(b, j), Z1[i], y[j][i]));
+      }
+      griddep_wait();
+      const int32_t* ids = smap + m0 * L::MAP_INTS + slot * MRS;
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int i = 0; i < P; ++i) scatter_add(p.y, 2 * (int64_t)ids[j * P + i] + c, y[j][i]);
+    }
+    __syncwarp();              // the rings are rewritten by the next iteration's copies
+    m0 = m1;
+    d0 ^= 1;
+  }
+  cp_wait_all();
+}
+
 }  // namespace fe
 
 // registry hook (plan.cu): PRV(form, degree, P, Q, MINB); C4-quad-Q3/Q4 (Q1/Q2:

@@ -38,8 +38,14 @@
 #include "common.cuh"
 #include "kern_tensor.cuh"
 
-namespace fe {
+#ifndef FE_PLANE_MONO
+#define FE_PLANE_MONO 1   // monomial trilinear geometry (round 2)
+#endif
+#ifndef FE_PLANE_RCP
+#define FE_PLANE_RCP 0    // 1: MUFU-seeded reciprocal instead of the IEEE division
+#endif
 
+namespace fe {
 
 // ---- compile-time layout ------------------------------------------------------
 // Lanes are team-major (lane = T * Q + t).  Worst count of 8-byte words on one
@@ -200,7 +206,26 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     issue_map(wb + 2 * GW, (it + 2) % 3);
     cp_commit();
 
-    const double* sX = sX0 + (cur * TPW + Tc) * XS;
+    double* sX = sX0 + (cur * TPW + Tc) * XS;
+#if FE_PLANE_MONO
+    // trilinear map in monomial form, once per cell: x = sum C_abc xi^a eta^b zeta^c.
+    // Thread d < 3 converts coordinate d in place (slot v = a + 2b + 4c), so a
+    // point line needs 6 FMAs per coordinate for its Jacobian factors instead
+    // of 22 operations on vertex differences.
+    if (active && t < 3) {
+      double xv[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) xv[v] = sX[v * 4 + t];
+      sX[1 * 4 + t] = xv[1] - xv[0];
+      sX[2 * 4 + t] = xv[2] - xv[0];
+      sX[4 * 4 + t] = xv[4] - xv[0];
+      sX[3 * 4 + t] = (xv[3] - xv[2]) - (xv[1] - xv[0]);
+      sX[5 * 4 + t] = (xv[5] - xv[4]) - (xv[1] - xv[0]);
+      sX[6 * 4 + t] = (xv[6] - xv[4]) - (xv[2] - xv[0]);
+      sX[7 * 4 + t] = ((xv[7] - xv[6]) - (xv[5] - xv[4])) - ((xv[3] - xv[2]) - (xv[1] - xv[0]));
+    }
+    __syncwarp();
+#endif
     auto X = [&](int vx, int vy, int vz, int d) { return sX[(vx + 2 * vy + 4 * vz) * 4 + d]; };
     double yp[P][P];  // output plane y[i, j = t, k], [k][i]
 #pragma unroll
@@ -253,6 +278,18 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         const double lx0 = 1.0 - xi, lz0 = 1.0 - zeta;
         // d/dxi column: linear in eta; d/deta: constant on the line; d/dzeta: linear in eta
         double g0[3], dg[3], J1[3], h0[3], dh[3];
+#if FE_PLANE_MONO
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          g0[d] = fma(zeta, X(1, 0, 1, d), X(1, 0, 0, d));
+          dg[d] = fma(zeta, X(1, 1, 1, d), X(1, 1, 0, d));
+          J1[d] = fma(xi, dg[d], fma(zeta, X(0, 1, 1, d), X(0, 1, 0, d)));
+          h0[d] = fma(xi, X(1, 0, 1, d), X(0, 0, 1, d));
+          dh[d] = fma(xi, X(1, 1, 1, d), X(0, 1, 1, d));
+        }
+        (void)lx0;
+        (void)lz0;
+#else
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           const double q0 = (X(1, 0, 0, d) - X(0, 0, 0, d)) * lz0 + (X(1, 0, 1, d) - X(0, 0, 1, d)) * zeta;
@@ -265,6 +302,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double f1 = (X(0, 1, 1, d) - X(0, 1, 0, d)) * lx0 + (X(1, 1, 1, d) - X(1, 1, 0, d)) * xi;
           h0[d] = f0; dh[d] = f1 - f0;
         }
+#endif
         double W0[P], W1[P], W2[P];
 #pragma unroll
         for (int j = 0; j < P; ++j) W0[j] = W1[j] = W2[j] = 0.0;
@@ -296,7 +334,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wac * p.w[b]) / fabs(det);
+          const double s = (wac * p.w[b]) * recip<(FE_PLANE_RCP != 0)>(fabs(det));
           // v = adj^T g (= det * physical gradient), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;

@@ -184,8 +184,24 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
     const bool active = valid(wb);
     double* sU = sU0 + (cur * TPW + Tc) * CS;
-    const double* sX = sX0 + (cur * TPW + Tc) * XS;
+    double* sX = sX0 + (cur * TPW + Tc) * XS;
     const int32_t* sM = sM0 + ((it % 3) * TPW + Tc) * MS;
+#if FE_PLANE_MONO
+    // trilinear map in monomial form, once per cell (kern_plane.cuh): thread
+    // d < 3 converts coordinate d in place; consumed after the phase-1 barriers
+    if (active && t < 3) {
+      double xv[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) xv[v] = sX[v * 4 + t];
+      sX[1 * 4 + t] = xv[1] - xv[0];
+      sX[2 * 4 + t] = xv[2] - xv[0];
+      sX[4 * 4 + t] = xv[4] - xv[0];
+      sX[3 * 4 + t] = (xv[3] - xv[2]) - (xv[1] - xv[0]);
+      sX[5 * 4 + t] = (xv[5] - xv[4]) - (xv[1] - xv[0]);
+      sX[6 * 4 + t] = (xv[6] - xv[4]) - (xv[2] - xv[0]);
+      sX[7 * 4 + t] = ((xv[7] - xv[6]) - (xv[5] - xv[4])) - ((xv[3] - xv[2]) - (xv[1] - xv[0]));
+    }
+#endif
 
     // ---- phase 1: thread j = t < P holds the dof plane u[i, j, k] --------
     double Z[P][Q];  // Z[i][c] = sum_k B[c][k] u[i][j][k]
@@ -258,6 +274,15 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       auto X = [&](int vx, int vy, int vz, int d) { return sX[(vx + 2 * vy + 4 * vz) * 4 + d]; };
       // d/deta column: linear in zeta; d/dzeta column: linear in eta (xi fixed)
       double e0[3], de[3], f0[3], df[3];
+#if FE_PLANE_MONO
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        e0[d] = fma(xi, X(1, 1, 0, d), X(0, 1, 0, d));
+        de[d] = fma(xi, X(1, 1, 1, d), X(0, 1, 1, d));
+        f0[d] = fma(xi, X(1, 0, 1, d), X(0, 0, 1, d));
+        df[d] = de[d];
+      }
+#else
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         const double s0 = (X(0, 1, 0, d) - X(0, 0, 0, d)) * (1.0 - xi) + (X(1, 1, 0, d) - X(1, 0, 0, d)) * xi;
@@ -267,6 +292,7 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         e0[d] = s0; de[d] = s1 - s0;
         f0[d] = g0; df[d] = g1 - g0;
       }
+#endif
 #pragma unroll
       for (int b = 0; b < Q; ++b) {
         const double eta = p.x[b], wab = wa * p.w[b];
@@ -274,9 +300,14 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         double r0[3], dr[3], J2[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
+#if FE_PLANE_MONO
+          r0[d] = fma(eta, X(1, 1, 0, d), X(1, 0, 0, d));
+          dr[d] = fma(eta, X(1, 1, 1, d), X(1, 0, 1, d));
+#else
           const double q0 = (X(1, 0, 0, d) - X(0, 0, 0, d)) * (1.0 - eta) + (X(1, 1, 0, d) - X(0, 1, 0, d)) * eta;
           const double q1 = (X(1, 0, 1, d) - X(0, 0, 1, d)) * (1.0 - eta) + (X(1, 1, 1, d) - X(0, 1, 1, d)) * eta;
           r0[d] = q0; dr[d] = q1 - q0;
+#endif
           J2[d] = fma(eta, df[d], f0[d]);
         }
         double uq[Q];
@@ -317,7 +348,7 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wab * p.w[c]) / fabs(det);
+          const double s = (wab * p.w[c]) * recip<(FE_PLANE_RCP != 0)>(fabs(det));
           // v = adj^T g (physical gradient * det), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;

@@ -97,6 +97,9 @@ constexpr int pick_inner(int lo, int nr, int ns, int rstep) {
 }
 constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
 
+#ifndef FE_TK_MONO
+#define FE_TK_MONO 1    // monomial trilinear geometry (round 2)
+#endif
 #ifndef FE_TK_ASYNC
 #define FE_TK_ASYNC 0   // 1: cp.async gather pipeline (no prefetch registers)
 #endif
@@ -366,6 +369,42 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       load_map(batch + 2 * gridDim.x);
     }
 
+#if FE_TK_MONO
+    // trilinear map in monomial form, once per cell: x = sum C_abc xi^a eta^b
+    // zeta^c, thread d < 3 converting coordinate d in place (slot a + 2b + 4c).
+    // The per-pencil Jacobian factors below then cost 6 FMAs per coordinate
+    // instead of ~40 operations on vertex differences.  Consumed after the
+    // z-stage barrier.
+    if constexpr (DIM == 3) {
+      if (active && t < 3) {
+        double xv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) xv[v] = sX[v * 3 + t];
+        sX[1 * 3 + t] = xv[1] - xv[0];
+        sX[2 * 3 + t] = xv[2] - xv[0];
+        sX[4 * 3 + t] = xv[4] - xv[0];
+        sX[3 * 3 + t] = (xv[3] - xv[2]) - (xv[1] - xv[0]);
+        sX[5 * 3 + t] = (xv[5] - xv[4]) - (xv[1] - xv[0]);
+        sX[6 * 3 + t] = (xv[6] - xv[4]) - (xv[2] - xv[0]);
+        sX[7 * 3 + t] = ((xv[7] - xv[6]) - (xv[5] - xv[4])) - ((xv[3] - xv[2]) - (xv[1] - xv[0]));
+      }
+      if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {   // mu, lambda likewise
+        if (active && (t == 3 || t == 4)) {
+          double* f = t == 3 ? sMU : sLAM;
+          double xv[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) xv[v] = f[v];
+          f[1] = xv[1] - xv[0];
+          f[2] = xv[2] - xv[0];
+          f[4] = xv[4] - xv[0];
+          f[3] = (xv[3] - xv[2]) - (xv[1] - xv[0]);
+          f[5] = (xv[5] - xv[4]) - (xv[1] - xv[0]);
+          f[6] = (xv[6] - xv[4]) - (xv[2] - xv[0]);
+          f[7] = ((xv[7] - xv[6]) - (xv[5] - xv[4])) - ((xv[3] - xv[2]) - (xv[1] - xv[0]));
+        }
+      }
+    }
+#endif
     // ---- forward: reference gradients at the points of this thread's x-pencil
     double g[VS][DIM][Q];
 #pragma unroll
@@ -543,7 +582,13 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       double m0 = 0.0, dm = 0.0, l0 = 0.0, dl = 0.0;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        if constexpr (DIM == 3) {
+        if constexpr (DIM == 3 && FE_TK_MONO) {
+          d1[d] = fma(zeta, Xv(1, 1, 1, d), Xv(1, 1, 0, d));
+          c0[d] = fma(eta, d1[d], fma(zeta, Xv(1, 0, 1, d), Xv(1, 0, 0, d)));
+          j1[d] = fma(zeta, Xv(0, 1, 1, d), Xv(0, 1, 0, d));
+          j2[d] = fma(eta, Xv(0, 1, 1, d), Xv(0, 0, 1, d));
+          d2[d] = fma(eta, Xv(1, 1, 1, d), Xv(1, 0, 1, d));
+        } else if constexpr (DIM == 3) {
           double s = 0.0;
 #pragma unroll
           for (int vy = 0; vy < 2; ++vy)
@@ -566,7 +611,12 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           j1[d] = e0; d1[d] = e1 - e0;
         }
       }
-      if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+      if constexpr (FORM == FE_FORM_ELASTICITY_LAME && DIM == 3 && FE_TK_MONO) {
+        m0 = fma(eta, fma(zeta, sMU[6], sMU[2]), fma(zeta, sMU[4], sMU[0]));
+        dm = fma(eta, fma(zeta, sMU[7], sMU[3]), fma(zeta, sMU[5], sMU[1]));
+        l0 = fma(eta, fma(zeta, sLAM[6], sLAM[2]), fma(zeta, sLAM[4], sLAM[0]));
+        dl = fma(eta, fma(zeta, sLAM[7], sLAM[3]), fma(zeta, sLAM[5], sLAM[1]));
+      } else if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
         double mx[2] = {0.0, 0.0}, lx[2] = {0.0, 0.0};
 #pragma unroll
         for (int v = 0; v < NV; ++v) {

@@ -1030,7 +1030,65 @@ int hexq1_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   return FE_OK;
 }
 
-// component-pair 2D elasticity kernel (kern_pair.cuh)
+// thread-per-cell sum-factorised Q2 hex Laplacian (kern_hexq1.cuh)
+#ifndef FE_HEXQ2_BLOCK
+#define FE_HEXQ2_BLOCK 64
+#endif
+int hexq2_prepare(fe_plan* p) {
+  if ((int)p->lex.size() != 27) return fail(FE_EUNSUPPORTED, "hexq2 kernel needs the 27-node tensor map");
+  TensorParams<3, 3> tp;
+  if (int rc = fill_tensor_tables<3, 3>(p, &tp)) return rc;
+  HexQ2Params* hp = new HexQ2Params();
+  for (int n = 0; n < 27; ++n) hp->lex[n] = p->lex[n];
+  for (int a = 0; a < 3; ++a) {
+    for (int i = 0; i < 3; ++i) {
+      hp->B[a][i] = tp.B[a][i];
+      hp->Dc[a][i] = tp.Dc[a][i];
+    }
+    hp->x[a] = tp.x[a];
+    hp->w[a] = tp.w[a];
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(HexQ2Params);
+  return FE_OK;
+}
+
+int hexq2_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                 const double*, const double*, cudaStream_t s) {
+  HexQ2Params hpv = *static_cast<const HexQ2Params*>(p->host_params);
+  hpv.mesh = mesh_view(p);
+  hpv.u = u;
+  hpv.y = y;
+  hpv.start = start;
+  hpv.end = end;
+  const int n = end - start;
+  if (n > 0) launch_op(hexq2_lap_kernel<FE_HEXQ2_BLOCK, 1>, (unsigned)((n + FE_HEXQ2_BLOCK - 1) / FE_HEXQ2_BLOCK), FE_HEXQ2_BLOCK, 0, s, hpv);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
+// component-pair 2D elasticity kernel (kern_pair.cuh).  FE_PAIR_CFG selects
+// the kernel: 0 = round-1 kernel (one cell pair per thread pair, gather on
+// the critical path), 1 = pipelined persistent kernel, 4-warp CTAs, 2 per SM
+#ifndef FE_PAIR_CFG
+#define FE_PAIR_CFG 0   // measured: the pipelined kernel is slower (0.37 / 0.68 vs 0.32 / 0.58 ms at Q3 / Q4,
+#endif                  // profiles/r02/ab_pair_pipe.txt): ptxas hoists the table constants out of the persistent
+                        // loop into vector registers (sm_100a has ~80 uniform registers) and the loop fills with moves
+constexpr int kPairPipeWarps = 4;
+
+template <int FORM, int P, int Q, int MINB>
+int pair_pipe_setup(fe_plan* p, int dev_sms) {
+  using L = PairPipeLayout<P>;
+  auto kfn = pair_pipe_kernel<FORM, P, Q, kPairPipeWarps, MINB>;
+  const size_t smem = (size_t)kPairPipeWarps * L::WARP_DOUBLES * sizeof(double);
+  CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPairPipeWarps * 32, smem));
+  p->tables_bytes = smem;
+  p->persistent_ctas = dev_sms * (per_sm > 0 ? per_sm : 1);
+  return FE_OK;
+}
+
 template <int FORM, int P, int Q, int MINB>
 int pair_prepare(fe_plan* p) {
   using TP = TensorParams<Q, P>;
@@ -1041,6 +1099,22 @@ int pair_prepare(fe_plan* p) {
   }
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
+  const char* env = getenv("FE_PAIR_CFG");
+  p->dmma_cfg = env ? atoi(env) : FE_PAIR_CFG;
+  if (p->dmma_cfg < 0 || p->dmma_cfg > 1) p->dmma_cfg = FE_PAIR_CFG;
+  // the pipelined kernel reads the mirror-symmetric half of the 1D tables
+  for (int q = 0; q < Q; ++q) {
+    if (std::fabs(hp->x[q] - (1.0 - hp->x[Q - 1 - q])) > 1e-13 || std::fabs(hp->w[q] - hp->w[Q - 1 - q]) > 1e-13)
+      p->dmma_cfg = 0;
+    for (int i = 0; i < P; ++i)
+      if (std::fabs(hp->B[q][i] - hp->B[Q - 1 - q][P - 1 - i]) > 1e-12 ||
+          std::fabs(hp->D[q][i] + hp->D[Q - 1 - q][P - 1 - i]) > 1e-11)
+        p->dmma_cfg = 0;
+  }
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (p->dmma_cfg != 0) return pair_pipe_setup<FORM, P, Q, 2>(p, sms);
   return FE_OK;
 }
 
@@ -1059,8 +1133,18 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   hp->lam = c1;
   hp->start = start;
   hp->end = end;
-  const int64_t nt = 2 * (int64_t)(end - start);
-  launch_op(pair_kernel<FORM, P, Q, MINB>, (unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s, *hp);
+  if (p->dmma_cfg == 0) {
+    const int64_t nt = 2 * (int64_t)(end - start);
+    launch_op(pair_kernel<FORM, P, Q, MINB>, (unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s, *hp);
+  } else {
+    const int nbatch = (end - start + 15) / 16;
+    const int need = (nbatch + kPairPipeWarps - 1) / kPairPipeWarps;
+    const unsigned grid = (unsigned)(need < p->persistent_ctas ? need : p->persistent_ctas);
+    if (grid > 0) {
+      const unsigned blk = kPairPipeWarps * 32;
+      launch_op(pair_pipe_kernel<FORM, P, Q, kPairPipeWarps, 2>, grid, blk, p->tables_bytes, s, *hp);
+    }
+  }
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
 }
@@ -1120,6 +1204,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define HQ1V()                                                                               \
   {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 1, 8, 27, "sum_factorised_q1", 128,           \
    hexq1_prepare, hexq1_launch}
+#define HQ2V()                                                                               \
+  {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 2, 27, 28, "sum_factorised_q2", FE_HEXQ2_BLOCK, \
+   hexq2_prepare, hexq2_launch}
 #define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
   {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
    split_launch<FORM, DIM, ND, NQS>}
@@ -1212,6 +1299,7 @@ static const Variant kVariants[] = {
     // (..., MINB, quadrature-loop unroll): per measurement, profiles/r01/sweep_unroll*.txt
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1, 8),
     HQ1V(),
+    HQ2V(),
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 1, 1),
@@ -1381,6 +1469,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 23 && getenv("FE_NO_PLANE1")) continue;
     if (v.priority == 26 && getenv("FE_NO_PAIR")) continue;
     if (v.priority == 27 && getenv("FE_NO_HEXQ1")) continue;
+    if (v.priority == 28 && getenv("FE_NO_HEXQ2")) continue;
     if (v.priority == 6 && getenv("FE_NO_VTX")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments

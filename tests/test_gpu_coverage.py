@@ -85,6 +85,8 @@ ALTERNATIVES = [
     ("neohookean", "tetrahedron", 2, {}, "quad_vertex_grad"),
     ("neohookean", "tetrahedron", 2, {"FE_NO_VTX": "1"}, "quad_const"),
     ("neohookean_tangent", "tetrahedron", 2, {"FE_NO_VTX": "1"}, "quad_const"),
+    ("elasticity_lame", "quadrilateral", 3, {"FE_PAIR_CFG": "1"}, "component_pair"),
+    ("elasticity_lame", "quadrilateral", 4, {"FE_PAIR_CFG": "1"}, "component_pair"),
 ]
 
 
@@ -95,3 +97,37 @@ def test_alternative_kernel_families_match_oracle(monkeypatch, form, cell, k, en
     got, err = _run(form, cell, k, False)
     assert got == kernel
     assert err <= 1e-12, (got, err)
+
+
+# C3 uses the (k+1)-point Gauss rule, for which dedicated kernels exist
+C3_KERNELS = [
+    ("C3-Q1", {}, "sum_factorised_q1"),
+    ("C3-Q2", {}, "sum_factorised_q2"),
+    ("C3-Q2", {"FE_NO_HEXQ2": "1"}, "sum_factorised_plane_t"),
+    ("C3-Q2", {"FE_NO_HEXQ2": "1", "FE_NO_PLANE1": "1"}, "sum_factorised"),
+    ("C3-Q3", {}, "sum_factorised_plane"),
+    ("C3-Q3", {"FE_NO_PLANE": "1"}, "sum_factorised"),
+]
+
+
+@pytest.mark.parametrize("name,env,kernel", C3_KERNELS)
+def test_c3_rule_kernels_match_oracle(monkeypatch, name, env, kernel):
+    from paper_1903_08243_b200 import configs as C
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    prob = C.build_problem(C.get_config(name, 5), seed=3)
+    h = fe.compile_and_load(fe.emit_for(prob.spec, fe.Target(), prob.rule))
+    assert h.info["kernel"] == kernel
+    out = np.zeros(prob.ndofs)
+    b = fe.make_bindings(prob.mesh, prob.dofmap, prob.u, out, prob.mu, prob.lam, state=prob.state)
+    h(0, prob.mesh.ncells, b)
+    P = fo.Problem(prob.spec.form, prob.spec.cell.kind, prob.spec.element.degree,
+                   prob.rule.exactness_degree, prob.spec.params)
+    ref = fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof, prob.u,
+                      prob.mu, prob.lam, state=prob.state)
+    assert fo.rel_l2(out, ref) <= 1e-12
+    # ragged sub-range with accumulate semantics: [7, 101) on top of the full apply
+    h(7, 101, b)
+    ref2 = ref + fo.assemble(P, prob.mesh.coords, prob.mesh.cell2vert, prob.dofmap.cell2dof,
+                             prob.u, prob.mu, prob.lam, start=7, end=101, state=prob.state)
+    assert fo.rel_l2(out, ref2) <= 1e-12
