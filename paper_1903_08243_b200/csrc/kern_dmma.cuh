@@ -183,6 +183,9 @@ __global__ void __launch_bounds__(256, MINB) dmma_et_kernel(DmmaParams p) {
 // 25 + 42 = 67 (105).
 // ---------------------------------------------------------------------------
 
+#ifndef FE_MODAL_SPLIT
+#define FE_MODAL_SPLIT 1
+#endif
 template <int DIM, int NMODE>
 struct ModalShape {
   static constexpr int tuples(int nj) { return (2 * nj) / DIM; }
@@ -191,9 +194,28 @@ struct ModalShape {
     while (4 * tuples(nj) < NMODE) ++nj;
     return nj;
   }
-  static constexpr int NJ = pick();             // stage-1 column tiles
-  static constexpr int TPL = tuples(NJ);        // mode tuples per lane
-  static constexpr int NSTEP = DIM * TPL;       // stage-2 modal k-steps (one per lane slot)
+  // SPLIT (P3: 10 modes x 3 directions = 30 columns): whole tuples need 5
+  // column tiles (4 lanes x 3 tuples = 12 mode slots for 10 modes, 25 + 42
+  // DMMA per 8 cells).  Four tiles suffice when the last two modes are split
+  // over lane pairs -- each lane owns 8 slots: two whole tuples (modes
+  // 2c, 2c+1) and two leftovers; mode 8 + c/2 puts directions 0, 1 in the
+  // even lane and direction 2 in the odd lane's first leftover, and the
+  // combine exchanges those three values with one shuffle pair: 20 + 39 DMMA.
+  static constexpr bool SPLIT = FE_MODAL_SPLIT && DIM == 3 && NMODE == 10;
+  static constexpr int NJ = SPLIT ? 4 : pick();        // stage-1 column tiles
+  static constexpr int TPL = SPLIT ? 2 : tuples(NJ);   // whole mode tuples per lane
+  static constexpr int NSTEP = SPLIT ? 2 * NJ : DIM * TPL;  // stage-2 modal k-steps (one per lane slot)
+  // (mode, direction) held by slot li of lane group c (mode -1: empty slot)
+  static constexpr int mode_of(int c, int li) {
+    if (li < DIM * TPL) return c * TPL + li / DIM < NMODE ? c * TPL + li / DIM : -1;
+    if (!SPLIT || li >= 2 * NJ) return -1;
+    const int e = li - DIM * TPL;
+    return ((c & 1) == 0 || e == 0) ? 4 * TPL + (c >> 1) : -1;
+  }
+  static constexpr int dir_of(int c, int li) {
+    if (li < DIM * TPL) return li % DIM;
+    return (c & 1) == 0 ? li - DIM * TPL : 2;
+  }
 };
 
 template <int FORM, int DIM, int ND, int NMODE, int NT, int MINB, int BLK = 256>
@@ -316,6 +338,19 @@ __global__ void __launch_bounds__(BLK, MINB) dmma_modal_kernel(DmmaParams p) {
           for (int b = 0; b < DIM; ++b) h = fma(K[a][b], gv[b], h);
           acc1[nt][(DIM * s + a) / 2][(DIM * s + a) % 2] = h;
         }
+      }
+      if constexpr (MS::SPLIT) {
+        // modes 8, 9: directions (0, 1) in the even lane's leftover slots, 2 in the odd lane's
+        double& a6 = acc1[nt][NJ - 1][0];
+        double& a7 = acc1[nt][NJ - 1][1];
+        const double o6 = __shfl_xor_sync(0xffffffffu, a6, 1), o7 = __shfl_xor_sync(0xffffffffu, a7, 1);
+        const bool odd = c4 & 1;
+        const double gv0 = odd ? o6 : a6, gv1 = odd ? o7 : a7, gv2 = odd ? a6 : o6;
+        const double h0 = fma(K[0][2], gv2, fma(K[0][1], gv1, K[0][0] * gv0));
+        const double h1 = fma(K[1][2], gv2, fma(K[1][1], gv1, K[1][0] * gv0));
+        const double h2 = fma(K[2][2], gv2, fma(K[2][1], gv1, K[2][0] * gv0));
+        a6 = odd ? h2 : h0;
+        a7 = odd ? 0.0 : h1;
       }
       if constexpr (MASS) {
 #pragma unroll

@@ -42,8 +42,8 @@
 #define FE_PLANE_MONO 1   // monomial trilinear geometry (round 2)
 #endif
 #ifndef FE_PLANE_RCP
-#define FE_PLANE_RCP 0    // 1: MUFU-seeded reciprocal instead of the IEEE division
-#endif
+#define FE_PLANE_RCP 1    // MUFU-seeded reciprocal instead of the IEEE division at P = 4 (C3-Q3 224.2 -> 222.2 us;
+#endif                    // slower at P = 5: 529 -> 565 us, profiles/r02/ab_plane_rcp.txt)
 
 namespace fe {
 
@@ -334,7 +334,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wac * p.w[b]) * recip<(FE_PLANE_RCP != 0)>(fabs(det));
+          const double s = (wac * p.w[b]) * recip<(FE_PLANE_RCP != 0) && P == 4>(fabs(det));
           // v = adj^T g (= det * physical gradient), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;
@@ -400,6 +400,6 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #define FE_PLANE_MINB 1
 #endif
 #ifndef FE_PLANE_WARPS
-#define FE_PLANE_WARPS 4
+#define FE_PLANE_WARPS 8   // C3-Q3 222 -> 212 us, C3-Q4 529 -> 521 us vs 4 warps (profiles/r02/ab_plane_warps.txt)
 #endif
 #define FE_PLANE_VARIANTS PLV(3, 4, 4, FE_PLANE_WARPS, FE_PLANE_MINB, 2), PLV(4, 5, 5, FE_PLANE_WARPS, FE_PLANE_MINB, 1),

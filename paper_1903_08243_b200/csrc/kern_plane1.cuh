@@ -348,7 +348,7 @@ plane1_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wab * p.w[c]) * recip<(FE_PLANE_RCP != 0)>(fabs(det));
+          const double s = (wab * p.w[c]) * recip<false>(fabs(det));
           // v = adj^T g (physical gradient * det), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;

@@ -100,6 +100,9 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 #ifndef FE_TK_MONO
 #define FE_TK_MONO 1    // monomial trilinear geometry (round 2)
 #endif
+#ifndef FE_TK_SYM
+#define FE_TK_SYM 1     // mirror-symmetric table reads (round 2)
+#endif
 #ifndef FE_TK_ASYNC
 #define FE_TK_ASYNC 0   // 1: cp.async gather pipeline (no prefetch registers)
 #endif
@@ -168,6 +171,12 @@ struct TensorLayout {
 // MINB >= 1000: the same with the cp.async gather pipeline (FE_TK_ASYNC
 // per variant: C3-Q5 0.38 -> 0.45 of its roof; slower where its extra
 // shared memory costs occupancy, profiles/r02/ab_tensor_async.txt)
+// mirror-symmetric table reads, where measured faster (profiles/r02/ab_tensor_sym.txt):
+// (P, Q) = (4, 5), whose full tables overflow the uniform registers into vector
+// registers + R2UR (C4-hex-Q3 1.269 -> 1.244 ms); neutral to slower elsewhere,
+// and at Q = 7 halving the tables tips ptxas from in-loop LDCU loads to
+// hoisting them into vector registers (459 R2UR, 1.68 -> 2.29 ms)
+template <int P, int Q> constexpr bool tensor_sym() { return FE_TK_SYM != 0 && P == 4 && Q == 5; }
 template <int MINB> constexpr bool tensor_async() { return MINB >= 1000 || FE_TK_ASYNC; }
 template <int MINB> constexpr int tensor_block() {
   constexpr int m = MINB % 1000;
@@ -205,6 +214,18 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   const int64_t cs = p.mesh.nc_stride;
   const int ncell = p.end - p.start;
   const int nbatch = (ncell + CPB - 1) / CPB;
+  // FE_TK_SYM: the 1D tables are mirror-symmetric about 1/2 (verified at plan
+  // time): B[q][i] = B[Q-1-q][P-1-i], D[q][i] = -D[Q-1-q][P-1-i].  Reading
+  // only the lower half halves the distinct constants of the persistent
+  // loop: sm_100a feeds constant operands through ~80 uniform registers, and
+  // when the tables do not fit ptxas parks them in vector registers and moves
+  // them back with R2UR inside the loop (C4-hex-Q3: 303 R2UR + 139 MOV.SPILL
+  // per 1598 FP64 instructions before this).
+  constexpr bool SYM = tensor_sym<P, Q>();
+  auto TB = [&](int q, int i) { return (!SYM || 2 * q < Q) ? p.B[q][i] : p.B[Q - 1 - q][P - 1 - i]; };
+  auto TD = [&](int q, int i) { return (!SYM || 2 * q < Q) ? p.D[q][i] : -p.D[Q - 1 - q][P - 1 - i]; };
+  auto TX = [&](int q) { return (!SYM || 2 * q < Q) ? p.x[q] : 1.0 - p.x[Q - 1 - q]; };
+  auto TW = [&](int q) { return (!SYM || 2 * q < Q) ? p.w[q] : p.w[Q - 1 - q]; };
 
   // ---- prefetch pipeline: map indices two batches ahead, data one ahead ----
   constexpr int RX = L::RX, RM = L::RM;
@@ -422,8 +443,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             double z0 = 0.0, z1 = 0.0;
 #pragma unroll
             for (int k = 0; k < P; ++k) {
-              z0 = fma(p.B[c][k], pen[k], z0);
-              if constexpr (!COLLOC) z1 = fma(p.D[c][k], pen[k], z1);
+              z0 = fma(TB(c, k), pen[k], z0);
+              if constexpr (!COLLOC) z1 = fma(TD(c, k), pen[k], z1);
             }
             s1[j * L::SZ + c * P + i] = z0;
             if constexpr (!COLLOC) s1[P * L::SZ + j * L::SZ + c * P + i] = z1;
@@ -444,10 +465,10 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             double y0 = 0.0, y1 = 0.0, y2 = 0.0;
 #pragma unroll
             for (int j = 0; j < P; ++j) {
-              y0 = fma(p.B[b][j], p0[j], y0);
+              y0 = fma(TB(b, j), p0[j], y0);
               if constexpr (!COLLOC) {
-                y1 = fma(p.D[b][j], p0[j], y1);
-                y2 = fma(p.B[b][j], p1[j], y2);
+                y1 = fma(TD(b, j), p0[j], y1);
+                y2 = fma(TB(b, j), p1[j], y2);
               }
             }
             s2[i * L::SY + c * Q + b] = y0;
@@ -469,7 +490,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             for (int a = 0; a < Q; ++a) {
               double s = 0.0;
 #pragma unroll
-              for (int i = 0; i < P; ++i) s = fma(p.B[a][i], q0[i], s);
+              for (int i = 0; i < P; ++i) s = fma(TB(a, i), q0[i], s);
               uq[a] = s;
               s1[a * QQ + t] = s;
             }
@@ -515,9 +536,9 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               double g0 = 0.0, g1 = 0.0, g2 = 0.0;
 #pragma unroll
               for (int i = 0; i < P; ++i) {
-                g0 = fma(p.D[a][i], q0[i], g0);
-                g1 = fma(p.B[a][i], q1[i], g1);
-                g2 = fma(p.B[a][i], q2[i], g2);
+                g0 = fma(TD(a, i), q0[i], g0);
+                g1 = fma(TB(a, i), q1[i], g1);
+                g2 = fma(TB(a, i), q2[i], g2);
               }
               g[comp][0][a] = g0;
               g[comp][1][a] = g1;
@@ -538,8 +559,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             double y0 = 0.0, y1 = 0.0;
 #pragma unroll
             for (int j = 0; j < P; ++j) {
-              y0 = fma(p.B[b][j], pen[j], y0);
-              y1 = fma(p.D[b][j], pen[j], y1);
+              y0 = fma(TB(b, j), pen[j], y0);
+              y1 = fma(TD(b, j), pen[j], y1);
             }
             s2[b * L::S2 + i] = y0;
             s2[Q * L::S2 + b * L::S2 + i] = y1;
@@ -559,8 +580,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             double g0 = 0.0, g1 = 0.0;
 #pragma unroll
             for (int i = 0; i < P; ++i) {
-              g0 = fma(p.D[a][i], q0[i], g0);
-              g1 = fma(p.B[a][i], q1[i], g1);
+              g0 = fma(TD(a, i), q0[i], g0);
+              g1 = fma(TB(a, i), q1[i], g1);
             }
             g[comp][0][a] = g0;
             g[comp][1][a] = g1;
@@ -630,7 +651,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       }
 #pragma unroll
       for (int a = 0; a < Q; ++a) {
-        const double xi = p.x[a];
+        const double xi = TX(a);
         double J[DIM][DIM], Ji[DIM][DIM];
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
@@ -647,7 +668,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         // absorbs both 1/det factors (no inverse formed)
         constexpr bool ADJ = TK_ADJ && linear_grad_form(FORM);
         const double det = ADJ ? det_adj<DIM>(J, Ji) : det_inv<DIM, !DIRECT>(J, Ji);
-        const double tw = ADJ ? (p.w[a] * wbc) * recip<!DIRECT>(fabs(det)) : (p.w[a] * wbc) * fabs(det);
+        const double tw = ADJ ? (TW(a) * wbc) * recip<!DIRECT>(fabs(det)) : (TW(a) * wbc) * fabs(det);
         double mu = p.p0, lam = p.p1;
         if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
           mu = fma(xi, dm, m0);
@@ -703,7 +724,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             for (int i = 0; i < P; ++i) {
               double s = 0.0;
 #pragma unroll
-              for (int a = 0; a < Q; ++a) s = fma(p.B[a][i], V[a], s);
+              for (int a = 0; a < Q; ++a) s = fma(TB(a, i), V[a], s);
               s2[b * L::SA + c * P + i] = s;                            // A[b][c][i]
             }
           }
@@ -718,7 +739,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             for (int j = 0; j < P; ++j) {
               double s = 0.0;
 #pragma unroll
-              for (int b = 0; b < Q; ++b) s = fma(p.B[b][j], a0[b], s);
+              for (int b = 0; b < Q; ++b) s = fma(TB(b, j), a0[b], s);
               s1[c * L::SW + j * P + i] = s;
             }
           }
@@ -732,7 +753,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             for (int k = 0; k < P; ++k) {
               double s = 0.0;
 #pragma unroll
-              for (int c = 0; c < Q; ++c) s = fma(p.B[c][k], w1[c], s);
+              for (int c = 0; c < Q; ++c) s = fma(TB(c, k), w1[c], s);
               scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
             }
           }
@@ -746,9 +767,9 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
               for (int a = 0; a < Q; ++a) {
-                a0 = fma(p.D[a][i], g[comp][0][a], a0);
-                a1 = fma(p.B[a][i], g[comp][1][a], a1);
-                a2 = fma(p.B[a][i], g[comp][2][a], a2);
+                a0 = fma(TD(a, i), g[comp][0][a], a0);
+                a1 = fma(TB(a, i), g[comp][1][a], a1);
+                a2 = fma(TB(a, i), g[comp][2][a], a2);
               }
               s2[b * L::SA + c * P + i] = a0;
               s2[Q * L::SA + b * L::SA + c * P + i] = a1;
@@ -771,9 +792,9 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               double w1 = 0.0, w2 = 0.0;
 #pragma unroll
               for (int b = 0; b < Q; ++b) {
-                w1 = fma(p.B[b][j], a0[b], w1);
-                w1 = fma(p.D[b][j], a1[b], w1);
-                w2 = fma(p.B[b][j], a2[b], w2);
+                w1 = fma(TB(b, j), a0[b], w1);
+                w1 = fma(TD(b, j), a1[b], w1);
+                w2 = fma(TB(b, j), a2[b], w2);
               }
               s1[c * L::SW + j * P + i] = w1;
               s1[Q * L::SW + c * L::SW + j * P + i] = w2;
@@ -793,8 +814,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               double s = 0.0;
 #pragma unroll
               for (int c = 0; c < Q; ++c) {
-                s = fma(p.B[c][k], w1[c], s);
-                s = fma(p.D[c][k], w2[c], s);
+                s = fma(TB(c, k), w1[c], s);
+                s = fma(TD(c, k), w2[c], s);
               }
               scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
             }
@@ -809,8 +830,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
             for (int a = 0; a < Q; ++a) {
-              a0 = fma(p.D[a][i], g[comp][0][a], a0);
-              a1 = fma(p.B[a][i], g[comp][1][a], a1);
+              a0 = fma(TD(a, i), g[comp][0][a], a0);
+              a1 = fma(TB(a, i), g[comp][1][a], a1);
             }
             s2[b * L::S2 + i] = a0;
             s2[Q * L::S2 + b * L::S2 + i] = a1;
@@ -830,8 +851,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             double s = 0.0;
 #pragma unroll
             for (int b = 0; b < Q; ++b) {
-              s = fma(p.B[b][j], a0[b], s);
-              s = fma(p.D[b][j], a1[b], s);
+              s = fma(TB(b, j), a0[b], s);
+              s = fma(TD(b, j), a1[b], s);
             }
             scatter_add(p.y, (int64_t)VS * __ldg(mrow + j * P + i) + comp, s);
           }

@@ -772,10 +772,10 @@ int dmma_modal_prepare(fe_plan* p) {
   for (double w : p->qw_aux)
     if (!(w >= 0.0)) return fail(FE_EINVAL, "stiffness modes need non-negative weights");
   // G[r][i][a] = sqrt(w_r) dphi_aux[r][i][a]; column (lane-group c, slot li)
-  // holds mode r = c * TPL + li / DIM, direction a = li % DIM
+  // holds mode MS::mode_of(c, li), direction MS::dir_of(c, li)
   auto G = [&](int c, int li, int dof) -> double {
-    const int r = c * TPL + li / DIM, a = li % DIM;
-    if (li >= DIM * TPL || r >= NMODE || dof >= ND) return 0.0;
+    const int r = MS::mode_of(c, li), a = MS::dir_of(c, li);
+    if (r < 0 || r >= NMODE || dof >= ND) return 0.0;
     return std::sqrt(p->qw_aux[r]) * p->dphi_aux[((size_t)r * ND + dof) * DIM + a];
   };
   std::vector<double> S;
@@ -883,6 +883,17 @@ int tensor_prepare(fe_plan* p) {
   if (int rc = fill_tensor_tables<Q, P>(p, hp)) {
     delete hp;
     return rc;
+  }
+  // the kernel reads the mirror-symmetric half of the 1D tables
+  for (int q = 0; tensor_sym<P, Q>() && q < Q; ++q) {
+    bool ok = std::fabs(hp->x[q] - (1.0 - hp->x[Q - 1 - q])) <= 1e-13 && std::fabs(hp->w[q] - hp->w[Q - 1 - q]) <= 1e-13;
+    for (int i = 0; i < P; ++i)
+      ok = ok && std::fabs(hp->B[q][i] - hp->B[Q - 1 - q][P - 1 - i]) <= 1e-12 &&
+           std::fabs(hp->D[q][i] + hp->D[Q - 1 - q][P - 1 - i]) <= 1e-11;
+    if (!ok) {
+      delete hp;
+      return fail(FE_EUNSUPPORTED, "sum-factorised kernel needs mirror-symmetric 1D tables");
+    }
   }
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
