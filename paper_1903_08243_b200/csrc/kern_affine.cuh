@@ -458,6 +458,87 @@ macro_split_kernel(const __grid_constant__ SplitParams<NQS, ND, DIM> p, const in
   }
 }
 
+// Pipelined variant (round 2, P1 analytic case): macro_split_kernel above
+// prefetches only the macro-dof ids; the coordinates and u values they point
+// to are still a dependent DRAM round trip at the top of every macro-cell
+// (ncu: long_scoreboard 4.1 of 7.4 stall cycles per instruction, FP64 pipe
+// 40%).  Here that second hop is taken off the critical path too: while
+// macro-cell n computes, cp.async (LDGSTS) copies the NU vertex coordinates
+// and u values of macro-cell n+1 into a thread-private shared-memory column
+// (double-buffered, layout [slot][thread]: conflict-free, no barriers) and the
+// ids of macro-cell n+2 are loaded into registers.  The P1 case has no table
+// constants, so the persistent loop costs no uniform registers.
+template <int FORM, int DIM, int ND, class PAT>
+__global__ void __launch_bounds__(128, FE_MACRO_MINB)
+macro_pipe_kernel(const __grid_constant__ SplitParams<1, ND, DIM> p, const int32_t* __restrict__ corner,
+                  int64_t mstride, int32_t m0, int32_t m1) {
+  static_assert(PAT::ND == ND && ND == DIM + 1, "P1 macro pattern");
+  constexpr int NU = PAT::NU, MC = PAT::MC, SL = NU * (DIM + 1);   // slots per thread and buffer
+  extern __shared__ double smem_mp[];
+  double* const sb = smem_mp + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  int m = m0 + blockIdx.x * blockDim.x + threadIdx.x;
+  auto issue = [&](const int (&id)[NU], int buf) {
+    double* d = sb + buf * SL * 128;
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      const double* x = p.mesh.coords + (int64_t)id[k] * CStride<DIM>::value;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) cp_async8(d + (k * (DIM + 1) + a) * 128, x + a);
+      cp_async8(d + (k * (DIM + 1) + DIM) * 128, p.u + id[k]);
+    }
+  };
+  int cur[NU], nxt[NU];
+#pragma unroll
+  for (int k = 0; k < NU; ++k) cur[k] = m < m1 ? __ldg(corner + k * mstride + m) : 0;
+  if (m < m1) issue(cur, 0);
+  cp_commit();
+#pragma unroll
+  for (int k = 0; k < NU; ++k) nxt[k] = m + stride < m1 ? __ldg(corner + k * mstride + m + stride) : 0;
+  int buf = 0;
+#pragma unroll 1
+  for (; m < m1; m += stride) {
+    if (m + stride < m1) issue(nxt, buf ^ 1);     // next macro-cell's data
+    cp_commit();
+    int nn[NU];                                   // ids two ahead
+#pragma unroll
+    for (int k = 0; k < NU; ++k) nn[k] = m + 2 * stride < m1 ? __ldg(corner + k * mstride + m + 2 * stride) : 0;
+    cp_wait_group<1>();                           // this macro-cell's data has landed
+    const double* d = sb + buf * SL * 128;
+    double X[NU][DIM], w[NU], yl[NU];
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) X[k][a] = d[(k * (DIM + 1) + a) * 128];
+      w[k] = d[(k * (DIM + 1) + DIM) * 128];
+      yl[k] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < MC; ++t) {
+      double Xt[DIM + 1][DIM], wt[ND], yt[ND];
+#pragma unroll
+      for (int i = 0; i < ND; ++i) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) Xt[i][a] = X[PAT::at(t, i)][a];
+        wt[i] = w[PAT::at(t, i)];
+      }
+      p1_simplex_compute<FORM, DIM>(Xt, wt, yt);
+#pragma unroll
+      for (int i = 0; i < ND; ++i) yl[PAT::at(t, i)] += yt[i];
+    }
+    griddep_wait();
+#pragma unroll
+    for (int k = 0; k < NU; ++k) scatter_add(p.y, cur[k], yl[k]);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+      cur[k] = nxt[k];
+      nxt[k] = nn[k];
+    }
+    buf ^= 1;
+  }
+  cp_wait_all();
+}
+
 // ---------------------------------------------------------------------------
 // Patch-aggregated variant (low degree: C1, C2-P1/P2).  At these intensities
 // the global FP64 RED stream (one per cell-dof pair: 6.3M for P1, 15.7M for

@@ -24,6 +24,9 @@
 
 namespace fe {
 
+#ifndef FE_PAIR_RELOAD
+#define FE_PAIR_RELOAD 0   // 1: re-read the dof ids for the scatter instead of holding them in registers
+#endif
 #ifndef FE_PAIR_BLOCK
 #define FE_PAIR_BLOCK 32  // one warp per CTA: measured best (profiles/r01/sweep_warps.txt)
 #endif
@@ -140,7 +143,8 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
   for (int j = 0; j < P; ++j)
 #pragma unroll
-    for (int i = 0; i < P; ++i) scatter_add(p.y, 2 * (int64_t)dof[j * P + i] + c, y[j][i]);
+    for (int i = 0; i < P; ++i)
+      scatter_add(p.y, 2 * (int64_t)(FE_PAIR_RELOAD ? __ldg(mrow + j * P + i) : dof[j * P + i]) + c, y[j][i]);
 }
 
 

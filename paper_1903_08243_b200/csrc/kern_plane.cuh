@@ -402,4 +402,10 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #ifndef FE_PLANE_WARPS
 #define FE_PLANE_WARPS 8   // C3-Q3 222 -> 212 us, C3-Q4 529 -> 521 us vs 4 warps (profiles/r02/ab_plane_warps.txt)
 #endif
-#define FE_PLANE_VARIANTS PLV(3, 4, 4, FE_PLANE_WARPS, FE_PLANE_MINB, 2), PLV(4, 5, 5, FE_PLANE_WARPS, FE_PLANE_MINB, 1),
+#ifndef FE_PLANE_CU4
+#define FE_PLANE_CU4 2
+#endif
+#ifndef FE_PLANE_CU5
+#define FE_PLANE_CU5 1
+#endif
+#define FE_PLANE_VARIANTS PLV(3, 4, 4, FE_PLANE_WARPS, FE_PLANE_MINB, FE_PLANE_CU4), PLV(4, 5, 5, FE_PLANE_WARPS, FE_PLANE_MINB, FE_PLANE_CU5),

@@ -103,6 +103,9 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 #ifndef FE_TK_SYM
 #define FE_TK_SYM 1     // mirror-symmetric table reads (round 2)
 #endif
+#ifndef FE_TK_FLATZ
+#define FE_TK_FLATZ 0   // 1: one z stage for all components of a vector form; measured neutral
+#endif                  // (C4-hex-Q2 0.456 -> 0.460 ms, C4-hex-Q3 1.244 -> 1.239 ms, profiles/r02/ab_tensor_flatz.txt)
 #ifndef FE_TK_ASYNC
 #define FE_TK_ASYNC 0   // 1: cp.async gather pipeline (no prefetch registers)
 #endif
@@ -139,7 +142,12 @@ struct TensorLayout {
   static constexpr int S2 = P + ((17 - P) % 16 + 16) % 16;
   static constexpr int NZ = COLLOC ? 1 : 2;
   static constexpr int NY = COLLOC ? 1 : 3;
-  static constexpr int R1 = DIM == 3 ? cmax3(NZ * P * SZ, 2 * Q * Q * Q, 2 * Q * SW) : 0;
+  // FLATZ (vector forms, direct algorithm): the z stages of all VS components run
+  // as one stage over VS P^2 pencils, so Z and W of every component are resident
+  static constexpr bool FLATZ = FE_TK_FLATZ && DIM == 3 && VS > 1 && !COLLOC;
+  static constexpr int ZS = NZ * P * SZ;                    // Z region of one component
+  static constexpr int WS = 2 * Q * SW;                     // W region of one component
+  static constexpr int R1 = DIM == 3 ? cmax3((FLATZ ? VS : 1) * ZS, 2 * Q * Q * Q, (FLATZ ? VS : 1) * WS) : 0;
   static constexpr int R2 = DIM == 3 ? cmax3(NY * P * SY, 3 * Q * SA, 0) : 2 * Q * S2;
   // per-cell region
   static constexpr int U = 0;
@@ -428,29 +436,45 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #endif
     // ---- forward: reference gradients at the points of this thread's x-pencil
     double g[VS][DIM][Q];
+    constexpr bool FLATZ = L::FLATZ;
+    // z: pencil (i, j) over k -> Z0 = B u (Z1 = D u: direct)      Z[j][c][i]
+    auto z_stage = [&](const double* uc, double* zb, int e) {
+      const int i = e % P, j = e / P;
+      double pen[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) pen[k] = uc[k * P * P + e];
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          z0 = fma(TB(c, k), pen[k], z0);
+          if constexpr (!COLLOC) z1 = fma(TD(c, k), pen[k], z1);
+        }
+        zb[j * L::SZ + c * P + i] = z0;
+        if constexpr (!COLLOC) zb[P * L::SZ + j * L::SZ + c * P + i] = z1;
+      }
+    };
+    if constexpr (FLATZ) {
+      // all VS P^2 pencils of the cell as one stage: ceil(VS P^2 / TS) rounds of the
+      // team instead of VS rounds with P^2 of its Q^2 threads busy
+#pragma unroll
+      for (int r = 0; r < (VS * P * P + TS - 1) / TS; ++r) {
+        const int it = t + r * TS;
+        if (active && it < VS * P * P) z_stage(sU + (it / (P * P)) * ND, s1 + (it / (P * P)) * L::ZS, it % (P * P));
+      }
+      team_sync();
+    }
 #pragma unroll
     for (int comp = 0; comp < VS; ++comp) {
       const double* uc = sU + comp * ND;
       if constexpr (DIM == 3) {
-        // z: pencil (i, j) over k -> Z0 = B u (Z1 = D u: direct)      Z[j][c][i]
-        if (active && t < P * P) {
-          const int i = t % P, j = t / P;
-          double pen[P];
-#pragma unroll
-          for (int k = 0; k < P; ++k) pen[k] = uc[k * P * P + t];
-#pragma unroll
-          for (int c = 0; c < Q; ++c) {
-            double z0 = 0.0, z1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-              z0 = fma(TB(c, k), pen[k], z0);
-              if constexpr (!COLLOC) z1 = fma(TD(c, k), pen[k], z1);
-            }
-            s1[j * L::SZ + c * P + i] = z0;
-            if constexpr (!COLLOC) s1[P * L::SZ + j * L::SZ + c * P + i] = z1;
-          }
+        double* const s1f = s1;   // this component's Z region
+        double* s1 = s1f + (FLATZ ? comp * L::ZS : 0);
+        if constexpr (!FLATZ) {
+          if (active && t < P * P) z_stage(uc, s1, t);
+          team_sync();
         }
-        team_sync();
         // y: pencil (i, c) over j -> Y0 = B Z0 (Y1 = D Z0, Y2 = B Z1)    Y[i][c][b]
         if (active && t < Q * P) {
           const int i = t % P, c = t / P;
@@ -692,6 +716,25 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     // ---- transposed chain and scatter, one component at a time ------------
     griddep_wait();   // y zero-filled by the preceding kernel (PDL overwrite path)
     const int32_t* mrow = p.maplex + (int64_t)cell * ND;
+    // z^T: pencil (i, j) = e over c: y_k = B^T W1 + D^T W2; scatter      W[c][j][i]
+    auto zt_stage = [&](const double* wb, int e, int comp) {
+      double w1[Q], w2[Q];
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        w1[c] = wb[c * L::SW + e];
+        w2[c] = wb[Q * L::SW + c * L::SW + e];
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          s = fma(TB(c, k), w1[c], s);
+          s = fma(TD(c, k), w2[c], s);
+        }
+        scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + e) + comp, s);
+      }
+    };
 #pragma unroll
     for (int comp = 0; comp < VS; ++comp) {
       if constexpr (DIM == 3) {
@@ -759,6 +802,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           }
           team_sync();
         } else {
+          double* const sw = s1 + (L::FLATZ ? comp * L::WS : 0);   // this component's W region
           // x^T: thread (b, c): A0 = D^T F0, A1 = B^T F1, A2 = B^T F2 over i  A[b][c][i]
           if (active) {
             const int b = t % Q, c = t / Q;
@@ -796,31 +840,15 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
                 w1 = fma(TD(b, j), a1[b], w1);
                 w2 = fma(TB(b, j), a2[b], w2);
               }
-              s1[c * L::SW + j * P + i] = w1;
-              s1[Q * L::SW + c * L::SW + j * P + i] = w2;
+              sw[c * L::SW + j * P + i] = w1;
+              sw[Q * L::SW + c * L::SW + j * P + i] = w2;
             }
           }
           team_sync();
-          // z^T: pencil (i, j) over c: y_k = B^T W1 + D^T W2; scatter
-          if (active && t < P * P) {
-            double w1[Q], w2[Q];
-#pragma unroll
-            for (int c = 0; c < Q; ++c) {
-              w1[c] = s1[c * L::SW + t];
-              w2[c] = s1[Q * L::SW + c * L::SW + t];
-            }
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-              double s = 0.0;
-#pragma unroll
-              for (int c = 0; c < Q; ++c) {
-                s = fma(TB(c, k), w1[c], s);
-                s = fma(TD(c, k), w2[c], s);
-              }
-              scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + t) + comp, s);
-            }
+          if constexpr (!L::FLATZ) {
+            if (active && t < P * P) zt_stage(sw, t, comp);
+            team_sync();
           }
-          team_sync();
         }
       } else {
         if (active) {
@@ -859,6 +887,14 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         }
         team_sync();
       }
+    }
+    if constexpr (L::FLATZ) {
+#pragma unroll
+      for (int r = 0; r < (VS * P * P + TS - 1) / TS; ++r) {
+        const int it = t + r * TS;
+        if (active && it < VS * P * P) zt_stage(s1 + (it / (P * P)) * L::WS, it % (P * P), it / (P * P));
+      }
+      team_sync();
     }
     // the next batch's data (loads issued at the top of this iteration)
     if constexpr (ASYNC) {

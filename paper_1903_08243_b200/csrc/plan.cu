@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <omp.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -630,7 +631,24 @@ int split_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
           launch_op(kfn, nb, 128, 0, s, *hp, p->d_macro, p->macro_stride, m0, m1);
         };
         if constexpr (ND == 4) {
-          if (p->p1_analytic)
+          // opt-in (FE_MACRO_PIPE=1): measured slower, 23.5 vs 19.5 us (profiles/r02/ab_macro_pipe.txt)
+          static const bool pipe = getenv("FE_MACRO_PIPE") != nullptr;
+          if (p->p1_analytic && pipe && waves > 0) {
+            // cp.async-pipelined macro kernel: thread-private shared-memory columns, 2 buffers
+            auto kfn = macro_pipe_kernel<FORM, DIM, ND, PAT>;
+            constexpr size_t smem = 2 * (size_t)PAT::NU * (DIM + 1) * 128 * sizeof(double);
+            static bool attr_done = false;
+            if (!attr_done) {
+              CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+              attr_done = true;
+            }
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 128, smem);
+            nb = std::min(nb, std::max(1, waves * sms * per_sm));
+            launch_op(kfn, nb, 128, smem, s, *hp, p->d_macro, p->macro_stride, m0, m1);
+          } else if (p->p1_analytic)
             launch(macro_split_kernel<FORM, DIM, ND, NQS, PAT, true>);
           else
             launch(macro_split_kernel<FORM, DIM, ND, NQS, PAT>);
@@ -1030,12 +1048,13 @@ int hexq1_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   hp->start = start;
   hp->end = end;
   const int n = end - start;
-  const unsigned g = (n + 127) / 128;
+  static const int blk = getenv("FE_HEXQ1_BLOCK") ? atoi(getenv("FE_HEXQ1_BLOCK")) : 128;  // 32/64/128
+  const unsigned g = (n + blk - 1) / blk;
   switch (p->dmma_cfg) {
-    case 1: launch_op(hexq1_lap_kernel<1>, g, 128, 0, s, *hp); break;
-    case 2: launch_op(hexq1_lap_kernel<2>, g, 128, 0, s, *hp); break;
-    case 4: launch_op(hexq1_lap_kernel<4>, g, 128, 0, s, *hp); break;
-    default: launch_op(hexq1_lap_kernel<3>, g, 128, 0, s, *hp); break;
+    case 1: launch_op(hexq1_lap_kernel<1>, g, blk, 0, s, *hp); break;
+    case 2: launch_op(hexq1_lap_kernel<2>, g, blk, 0, s, *hp); break;
+    case 4: launch_op(hexq1_lap_kernel<4>, g, blk, 0, s, *hp); break;
+    default: launch_op(hexq1_lap_kernel<3>, g, blk, 0, s, *hp); break;
   }
   CUDA_TRY(cudaGetLastError());
   return FE_OK;
@@ -2060,10 +2079,15 @@ static int wrap_host_impl(fe_plan* p, int32_t start, int32_t end, double* dat0, 
     const int c = order[oc];
     const size_t a = (size_t)p->ybound[c], b = (size_t)p->ybound[c + 1];
     int nonzero = 0;
-    if (b > a) {
+    // experiment switches: FE_HOST_ASSUME_ZERO=1 skips the scan (measures its cost; breaks
+    // the accumulate semantics), FE_HOST_SCAN_THREADS = OpenMP threads of one call's scan
+    static const bool assume_zero = getenv("FE_HOST_ASSUME_ZERO") != nullptr;
+    static const int scan_threads = getenv("FE_HOST_SCAN_THREADS") ? atoi(getenv("FE_HOST_SCAN_THREADS")) : 0;
+    if (b > a && !assume_zero) {
       constexpr int NP = 64;
       const size_t w = (b - a + NP - 1) / NP;
-#pragma omp parallel for schedule(static) reduction(| : nonzero)
+      const int nthr = scan_threads > 0 ? scan_threads : omp_get_max_threads();
+#pragma omp parallel for schedule(static) reduction(| : nonzero) num_threads(nthr)
       for (int part = 0; part < NP; ++part) {
         const size_t lo = std::min(b, a + part * w), hi = std::min(b, lo + w);
         uint64_t acc = 0;

@@ -81,6 +81,7 @@ ALTERNATIVES = [
     ("helmholtz", "tetrahedron", 1, {"FE_NO_P1CONST": "1"}, "element_split_macro"),
     ("helmholtz", "tetrahedron", 1, {"FE_MACRO_WAVES": "0"}, "element_split_macro"),
     ("helmholtz", "tetrahedron", 1, {"FE_NO_MACRO": "1"}, "element_split"),
+    ("helmholtz", "tetrahedron", 1, {"FE_MACRO_PIPE": "1"}, "element_split_macro"),
     ("helmholtz", "tetrahedron", 2, {"FE_MACRO_P2": "1"}, "element_split_macro"),
     ("neohookean", "tetrahedron", 2, {}, "quad_vertex_grad"),
     ("neohookean", "tetrahedron", 2, {"FE_NO_VTX": "1"}, "quad_const"),

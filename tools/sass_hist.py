@@ -17,10 +17,10 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # mangled-name fragments of the kernels the BASELINE configs select
 HOT = ["affine_et_kernel", "macro_split_kernel", "affine_split_kernel", "dmma_modal_kernel",
-       "hexq1_lap_kernel", "plane1_kernel", "plane_kernel", "tensor_kernel", "quad_const_kernel",
+       "macro_pipe_kernel", "hexq1_lap_kernel", "hexq2_lap_kernel", "plane1_kernel", "plane_kernel", "tensor_kernel", "quad_const_kernel",
        "pair_kernel", "quad_vtx_kernel", "k_zero_pdl"]
 CLASSES = ["DMMA", "DFMA", "DMUL", "DADD", "MUFU", "LDG", "LDGSTS", "LDS", "STS", "REDG", "ATOMG",
-           "LDC", "SHFL", "BAR", "BRA", "ACQBULK", "PREEXIT", "IMAD", "IADD3", "LOP3", "ISETP", "MOV"]
+           "LDC", "LDCU", "R2UR", "SHFL", "BAR", "BRA", "ACQBULK", "PREEXIT", "IMAD", "IADD3", "LOP3", "ISETP", "MOV"]
 
 
 def demangle(names):
