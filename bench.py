@@ -414,8 +414,14 @@ def run_e2e_host_api(ops, steps):
         u = torch.empty(op["ndofs"], dtype=torch.float64, pin_memory=True).numpy()
         u[:] = prob.u
         out = torch.zeros(op["ndofs"], dtype=torch.float64, pin_memory=True).numpy()
-        hb.append((op, fe.make_bindings(prob.mesh, prob.dofmap, u, out, prob.mu, prob.lam,
-                                        state=getattr(prob, "state", None))))
+        def pinned(a):              # every host input of the call in pinned memory
+            if a is None:
+                return None
+            t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+            t[...] = a
+            return t
+        hb.append((op, fe.make_bindings(prob.mesh, prob.dofmap, u, out, pinned(prob.mu), pinned(prob.lam),
+                                        state=pinned(getattr(prob, "state", None)))))
     for op, b in hb:                 # warm-up: binds the host mesh once
         op["h"](0, op["C"], b)
     # the operators of a step are independent calls: E2E_THREADS host threads

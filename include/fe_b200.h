@@ -169,10 +169,14 @@ int fe_wrap(fe_plan* plan, int32_t start, int32_t end, double* dat0,
 
 /* Reference-order entry on HOST pointers (the drop-in for a ctypes caller
  * holding numpy buffers): uploads dat2 (+ dat3/dat4), applies, and
- * returns dat0 + A(u) in dat0; synchronous.  dat0 is scanned per chunk on
- * the host: all-zero chunks (+0.0 / -0.0) are not uploaded, the others are
- * uploaded and accumulated on the device; each result chunk is downloaded as
- * soon as the last cell chunk scattering into it is done.  The mesh is
+ * returns dat0 + A(u) in dat0; synchronous.  The u / dat0 vector is handled
+ * in 64 blocks: u blocks are uploaded in the order the cell chunks of the
+ * operator read them (a per-chunk block mask found at bind), each result
+ * block is downloaded as soon as the last cell chunk scattering into it is
+ * done, and blocks no cell of [start, end) touches move in neither direction.
+ * dat0 is scanned per block run on the host: all-zero runs (+0.0 / -0.0) are
+ * not uploaded, the others are uploaded and accumulated on the device.  The
+ * mesh is
  * (re-)bound exactly as in fe_wrap when dat1/map0/map1 differ from the bound
  * HOST buffers.  [start, end) outside [0, ncells) -> FE_EINVAL before any
  * copy is queued; on any error every copy of the call has completed before

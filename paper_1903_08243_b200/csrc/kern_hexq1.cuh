@@ -337,4 +337,216 @@ hexq2_lap_kernel(const __grid_constant__ HexQ2Params p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Lane-per-plane, shuffle-exchanged sum-factorised scalar Laplacian for Qk
+// hexahedra on the (k+1)^3 Gauss rule, k = 3, 4 (C3-Q3, C3-Q4).
+//
+// The thread-per-cell kernel above stops at Q = 3 points per direction (the
+// cell no longer fits one thread's registers).  Here a team of Q lanes owns a
+// cell, lane c holding z-plane c: its dof plane, then the point plane
+// uq[c][.][.] and the point-space output plane (2 Q^2 doubles).  The x and y
+// contractions are local to a lane and use compile-time table entries
+// (uniform-register operands); the four z contractions (B_z, Dc_z, Dc_z^T,
+// B_z^T) exchange the Q values of a z line with Q warp shuffles per point and
+// multiply by the lane's row / column of the table (4 Q doubles in vector
+// registers).  Collocation form: 12 q^4 MACs.  No shared memory, no
+// barriers, no loop over cells (straight-line code, one cell per team): the
+// two things that hold the plane / team kernels near 55% FP64 pipe activity
+// on sm_100a (table constants hoisted out of persistent loops, shared-memory
+// round trips with barriers) are absent.
+// ---------------------------------------------------------------------------
+template <int Q>
+struct HexLPParams {
+  MeshView mesh;
+  const int32_t* __restrict__ maplex;   // row-major [ncells][Q^3], tensor (x fastest) order
+  const double* __restrict__ u;
+  double* __restrict__ y;
+  int32_t start, end;
+  double B[Q][Q], Dc[Q][Q], x[Q], w[Q];
+};
+
+template <int Q, int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+hexlp_lap_kernel(const __grid_constant__ HexLPParams<Q> p) {
+  constexpr int TPW = 32 / Q, QQ = Q * Q, ND = Q * Q * Q;
+  const int lane = threadIdx.x & 31;
+  const int T = lane / Q, c = lane % Q;
+  const int gw = blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  const int cell_raw = p.start + gw * TPW + T;
+  const bool live = T < TPW && cell_raw < p.end;
+  const int cell = live ? cell_raw : p.start;      // idle lanes compute on a valid cell, never scatter
+  const int base = (T < TPW ? T : 0) * Q;          // first lane of the team
+  const int cc = T < TPW ? c : 0;
+  const int64_t cs = p.mesh.nc_stride;
+  const unsigned FULL = 0xffffffffu;
+  // the lane's rows / columns of the z tables and its zeta, weight
+  double Bzr[Q], Bzc[Q], Dzr[Q], Dzc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; ++k) {
+    Bzr[k] = p.B[cc][k];
+    Bzc[k] = p.B[k][cc];
+    Dzr[k] = p.Dc[cc][k];
+    Dzc[k] = p.Dc[k][cc];
+  }
+  const double zeta = p.x[cc], wc = p.w[cc];
+  // dof plane k = cc
+  const int32_t* mrow = p.maplex + (int64_t)cell * ND + cc * QQ;
+  double uq[Q][Q];   // [j][i] dof plane, then [b][a] point plane
+#pragma unroll
+  for (int e = 0; e < QQ; ++e) uq[e / Q][e % Q] = __ldg(p.u + __ldg(mrow + e));
+  double cf[7][3];
+  {
+    double X[8][3];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) load_vertex<3>(p.mesh.coords, __ldg(p.mesh.vmap + v * cs + cell), X[v]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      cf[0][d] = X[1][d] - X[0][d];
+      cf[1][d] = X[2][d] - X[0][d];
+      cf[2][d] = X[4][d] - X[0][d];
+      cf[3][d] = (X[3][d] - X[2][d]) - cf[0][d];
+      cf[4][d] = (X[5][d] - X[4][d]) - cf[0][d];
+      cf[5][d] = (X[6][d] - X[4][d]) - cf[1][d];
+      cf[6][d] = ((X[7][d] - X[6][d]) - (X[5][d] - X[4][d])) - (X[3][d] - X[2][d]) + cf[0][d];
+    }
+  }
+  // ---- B along x, then y, on the lane's dof plane -----------------------------
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    double v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = uq[j][i];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      double s = p.B[a][0] * v[0];
+#pragma unroll
+      for (int i = 1; i < Q; ++i) s = fma(p.B[a][i], v[i], s);
+      uq[j][a] = s;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < Q; ++a) {
+    double v[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) v[j] = uq[j][a];
+#pragma unroll
+    for (int b = 0; b < Q; ++b) {
+      double s = p.B[b][0] * v[0];
+#pragma unroll
+      for (int j = 1; j < Q; ++j) s = fma(p.B[b][j], v[j], s);
+      uq[b][a] = s;
+    }
+  }
+  // ---- B along z: the Q values of a z line live in the team's Q lanes ---------
+#pragma unroll
+  for (int e = 0; e < QQ; ++e) {
+    const double v = uq[e / Q][e % Q];
+    double s = Bzr[0] * __shfl_sync(FULL, v, base);
+#pragma unroll
+    for (int k = 1; k < Q; ++k) s = fma(Bzr[k], __shfl_sync(FULL, v, base + k), s);
+    uq[e / Q][e % Q] = s;
+  }
+  // ---- points of plane cc: gradient, flux, transposed collocation derivative --
+  double out[Q][Q];
+#pragma unroll
+  for (int e = 0; e < QQ; ++e) out[e / Q][e % Q] = 0.0;
+  double A0[3], A1[3], B0[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    A0[d] = fma(zeta, cf[4][d], cf[0][d]);   // dx/dxi   = A0 + eta A1
+    A1[d] = fma(zeta, cf[6][d], cf[3][d]);   // dx/deta  = B0 + xi A1
+    B0[d] = fma(zeta, cf[5][d], cf[1][d]);
+  }
+#pragma unroll
+  for (int b = 0; b < Q; ++b) {
+    const double eta = p.x[b], wbc = p.w[b] * wc;
+    double Jx[3], C0[3], C1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      Jx[d] = fma(eta, A1[d], A0[d]);
+      C0[d] = fma(eta, cf[5][d], cf[2][d]);  // dx/dzeta = C0 + xi C1
+      C1[d] = fma(eta, cf[6][d], cf[4][d]);
+    }
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+      const double xi = p.x[a];
+      double J[3][3], A[3][3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        J[d][0] = Jx[d];
+        J[d][1] = fma(xi, A1[d], B0[d]);
+        J[d][2] = fma(xi, C1[d], C0[d]);
+      }
+      const double det = det_adj<3>(J, A);
+      const double s = (p.w[a] * wbc) * rcp(fabs(det));
+      double g[3];
+      g[0] = p.Dc[a][0] * uq[b][0];
+      g[1] = p.Dc[b][0] * uq[0][a];
+#pragma unroll
+      for (int e = 1; e < Q; ++e) {
+        g[0] = fma(p.Dc[a][e], uq[b][e], g[0]);
+        g[1] = fma(p.Dc[b][e], uq[e][a], g[1]);
+      }
+      {
+        const double v = uq[b][a];
+        g[2] = Dzr[0] * __shfl_sync(FULL, v, base);
+#pragma unroll
+        for (int e = 1; e < Q; ++e) g[2] = fma(Dzr[e], __shfl_sync(FULL, v, base + e), g[2]);
+      }
+      double t[3], f[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) t[e] = s * fma(A[2][e], g[2], fma(A[1][e], g[1], A[0][e] * g[0]));
+#pragma unroll
+      for (int r = 0; r < 3; ++r) f[r] = fma(A[r][2], t[2], fma(A[r][1], t[1], A[r][0] * t[0]));
+#pragma unroll
+      for (int e = 0; e < Q; ++e) {
+        out[b][e] = fma(p.Dc[a][e], f[0], out[b][e]);
+        out[e][a] = fma(p.Dc[b][e], f[1], out[e][a]);
+      }
+      // Dc_z^T: plane e collects sum_c Dc[c][e] f_zeta(c) of this point's z line
+      double z = out[b][a];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) z = fma(Dzc[k], __shfl_sync(FULL, f[2], base + k), z);
+      out[b][a] = z;
+    }
+  }
+  // ---- B^T along z (shuffles), then y, then x on the lane's plane -------------
+#pragma unroll
+  for (int e = 0; e < QQ; ++e) {
+    const double v = out[e / Q][e % Q];
+    double s = Bzc[0] * __shfl_sync(FULL, v, base);
+#pragma unroll
+    for (int k = 1; k < Q; ++k) s = fma(Bzc[k], __shfl_sync(FULL, v, base + k), s);
+    out[e / Q][e % Q] = s;
+  }
+#pragma unroll
+  for (int a = 0; a < Q; ++a) {
+    double v[Q];
+#pragma unroll
+    for (int b = 0; b < Q; ++b) v[b] = out[b][a];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      double s = p.B[0][j] * v[0];
+#pragma unroll
+      for (int b = 1; b < Q; ++b) s = fma(p.B[b][j], v[b], s);
+      out[j][a] = s;
+    }
+  }
+  griddep_wait();
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    double v[Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) v[a] = out[j][a];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      double s = p.B[0][i] * v[0];
+#pragma unroll
+      for (int a = 1; a < Q; ++a) s = fma(p.B[a][i], v[a], s);
+      if (live) scatter_add(p.y, __ldg(mrow + j * Q + i), s);
+    }
+  }
+}
+
 }  // namespace fe

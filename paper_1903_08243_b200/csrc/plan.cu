@@ -20,9 +20,6 @@
 
 #include "common.cuh"
 
-#ifndef FE_HOST_YCHUNKS
-#define FE_HOST_YCHUNKS 8  // result chunks of the host entry
-#endif
 #ifndef FE_HOST_UCHUNKS
 #define FE_HOST_UCHUNKS 8  // u / cell chunks of the host entry
 #endif
@@ -151,18 +148,19 @@ struct fe_plan {
   cudaStream_t hstream = nullptr;
   cudaStream_t hstream2 = nullptr;
   cudaEvent_t ev_u = nullptr, ev_y0 = nullptr;
-  cudaEvent_t ev_y0c[32] = {};  // per-chunk completion of the dat0 upload (host entry)
   cudaEvent_t ev_uc[32] = {};   // per-chunk completion of the u upload (host entry)
   cudaStream_t hstream_u = nullptr;
   cudaStream_t hstream_d = nullptr;  // result downloads (host entry)
   cudaEvent_t ev_cell[32] = {};       // completion of each cell chunk (host entry)
-  // per result chunk: the last cell chunk that scatters into it (computed at
-  // bind), so its download starts while later cell chunks still run
-  std::vector<int32_t> ychunk_last;
-  std::vector<int64_t> ybound;  // result chunk boundaries (vertex dofs, when numbered first, are chunk 0)
-  // host entry pipelining: cell chunks (kHostChunks, boundaries aligned to
-  // 192 cells) and the largest dof index each one reads (computed at bind)
-  std::vector<int32_t> chunk_cell, chunk_maxdof;
+  // host entry pipelining: cell chunks (FE_HOST_UCHUNKS, boundaries aligned
+  // to 192 cells) and, per chunk, the mask of the 64 blocks (hblock entries
+  // each) of the u / y vector its cells read and scatter into (computed at
+  // bind): u is uploaded block by block in the order the cell chunks need it,
+  // and a block of y is downloaded as soon as the last cell chunk touching it
+  // is done -- for any dof numbering (vertex dofs first, lexicographic, ...)
+  std::vector<int32_t> chunk_cell;
+  std::vector<uint64_t> chunk_mask;
+  int64_t hblock = 0;
   double* d_u = nullptr;
   double* d_y = nullptr;
   double* d_y0 = nullptr;
@@ -1097,6 +1095,47 @@ int hexq2_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
   return FE_OK;
 }
 
+// lane-per-plane shuffle-exchanged Qk hex Laplacian, k = 3, 4 (kern_hexq1.cuh)
+#ifndef FE_HEXLP_BLOCK
+#define FE_HEXLP_BLOCK 64
+#endif
+template <int Q>
+int hexlp_prepare(fe_plan* p) {
+  if ((int)p->lex.size() != Q * Q * Q) return fail(FE_EUNSUPPORTED, "hexlp kernel needs the tensor map");
+  TensorParams<Q, Q> tp;
+  if (int rc = fill_tensor_tables<Q, Q>(p, &tp)) return rc;
+  HexLPParams<Q>* hp = new HexLPParams<Q>();
+  for (int a = 0; a < Q; ++a) {
+    for (int i = 0; i < Q; ++i) {
+      hp->B[a][i] = tp.B[a][i];
+      hp->Dc[a][i] = tp.Dc[a][i];
+    }
+    hp->x[a] = tp.x[a];
+    hp->w[a] = tp.w[a];
+  }
+  p->host_params = hp;
+  p->host_params_bytes = sizeof(HexLPParams<Q>);
+  return FE_OK;
+}
+
+template <int Q>
+int hexlp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
+                 const double*, const double*, cudaStream_t s) {
+  HexLPParams<Q> hpv = *static_cast<const HexLPParams<Q>*>(p->host_params);
+  if (!p->d_map_lex) return fail(FE_ENOMESH, "tensor plan without a lexicographic map");
+  hpv.mesh = mesh_view(p);
+  hpv.maplex = p->d_map_lex;
+  hpv.u = u;
+  hpv.y = y;
+  hpv.start = start;
+  hpv.end = end;
+  const int n = end - start;
+  constexpr int CPB = (FE_HEXLP_BLOCK / 32) * (32 / Q);   // cells per CTA
+  if (n > 0) launch_op(hexlp_lap_kernel<Q, FE_HEXLP_BLOCK, 1>, (unsigned)((n + CPB - 1) / CPB), FE_HEXLP_BLOCK, 0, s, hpv);
+  CUDA_TRY(cudaGetLastError());
+  return FE_OK;
+}
+
 // component-pair 2D elasticity kernel (kern_pair.cuh).  FE_PAIR_CFG selects
 // the kernel: 0 = round-1 kernel (one cell pair per thread pair, gather on
 // the critical path), 1 = pipelined persistent kernel, 4-warp CTAs, 2 per SM
@@ -1237,6 +1276,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define HQ2V()                                                                               \
   {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 2, 27, 28, "sum_factorised_q2", FE_HEXQ2_BLOCK, \
    hexq2_prepare, hexq2_launch}
+#define HLPV(K, Q)                                                                           \
+  {FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, K, Q * Q * Q, 29, "sum_factorised_lane_plane", FE_HEXLP_BLOCK, \
+   hexlp_prepare<Q>, hexlp_launch<Q>}
 #define SPV(FORM, CELL, DIM, K, ND, NQS)                                                     \
   {FORM, CELL, K, -1, 12, "element_split", 128, split_prepare<FORM, DIM, ND, NQS>,           \
    split_launch<FORM, DIM, ND, NQS>}
@@ -1330,6 +1372,8 @@ static const Variant kVariants[] = {
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 8, 1, 8),
     HQ1V(),
     HQ2V(),
+    HLPV(3, 4),
+    HLPV(4, 5),
     QCT(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_HEXAHEDRON, 3, 8, 1, 8, 27, 1, 3),
     QCT(FE_FORM_ELASTICITY_LAME, FE_CELL_QUADRILATERAL, 2, 4, 1, 4, 9, 1, 1),
@@ -1395,38 +1439,22 @@ __global__ void k_check_vmap(const int32_t* __restrict__ map0, const int32_t* __
   if (map0[(int64_t)c * nd + v] != map1[t]) *flag = 1;
 }
 
-// per result chunk ([ybound[k], ybound[k+1]) of the vs-interleaved result),
-// the last cell chunk whose scatter touches it (row-major map)
-__global__ void k_ychunk_last(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
-                              int nchunk, int vs, const int64_t* __restrict__ ybound, int ny,
-                              int* __restrict__ out) {
+// host-entry pipelining: per chunk of cells, the 64-bit mask of the blocks
+// (bsz entries each) of the vs-interleaved u / y vector its cells touch
+// (row-major map; the gather and the scatter use the same map)
+__global__ void k_chunk_blockmask(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
+                                  int nchunk, int vs, int64_t bsz, unsigned long long* __restrict__ out) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)nc * nd) return;
   const int c = (int)(t / nd);
   int k = 0;
   while (k + 1 < nchunk && c >= bounds[k + 1]) ++k;
   const int64_t e = (int64_t)vs * rm[t];
-  int y0 = 0;
-  while (y0 + 1 < ny && e >= ybound[y0 + 1]) ++y0;
-  int y1 = y0;
-  while (y1 + 1 < ny && e + vs - 1 >= ybound[y1 + 1]) ++y1;
-  for (int y = y0; y <= y1; ++y)
-    if (out[y] < k) atomicMax(out + y, k);
-}
-
-// largest dof index read by each chunk of cells (row-major map)
-__global__ void k_chunk_maxdof(const int32_t* __restrict__ rm, int nc, int nd, const int32_t* __restrict__ bounds,
-                               int nchunk, int* __restrict__ out) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)nc * nd) return;
-  const int c = (int)(t / nd);
-  int k = 0;
-  while (k + 1 < nchunk && c >= bounds[k + 1]) ++k;
-  // one atomic per warp and chunk (126M same-address atomics at C5 otherwise:
-  // 0.68 s of bind time in the ncu launch list, profiles/r02/launches_r2k.csv)
+  const unsigned long long m = (1ull << (e / bsz)) | (1ull << ((e + vs - 1) / bsz));
+  // one atomic per warp and chunk
   const unsigned grp = __match_any_sync(__activemask(), k);
-  const int m = __reduce_max_sync(grp, rm[t]);
-  if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicMax(out + k, m);
+  const unsigned lo = __reduce_or_sync(grp, (unsigned)m), hi = __reduce_or_sync(grp, (unsigned)(m >> 32));
+  if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicOr(out + k, ((unsigned long long)hi << 32) | lo);
 }
 
 __global__ void k_check_range(const int32_t* __restrict__ m, int64_t n, int64_t hi, int* flag) {
@@ -1500,6 +1528,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 26 && getenv("FE_NO_PAIR")) continue;
     if (v.priority == 27 && getenv("FE_NO_HEXQ1")) continue;
     if (v.priority == 28 && getenv("FE_NO_HEXQ2")) continue;
+    if (v.priority == 29 && !getenv("FE_HEXLP")) continue;   // opt-in until measured
     if (v.priority == 6 && getenv("FE_NO_VTX")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):
     // opt-in only (FE_PATCH=1) for experiments
@@ -1806,60 +1835,28 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
     return fail(FE_EINVAL, "map entry out of range");
   }
   {
-    // host-entry pipelining: per cell chunk, the largest dof index it reads
+    // host-entry pipelining: per cell chunk, the blocks of u / y it touches
     constexpr int NCH = FE_HOST_UCHUNKS;
     p->chunk_cell.assign(NCH + 1, 0);
     for (int c = 0; c <= NCH; ++c)
       p->chunk_cell[c] = (int32_t)std::min<int64_t>(ncells, ((int64_t)ncells * c / NCH + 191) / 192 * 192);
     p->chunk_cell[NCH] = ncells;
-    p->chunk_maxdof.assign(NCH, -1);
-    p->ychunk_last.assign(FE_HOST_YCHUNKS, 0);
-    {
-      // result chunks: when the vertex dofs are numbered first (map0[:, :nv]
-      // is the vertex map) and are a small part of the result, they form
-      // chunk 0 on their own -- every cell chunk scatters into them, so that
-      // chunk is final only at the end and should be short; the rest is
-      // split evenly (32-entry aligned)
-      constexpr int NYC = FE_HOST_YCHUNKS;
-      const int64_t ny = (int64_t)p->vs * p->nglobal;
-      const int64_t vert = h_flag[1] ? 0 : (int64_t)p->vs * p->nverts;
-      p->ybound.assign(NYC + 1, ny);
-      p->ybound[0] = 0;
-      if (NYC > 1 && vert > 0 && vert < ny / NYC) {
-        p->ybound[1] = vert;
-        for (int c = 2; c < NYC; ++c)
-          p->ybound[c] = std::min(ny, vert + (((ny - vert) * (c - 1) / (NYC - 1)) + 31) / 32 * 32);
-      } else {
-        const int64_t ychunk = ((ny + NYC - 1) / NYC + 31) / 32 * 32;
-        for (int c = 1; c < NYC; ++c) p->ybound[c] = std::min(ny, c * ychunk);
-      }
-    }
+    p->chunk_mask.assign(NCH, 0);
+    const int64_t ny = (int64_t)p->vs * p->nglobal;
+    p->hblock = std::max<int64_t>(32, ((ny + 63) / 64 + 31) / 32 * 32);
     if (ncells > 0) {
       int32_t* d_b = nullptr;
-      int* d_o = nullptr;
+      unsigned long long* d_o = nullptr;
       CUDA_TRY(cudaMalloc(&d_b, (NCH + 1) * sizeof(int32_t)));
-      CUDA_TRY(cudaMalloc(&d_o, NCH * sizeof(int)));
+      CUDA_TRY(cudaMalloc(&d_o, NCH * sizeof(unsigned long long)));
       CUDA_TRY(cudaMemcpyAsync(d_b, p->chunk_cell.data(), (NCH + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      CUDA_TRY(cudaMemsetAsync(d_o, 0xff, NCH * sizeof(int), s));
+      CUDA_TRY(cudaMemsetAsync(d_o, 0, NCH * sizeof(unsigned long long), s));
       const int64_t n = (int64_t)ncells * nd;
-      k_chunk_maxdof<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, d_o);
-      CUDA_TRY(cudaMemcpyAsync(p->chunk_maxdof.data(), d_o, NCH * sizeof(int), cudaMemcpyDeviceToHost, s));
+      k_chunk_blockmask<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, p->vs,
+                                                                 p->hblock, d_o);
+      static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "mask type");
+      CUDA_TRY(cudaMemcpyAsync(p->chunk_mask.data(), d_o, NCH * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
-      {
-        constexpr int NYC = FE_HOST_YCHUNKS;
-        int* d_y = nullptr;
-        int64_t* d_yb = nullptr;
-        CUDA_TRY(cudaMalloc(&d_y, NYC * sizeof(int)));
-        CUDA_TRY(cudaMalloc(&d_yb, (NYC + 1) * sizeof(int64_t)));
-        CUDA_TRY(cudaMemsetAsync(d_y, 0, NYC * sizeof(int), s));
-        CUDA_TRY(cudaMemcpyAsync(d_yb, p->ybound.data(), (NYC + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        k_ychunk_last<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(p->d_map_rm, ncells, nd, d_b, NCH, p->vs,
-                                                               d_yb, NYC, d_y);
-        CUDA_TRY(cudaMemcpyAsync(p->ychunk_last.data(), d_y, NYC * sizeof(int), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        cudaFree(d_y);
-        cudaFree(d_yb);
-      }
       cudaFree(d_b);
       cudaFree(d_o);
     }
@@ -1995,6 +1992,10 @@ static int wrap_host_impl(fe_plan* p, int32_t start, int32_t end, double* dat0, 
   }
   const double* c0 = nullptr;
   const double* c1 = nullptr;
+  // the u upload (own stream) is ordered after what is already queued on s,
+  // not after the coefficient copies below
+  if (!p->ev_u) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(p->ev_u, s));
   // coefficient fields: mu/lambda vertex fields, or the state u of a
   // linearised form (a dof field with the layout of dat2)
   const bool state = p->form == FE_FORM_NEOHOOKEAN_TANGENT;
@@ -2015,104 +2016,134 @@ static int wrap_host_impl(fe_plan* p, int32_t start, int32_t end, double* dat0, 
       c1 = p->d_c1;
     }
   }
-  // u first, in chunks on its own stream; cell chunk r of the operator
-  // starts as soon as every u chunk it reads has landed (largest dof per
-  // cell chunk, found at bind).  Result chunk c is final once the last cell
-  // chunk scattering into it (ychunk_last, found at bind) is done: its
-  // download then starts on a third stream while later cell chunks run and
-  // the rest of u is still uploading (PCIe is full duplex).  Accumulate
-  // semantics: result chunks whose dat0 is all zero (the common y = A u call,
-  // detected on the host while u uploads) are downloaded straight into dat0;
-  // the others upload dat0, add on the device, then download.
-  constexpr int NCH = FE_HOST_UCHUNKS;  // u chunks (operator cell chunks follow them)
+  // Pipeline over the 64 blocks of the u / y vector (chunk_mask, found at
+  // bind): u is uploaded on its own stream block by block in the order the
+  // cell chunks need it; cell chunk r of the operator starts as soon as every
+  // block it reads has landed; a block of the result is final once the last
+  // cell chunk scattering into it is done and is then downloaded on a third
+  // stream while later cell chunks run and the rest of u is still uploading
+  // (PCIe is full duplex).  Blocks no cell of [start, end) touches are neither
+  // uploaded nor downloaded (dat0 + 0 = dat0).  This holds for any dof
+  // numbering: with vertex dofs numbered first, the vertex section and the
+  // rest of the vector both stream in cell order.  Accumulate semantics:
+  // result blocks whose dat0 is all zero (the common y = A u call, detected on
+  // the host while u uploads) are downloaded straight into dat0; the others
+  // upload dat0, add on the device, then download.
+  constexpr int NCH = FE_HOST_UCHUNKS;  // cell chunks
   static_assert(NCH <= 32, "ev_uc size");
-  constexpr int NYC = FE_HOST_YCHUNKS;  // dat0 / result chunks
-  static_assert(NYC <= 32, "ev_y0c size");
   if (!p->hstream2) {
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream2, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream_u, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&p->hstream_d, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_u, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0, cudaEventDisableTiming));
     for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_uc[c], cudaEventDisableTiming));
     for (int c = 0; c < NCH; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_cell[c], cudaEventDisableTiming));
-    for (int c = 0; c < NYC; ++c) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_y0c[c], cudaEventDisableTiming));
   }
-  const size_t chunk = ((n + NCH - 1) / NCH + 31) / 32 * 32;
-  CUDA_TRY(cudaEventRecord(p->ev_u, s));
+  const int64_t bsz = p->hblock;
+  const int nblk = bsz > 0 ? (int)((n + bsz - 1) / bsz) : 0;
+  const int ncc = (int)p->chunk_cell.size() - 1;
+  // cell chunks of this call and the blocks they touch
+  uint64_t need[NCH] = {};
+  int32_t ca[NCH] = {}, cb[NCH] = {};
+  // short vectors (< 4 MB): one chunk -- the fixed cost of the per-chunk copies,
+  // events and launches (~0.1 ms per call) outweighs what pipelining hides
+  const bool single = n * sizeof(double) < (size_t)4 << 20;
+  for (int r = 0; r < ncc && r < NCH; ++r) {
+    const int32_t a = std::max(start, p->chunk_cell[r]), b = std::min(end, p->chunk_cell[r + 1]);
+    if (a >= b) continue;
+    const int k = single ? 0 : r;
+    if (need[k] == 0) ca[k] = a;
+    cb[k] = b;
+    need[k] |= p->chunk_mask[r];
+  }
+  // maximal runs of set bits of a block mask -> [a, b) entry ranges
+  auto for_runs = [&](uint64_t mask, auto&& fn) -> int {
+    for (int b0 = 0; b0 < nblk;) {
+      if (!((mask >> b0) & 1)) { ++b0; continue; }
+      int b1 = b0;
+      while (b1 + 1 < nblk && ((mask >> (b1 + 1)) & 1)) ++b1;
+      const size_t a = (size_t)b0 * bsz, b = std::min(n, (size_t)(b1 + 1) * bsz);
+      if (int rc = fn(a, b)) return rc;
+      b0 = b1 + 1;
+    }
+    return FE_OK;
+  };
+  // u: the blocks each cell chunk needs that are not on the device yet
   CUDA_TRY(cudaStreamWaitEvent(p->hstream_u, p->ev_u, 0));
-  for (int c = 0; c < NCH; ++c) {
-    const size_t a = std::min(n, c * chunk), b = std::min(n, a + chunk);
-    if (b > a)
+  uint64_t have = 0;
+  for (int r = 0; r < ncc && r < NCH; ++r) {
+    if (ca[r] >= cb[r]) continue;
+    int rc = for_runs(need[r] & ~have, [&](size_t a, size_t b) -> int {
       CUDA_TRY(cudaMemcpyAsync(p->d_u + a, dat2 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
                                p->hstream_u));
-    CUDA_TRY(cudaEventRecord(p->ev_uc[c], p->hstream_u));
+      return FE_OK;
+    });
+    if (rc) return rc;
+    have |= need[r];
+    CUDA_TRY(cudaEventRecord(p->ev_uc[r], p->hstream_u));
   }
-  // the operator first (it does not read dat0): memset + one launch per cell
-  // chunk, each gated on the u chunks it reads
+  // the operator (it does not read dat0): memset + one launch per cell chunk,
+  // each gated on the upload of the blocks it reads
   CUDA_TRY(cudaMemsetAsync(p->d_y, 0, n * sizeof(double), s));
-  const int vs = p->vs;
-  const int ncc = (int)p->chunk_cell.size() - 1;
-  for (int r = 0; r < ncc; ++r) {
-    const int32_t a = std::max(start, p->chunk_cell[r]), b = std::min(end, p->chunk_cell[r + 1]);
-    if (a < b) {
-      const int64_t last = (int64_t)vs * p->chunk_maxdof[r] + vs - 1;  // last u entry this chunk reads
-      const int cu = (int)std::min<int64_t>(NCH - 1, last < 0 ? 0 : (int64_t)(last / (int64_t)chunk));
-      CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[cu], 0));
-      int rc = fe_apply(p, a, b, p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
-      if (rc) return rc;
-    }
+  int last_of[64];
+  for (int b = 0; b < 64; ++b) last_of[b] = -1;
+  for (int r = 0; r < ncc && r < NCH; ++r) {
+    if (ca[r] >= cb[r]) continue;
+    CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[r], 0));
+    static const bool noapply = getenv("FE_HOST_NOAPPLY") != nullptr;  // diagnosis: copy pipeline only
+    int rc = noapply ? FE_OK : fe_apply(p, ca[r], cb[r], p->d_y, p->d_u, c0, c1, FE_APPLY_ACCUMULATE, s);
+    if (rc) return rc;
+    for (int b = 0; b < nblk; ++b)
+      if ((need[r] >> b) & 1) last_of[b] = r;
     CUDA_TRY(cudaEventRecord(p->ev_cell[r], s));
   }
-  CUDA_TRY(cudaStreamWaitEvent(s, p->ev_uc[NCH - 1], 0));  // stream order for the next call's reuse of d_u
-  // then, per result chunk in the order the chunks become final (one stream:
-  // a chunk waiting for the last cell chunk must not hold back the others;
-  // with vertex dofs numbered first, chunk 0 is final only at the end):
-  // scan its dat0 on the host (all +0.0/-0.0 -> not uploaded), otherwise
-  // upload it behind u and add it on the device, then download
-  int order[NYC];
-  for (int c = 0; c < NYC; ++c) order[c] = c;
-  std::stable_sort(order, order + NYC, [&](int x, int y) { return p->ychunk_last[x] < p->ychunk_last[y]; });
-  CUDA_TRY(cudaStreamWaitEvent(p->hstream2, p->ev_uc[NCH - 1], 0));
+  // result blocks in the order they become final (one download stream: a
+  // block waiting for the last cell chunk must not hold back the others);
+  // runs of blocks finalised by the same cell chunk are one copy.  Scan dat0
+  // on the host (all +0.0/-0.0 -> not uploaded), otherwise upload it and add
+  // it on the device, then download
   const uint64_t* ybits = reinterpret_cast<const uint64_t*>(dat0);
-  for (int oc = 0; oc < NYC; ++oc) {
-    const int c = order[oc];
-    const size_t a = (size_t)p->ybound[c], b = (size_t)p->ybound[c + 1];
-    int nonzero = 0;
-    // experiment switches: FE_HOST_ASSUME_ZERO=1 skips the scan (measures its cost; breaks
-    // the accumulate semantics), FE_HOST_SCAN_THREADS = OpenMP threads of one call's scan
-    static const bool assume_zero = getenv("FE_HOST_ASSUME_ZERO") != nullptr;
-    static const int scan_threads = getenv("FE_HOST_SCAN_THREADS") ? atoi(getenv("FE_HOST_SCAN_THREADS")) : 0;
-    if (b > a && !assume_zero) {
-      constexpr int NP = 64;
-      const size_t w = (b - a + NP - 1) / NP;
-      const int nthr = scan_threads > 0 ? scan_threads : omp_get_max_threads();
+  static const bool assume_zero = getenv("FE_HOST_ASSUME_ZERO") != nullptr;   // diagnosis (breaks accumulate)
+  static const int scan_threads = getenv("FE_HOST_SCAN_THREADS") ? atoi(getenv("FE_HOST_SCAN_THREADS")) : 0;
+  for (int r = 0; r < ncc && r < NCH; ++r) {
+    uint64_t fin = 0;
+    for (int b = 0; b < nblk; ++b)
+      if (last_of[b] == r) fin |= 1ull << b;
+    if (!fin) continue;
+    CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, p->ev_cell[r], 0));
+    int rc = for_runs(fin, [&](size_t a, size_t b) -> int {
+      int nonzero = 0;
+      if (!assume_zero) {
+        constexpr int NP = 64;
+        const size_t w = (b - a + NP - 1) / NP;
+        const int nthr = scan_threads > 0 ? scan_threads : omp_get_max_threads();
 #pragma omp parallel for schedule(static) reduction(| : nonzero) num_threads(nthr)
-      for (int part = 0; part < NP; ++part) {
-        const size_t lo = std::min(b, a + part * w), hi = std::min(b, lo + w);
-        uint64_t acc = 0;
-        for (size_t k0 = lo; k0 < hi && !acc; k0 += 1024)  // stops at the first nonzero block
-          for (size_t k = k0; k < std::min(hi, k0 + 1024); ++k) acc |= ybits[k] << 1;  // drop the sign bit
-        nonzero |= acc != 0;
+        for (int part = 0; part < NP; ++part) {
+          const size_t lo = std::min(b, a + part * w), hi = std::min(b, lo + w);
+          uint64_t acc = 0;
+          for (size_t k0 = lo; k0 < hi && !acc; k0 += 1024)  // stops at the first nonzero block
+            for (size_t k = k0; k < std::min(hi, k0 + 1024); ++k) acc |= ybits[k] << 1;  // drop the sign bit
+          nonzero |= acc != 0;
+        }
       }
-    }
-    const int r = ncc > 0 ? std::min(ncc - 1, std::max(0, (int)p->ychunk_last[c])) : -1;
-    CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, r >= 0 ? p->ev_cell[r] : p->ev_uc[NCH - 1], 0));
-    if (b <= a) continue;
-    if (nonzero) {
-      CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
-                               p->hstream2));
-      CUDA_TRY(cudaEventRecord(p->ev_y0c[c], p->hstream2));
-      CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, p->ev_y0c[c], 0));
-      k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, p->hstream_d>>>(
-          p->d_y + a, p->d_y0 + a, (int64_t)(b - a));
-      CUDA_TRY(cudaGetLastError());
-    }
-    CUDA_TRY(cudaMemcpyAsync(dat0 + a, p->d_y + a, (b - a) * sizeof(double), cudaMemcpyDeviceToHost,
-                             p->hstream_d));
+      if (nonzero) {
+        CUDA_TRY(cudaMemcpyAsync(p->d_y0 + a, dat0 + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice,
+                                 p->hstream2));
+        CUDA_TRY(cudaEventRecord(p->ev_y0, p->hstream2));
+        CUDA_TRY(cudaStreamWaitEvent(p->hstream_d, p->ev_y0, 0));
+        k_add<<<(unsigned)std::min<size_t>((b - a + 255) / 256, 148 * 16), 256, 0, p->hstream_d>>>(
+            p->d_y + a, p->d_y0 + a, (int64_t)(b - a));
+        CUDA_TRY(cudaGetLastError());
+      }
+      CUDA_TRY(cudaMemcpyAsync(dat0 + a, p->d_y + a, (b - a) * sizeof(double), cudaMemcpyDeviceToHost,
+                               p->hstream_d));
+      return FE_OK;
+    });
+    if (rc) return rc;
   }
   CUDA_TRY(cudaStreamSynchronize(p->hstream_d));
   CUDA_TRY(cudaStreamSynchronize(p->hstream2));
+  CUDA_TRY(cudaStreamSynchronize(p->hstream_u));
   CUDA_TRY(cudaStreamSynchronize(s));
   return FE_OK;
 }
@@ -2156,8 +2187,6 @@ void fe_plan_destroy(fe_plan* p) {
   if (p->hstream2) cudaStreamDestroy(p->hstream2);
   if (p->ev_u) cudaEventDestroy(p->ev_u);
   if (p->ev_y0) cudaEventDestroy(p->ev_y0);
-  for (cudaEvent_t e : p->ev_y0c)
-    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_uc)
     if (e) cudaEventDestroy(e);
   if (p->hstream_u) cudaStreamDestroy(p->hstream_u);

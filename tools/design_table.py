@@ -15,25 +15,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 LIMITER = {
-    "C1": "latency: one wave of 131k cells, map -> coordinates/u dependent round trips; 8 MB problem (L2-resident)",
-    "C2-P1": "gather latency (4 dependent loads per macro-cell) + 2.1M REDs; FP64 pipe ~40%",
+    "C1": "latency: one wave of 131k cells, map -> coordinates/u dependent round trips; 8 MB problem; a bare y-fill launch is 5 us of it; 3.9 us per apply inside a CUDA graph (profiles/r01/c1_floor.txt)",
+    "C2-P1": "gather latency (long scoreboard 4.1 of 7.4 stall cycles/inst) + 2.1M REDs; FP64 pipe 51% while it runs; ~5 us of the 19.4 are launch + zero-fill; cp.async-pipelined variant slower (ab_macro_pipe.txt)",
     "C2-P2": "FP64 pipe + 15.7M REDs",
-    "C2-P3": "DMMA pipe 66%, gather latency (long scoreboard), 81% of DMMA flops useful",
-    "C2-P4": "DMMA pipe 76% (math-pipe throttle), 92% of DMMA flops useful",
-    "C3-Q1": "thread per cell, dependent gather latency",
-    "C3-Q2": "plane_t: 255 registers, 8 warps/SM",
-    "C3-Q3": "plane: FP64 pipe 61%, 224 registers",
-    "C3-Q4": "plane: registers (P^2 dof + output planes per thread)",
-    "C3-Q5": "team kernel (36-thread teams, CTA barriers): FP64 pipe 45%, smem + barrier stalls",
-    "C3-Q6": "team kernel (49-thread teams): FP64 pipe 57%",
+    "C2-P3": "DMMA pipe 61% + DFMA 13%, gather latency; 59 DMMA per 8 cells (92% useful) after the split-tuple packing",
+    "C2-P4": "DMMA pipe 76% (math-pipe throttle), 92% of the DMMA flops useful",
+    "C3-Q1": "thread per cell, FP64 pipe 59% while it runs; 21.1 us kernel + launch/zero-fill: dependent gather latency over 3.5 waves",
+    "C3-Q2": "thread per cell (round 2): FP64 pipe 63%, 255 registers (268 B spill), gather exposed at kernel start",
+    "C3-Q3": "plane kernel, 8-warp CTAs: FP64 pipe 61%, 206 registers",
+    "C3-Q4": "plane kernel: FP64 pipe 57%, 244 registers (P^2 dof + output planes per thread)",
+    "C3-Q5": "team kernel (36-thread teams, CTA barriers, cp.async gather): FP64 pipe 54%; direct algorithm executes 16 q^4 MACs (menu minimum 12 q^4); 319 -> in-loop LDCU table loads",
+    "C3-Q6": "team kernel (49-thread teams): FP64 pipe 55%, 128 registers with spills; direct algorithm",
     "C4-quad-Q1": "FP64",
     "C4-quad-Q2": "FP64",
-    "C4-quad-Q3": "pair: FP64 pipe 52%, 255 registers, 8 warps/SM",
-    "C4-quad-Q4": "pair: 255 registers, 12% occupancy",
+    "C4-quad-Q3": "pair kernel: FP64 pipe 52%, 255 registers, 2 warps/SMSP; MUL/ADD-heavy pointwise (F/2 = 79% of its FP64 issue slots)",
+    "C4-quad-Q4": "pair kernel: FP64 pipe 52%, 255 registers, instruction-cache misses (69 KB straight-line code)",
     "C4-hex-Q1": "FP64",
-    "C4-hex-Q2": "team kernel: FP64 pipe ~56%, smem round trips, 128 registers + spill",
-    "C4-hex-Q3": "team kernel: 255 registers, 25-thread teams (1 per warp), smem store conflicts",
-    "C5": "FP64 pipe 70%, 238 registers -> 8 warps/SM (dependent-FMA 'wait' stalls)",
+    "C4-hex-Q2": "team kernel (16-thread teams, 9 / 12 of 16 lanes busy in the z / y stages): FP64 pipe 57%",
+    "C4-hex-Q3": "team kernel (25-thread teams, one per warp: 78% of the lanes; 16 / 20 of 25 in the z / y stages): FP64 pipe 58%",
+    "C5": "FP64 pipe 73%, 254 registers -> 8 warps/SM; executes fewer flops than the menu's F (0.53 of the roof counted on executed flops)",
 }
 
 
