@@ -108,6 +108,9 @@ C3_KERNELS = [
     ("C3-Q2", {"FE_NO_HEXQ2": "1", "FE_NO_PLANE1": "1"}, "sum_factorised"),
     ("C3-Q3", {}, "sum_factorised_plane"),
     ("C3-Q3", {"FE_NO_PLANE": "1"}, "sum_factorised"),
+    ("C3-Q3", {"FE_HEXLP": "1"}, "sum_factorised_lane_plane"),
+    ("C3-Q4", {"FE_HEXLP": "1"}, "sum_factorised_lane_plane"),
+    ("C3-Q4", {}, "sum_factorised_plane"),
 ]
 
 
