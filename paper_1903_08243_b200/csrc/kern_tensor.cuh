@@ -106,6 +106,9 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 #ifndef FE_TK_FLATZ
 #define FE_TK_FLATZ 0   // 1: one z stage for all components of a vector form; measured neutral
 #endif                  // (C4-hex-Q2 0.456 -> 0.460 ms, C4-hex-Q3 1.244 -> 1.239 ms, profiles/r02/ab_tensor_flatz.txt)
+#ifndef FE_TK_CPENCIL
+#define FE_TK_CPENCIL 1
+#endif
 #ifndef FE_TK_ASYNC
 #define FE_TK_ASYNC 0   // 1: cp.async gather pipeline (no prefetch registers)
 #endif
@@ -148,7 +151,7 @@ struct TensorLayout {
   static constexpr int ZS = NZ * P * SZ;                    // Z region of one component
   static constexpr int WS = 2 * Q * SW;                     // W region of one component
   static constexpr int R1 = DIM == 3 ? cmax3((FLATZ ? VS : 1) * ZS, 2 * Q * Q * Q, (FLATZ ? VS : 1) * WS) : 0;
-  static constexpr int R2 = DIM == 3 ? cmax3(NY * P * SY, 3 * Q * SA, 0) : 2 * Q * S2;
+  static constexpr int R2 = DIM == 3 ? cmax3(NY * P * SY, 3 * Q * SA, COLLOC ? Q * Q * Q : 0) : 2 * Q * S2;
   // per-cell region
   static constexpr int U = 0;
   static constexpr int O1 = U + VS * ND;
@@ -201,6 +204,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   using L = TensorLayout<DIM, P, Q, VS, DIRECT, tensor_block<MINB>(), ASYNC>;
   constexpr int TS = L::TS, CPB = L::CPB, ND = L::ND, NV = L::NV, RU = L::RU;
   constexpr bool COLLOC = L::COLLOC;
+  constexpr bool CPEN = COLLOC && FE_TK_CPENCIL && Q >= 6 && VS == 1;   // pencil-stage collocation derivatives
   constexpr int QQ = Q * Q;
   extern __shared__ double smem_all[];
 
@@ -529,6 +533,42 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             (void)c;
           }
           team_sync();
+          if constexpr (CPEN) {
+            // d/deta, d/dzeta as pencil stages too: thread (a, c) differentiates the
+            // eta line U[a][c][.] and thread (a, b) the zeta line U[a][.][b] -- every
+            // table entry a compile-time (uniform) operand, Q loads + Q stores per Q^2
+            // FMAs instead of one shared load per FMA and lane-indexed Dc rows
+            if (active) {
+              const int a = t % Q, o = t / Q;
+              double pen[Q];
+#pragma unroll
+              for (int e = 0; e < Q; ++e) pen[e] = s1[a * QQ + o * Q + e];
+#pragma unroll
+              for (int b = 0; b < Q; ++b) {
+                double s = 0.0;
+#pragma unroll
+                for (int e = 0; e < Q; ++e) s = fma(p.Dc[b][e], pen[e], s);
+                s2[a * QQ + o * Q + b] = s;                       // d/deta   [a][c][b]
+              }
+#pragma unroll
+              for (int e = 0; e < Q; ++e) pen[e] = s1[a * QQ + e * Q + o];
+#pragma unroll
+              for (int c = 0; c < Q; ++c) {
+                double s = 0.0;
+#pragma unroll
+                for (int e = 0; e < Q; ++e) s = fma(p.Dc[c][e], pen[e], s);
+                s1[Q * QQ + a * QQ + c * Q + o] = s;              // d/dzeta  [a][c][b]
+              }
+            }
+            team_sync();
+            if (active) {
+#pragma unroll
+              for (int a = 0; a < Q; ++a) {
+                g[comp][1][a] = s2[a * QQ + t];
+                g[comp][2][a] = s1[Q * QQ + a * QQ + t];
+              }
+            }
+          } else {
           // d/deta, d/dzeta with Dc across the pencils of the team
           if (active) {
             const int b = t % Q, c = t / Q;
@@ -543,6 +583,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               g[comp][1][a] = sa;
               g[comp][2][a] = sb;
             }
+          }
           }
           team_sync();
         } else {
@@ -748,6 +789,32 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             }
           }
           team_sync();
+          if constexpr (CPEN) {
+            // Dc^T along eta by thread (a, c), along zeta by thread (a, b), in place
+            if (active) {
+              const int a = t % Q, o = t / Q;
+              double pen[Q];
+#pragma unroll
+              for (int e = 0; e < Q; ++e) pen[e] = s1[a * QQ + o * Q + e];
+#pragma unroll
+              for (int b = 0; b < Q; ++b) {
+                double s = 0.0;
+#pragma unroll
+                for (int e = 0; e < Q; ++e) s = fma(p.Dc[e][b], pen[e], s);
+                s1[a * QQ + o * Q + b] = s;
+              }
+#pragma unroll
+              for (int e = 0; e < Q; ++e) pen[e] = s1[Q * QQ + a * QQ + e * Q + o];
+#pragma unroll
+              for (int c = 0; c < Q; ++c) {
+                double s = 0.0;
+#pragma unroll
+                for (int e = 0; e < Q; ++e) s = fma(p.Dc[e][c], pen[e], s);
+                s1[Q * QQ + a * QQ + c * Q + o] = s;
+              }
+            }
+            team_sync();
+          }
           // V = Dc^T F0 (local) + Dc^T F1 (eta) + Dc^T F2 (zeta); x^T: A = B^T V
           if (active) {
             const int b = t % Q, c = t / Q;
@@ -756,10 +823,15 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             for (int a = 0; a < Q; ++a) {
               double s = 0.0;
 #pragma unroll
-              for (int e = 0; e < Q; ++e) {
-                s = fma(p.Dc[e][a], g[comp][0][e], s);
-                s = fma(p.Dc[e][b], s1[a * QQ + c * Q + e], s);
-                s = fma(p.Dc[e][c], s1[Q * QQ + a * QQ + e * Q + b], s);
+              for (int e = 0; e < Q; ++e) s = fma(p.Dc[e][a], g[comp][0][e], s);
+              if constexpr (CPEN) {
+                s += s1[a * QQ + t] + s1[Q * QQ + a * QQ + t];
+              } else {
+#pragma unroll
+                for (int e = 0; e < Q; ++e) {
+                  s = fma(p.Dc[e][b], s1[a * QQ + c * Q + e], s);
+                  s = fma(p.Dc[e][c], s1[Q * QQ + a * QQ + e * Q + b], s);
+                }
               }
               V[a] = s;
             }
@@ -914,6 +986,12 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #ifndef FE_TK_Q6_MINB
 #define FE_TK_Q6_MINB 2
 #endif
+#ifndef FE_TK_Q5C_MINB
+#define FE_TK_Q5C_MINB 1002
+#endif
+#ifndef FE_TK_Q6C_MINB
+#define FE_TK_Q6C_MINB 2
+#endif
 #ifndef FE_TK_EQ2_MINB
 #define FE_TK_EQ2_MINB 192   // 192-thread CTAs, 168 registers: C4-hex-Q2 0.504 -> 0.466 ms (profiles/r02/ab_tensor_blocks.txt)
 #endif
@@ -925,6 +1003,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 4, 5, 5, 2),                             \
   TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, FE_TK_Q5_MINB),                \
   TVD(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, FE_TK_Q6_MINB),                \
+  TVC(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 5, 6, 6, FE_TK_Q5C_MINB),               \
+  TVC(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 6, 7, 7, FE_TK_Q6C_MINB),               \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 1, 2, 3, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 2, 3, 4, 1),                             \
   TV(FE_FORM_LAPLACIAN_SCALAR, FE_CELL_HEXAHEDRON, 3, 3, 4, 5, 1),                             \

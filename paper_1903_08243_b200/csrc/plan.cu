@@ -1234,6 +1234,9 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
 #define TV(FORM, CELL, DIM, K, P, Q, MINB)                                                   \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised", 256,                 \
    tensor_prepare<FORM, DIM, P, Q, MINB, false>, tensor_launch<FORM, DIM, P, Q, MINB, false>}
+#define TVC(FORM, CELL, DIM, K, P, Q, MINB)                                                  \
+  {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 19, "sum_factorised_colloc", 256,          \
+   tensor_prepare<FORM, DIM, P, Q, MINB, false>, tensor_launch<FORM, DIM, P, Q, MINB, false>}
 #define TVD(FORM, CELL, DIM, K, P, Q, MINB)                                                  \
   {FORM, CELL, K, (DIM == 3 ? Q * Q * Q : Q * Q), 20, "sum_factorised_direct", 256,          \
    tensor_prepare<FORM, DIM, P, Q, MINB, true>, tensor_launch<FORM, DIM, P, Q, MINB, true>}
@@ -1528,6 +1531,7 @@ const Variant* select_variant(const fe_plan* p, uint32_t flags) {
     if (v.priority == 26 && getenv("FE_NO_PAIR")) continue;
     if (v.priority == 27 && getenv("FE_NO_HEXQ1")) continue;
     if (v.priority == 28 && getenv("FE_NO_HEXQ2")) continue;
+    if (getenv("FE_TK_COLLOC56") && !strcmp(v.name, "sum_factorised_direct")) continue;   // experiments
     if (v.priority == 29 && !getenv("FE_HEXLP")) continue;   // opt-in until measured
     if (v.priority == 6 && getenv("FE_NO_VTX")) continue;
     // patch aggregation measured slower than plain REDs (profiles/r01/sweep_patch.jsonl):

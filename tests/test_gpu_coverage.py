@@ -111,6 +111,9 @@ C3_KERNELS = [
     ("C3-Q3", {"FE_HEXLP": "1"}, "sum_factorised_lane_plane"),
     ("C3-Q4", {"FE_HEXLP": "1"}, "sum_factorised_lane_plane"),
     ("C3-Q4", {}, "sum_factorised_plane"),
+    ("C3-Q5", {}, "sum_factorised_direct"),
+    ("C3-Q5", {"FE_TK_COLLOC56": "1"}, "sum_factorised_colloc"),
+    ("C3-Q6", {"FE_TK_COLLOC56": "1"}, "sum_factorised_colloc"),
 ]
 
 
