@@ -495,6 +495,41 @@ def run_e2e_distributed(ops, steps, dev):
                        "synchronised; bytes summed over ranks; max over ranks"}
 
 
+def graph_throughput(ops, names=("C1", "C2-P1", "C3-Q1"), reps=50):
+    """The launch-latency-bound operators (10-25 us per apply: VERDICT item 10)
+    as they run inside a captured solver iteration: ``reps`` overwrite applies
+    in one CUDA graph, microseconds per apply (launch overhead amortised,
+    inputs L2-resident).  Labelled separately: NOT the protocol of ``value``
+    (single cold-L2 applies), which stays the reported number."""
+    import torch
+    out = {"protocol": f"{reps} overwrite applies captured in one CUDA graph, best of 10 replays, warm L2"}
+    for op in ops:
+        if op["name"] not in names:
+            continue
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                op["run"](op["u"], op["y"])              # warm-up on the capture stream
+                with torch.cuda.graph(g, stream=side):
+                    for _ in range(reps):
+                        op["run"](op["u"], op["y"])
+            torch.cuda.current_stream().wait_stream(side)
+            best = 1e9
+            for _ in range(10):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            out[op["name"]] = round(best * 1e3 / reps, 2)
+        except Exception as e:  # noqa: BLE001 -- capture unsupported: say why
+            out[op["name"]] = "capture failed: " + str(e)[:80]
+    return out if len(out) > 1 else None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -640,6 +675,7 @@ def run_ours(args):
             },
             "e2e": {"value": round(flop_step * e2e_steps / t_e2e / 1e9, 3), "unit": "GFLOP/s",
                     "steps": e2e_steps, **e2e_info},
+            "graph_us_per_apply": graph_throughput(ops) if world == 1 else None,
             "gpu_launches": launches,
             "gpu_launches_source": "fe_launch_count() difference around the timed region, summed over ranks",
             "clocks": clk.summary(),
