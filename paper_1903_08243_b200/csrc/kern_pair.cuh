@@ -24,8 +24,11 @@
 
 namespace fe {
 
+#ifndef FE_PAIR_SYM
+#define FE_PAIR_SYM 1   // C4-quad-Q3 0.3205 -> 0.2960 ms, Q4 0.5808 -> 0.5746 (profiles/r02/ab_pair_sym.txt)
+#endif
 #ifndef FE_PAIR_RELOAD
-#define FE_PAIR_RELOAD 0   // 1: re-read the dof ids for the scatter instead of holding them in registers
+#define FE_PAIR_RELOAD 1   // 1: re-read the dof ids for the scatter instead of holding them in registers
 #endif
 #ifndef FE_PAIR_BLOCK
 #define FE_PAIR_BLOCK 32  // one warp per CTA: measured best (profiles/r01/sweep_warps.txt)
@@ -43,6 +46,19 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   const unsigned live = __ballot_sync(0xffffffffu, cell < p.end);  // pairs live or die together
   if (cell >= p.end) return;
   const int64_t cs = p.mesh.nc_stride;
+#if FE_PAIR_SYM
+  // mirror-symmetric table reads (verified at plan time): half the distinct
+  // constants, so the uniform registers hold them across the unrolled rows
+  auto TB = [&](int q, int i) { return 2 * q < Q ? p.B[q][i] : p.B[Q - 1 - q][P - 1 - i]; };
+  auto TD = [&](int q, int i) { return 2 * q < Q ? p.D[q][i] : -p.D[Q - 1 - q][P - 1 - i]; };
+  auto TX = [&](int q) { return 2 * q < Q ? p.x[q] : 1.0 - p.x[Q - 1 - q]; };
+  auto TW = [&](int q) { return 2 * q < Q ? p.w[q] : p.w[Q - 1 - q]; };
+#else
+  auto TB = [&](int q, int i) { return p.B[q][i]; };
+  auto TD = [&](int q, int i) { return p.D[q][i]; };
+  auto TX = [&](int q) { return p.x[q]; };
+  auto TW = [&](int q) { return p.w[q]; };
+#endif
 
   const int32_t* mrow = p.maplex + (int64_t)cell * NDS;
   int dof[NDS];
@@ -81,15 +97,15 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
 #pragma unroll
   for (int b = 0; b < Q; ++b) {
-    const double eta = p.x[b], le = 1.0 - eta, wb = p.w[b];
+    const double eta = TX(b), le = 1.0 - eta, wb = TW(b);
     double Y0[P], Y1[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int j = 0; j < P; ++j) {
-        s0 = fma(p.B[b][j], u[j][i], s0);
-        s1 = fma(p.D[b][j], u[j][i], s1);
+        s0 = fma(TB(b, j), u[j][i], s0);
+        s1 = fma(TD(b, j), u[j][i], s1);
       }
       Y0[i] = s0;
       Y1[i] = s1;
@@ -106,19 +122,19 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
     for (int i = 0; i < P; ++i) Z0[i] = Z1[i] = 0.0;
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
-      const double xi = p.x[a];
+      const double xi = TX(a);
       double gx = 0.0, gy = 0.0;  // du_c/dxi, du_c/deta
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        gx = fma(p.D[a][i], Y0[i], gx);
-        gy = fma(p.B[a][i], Y1[i], gy);
+        gx = fma(TD(a, i), Y0[i], gx);
+        gy = fma(TB(a, i), Y1[i], gy);
       }
       // adjugate form: with adj = det J^-1 = [[J11, -J01], [-J10, J00]] the
       // flux tw sigma(G) J^-T equals (w / |det|) sigma(g adj) adj^T, so no
       // inverse is formed; det is linear in xi along the row
       const double J01 = fma(xi, d1[0], j1[0]), J11 = fma(xi, d1[1], j1[1]);
       const double det = fma(xi, ddet, det0);
-      const double sc = (p.w[a] * wb) * recip<(P <= 4)>(fabs(det));  // fast at Q3, IEEE at Q4 (measured)
+      const double sc = (TW(a) * wb) * recip<(P <= 4)>(fabs(det));  // fast at Q3, IEEE at Q4 (measured)
       const double mu = sc * fma(xi, dm, m0), lam = sc * fma(xi, dl, l0);
       // own row of g adj, the partner's by shuffle
       const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
@@ -130,14 +146,14 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       const double f0 = t0 * J11 - t1 * J01, f1 = t1 * J0[0] - t0 * J0[1];
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        Z0[i] = fma(p.D[a][i], f0, Z0[i]);
-        Z1[i] = fma(p.B[a][i], f1, Z1[i]);
+        Z0[i] = fma(TD(a, i), f0, Z0[i]);
+        Z1[i] = fma(TB(a, i), f1, Z1[i]);
       }
     }
 #pragma unroll
     for (int j = 0; j < P; ++j)
 #pragma unroll
-      for (int i = 0; i < P; ++i) y[j][i] = fma(p.B[b][j], Z0[i], fma(p.D[b][j], Z1[i], y[j][i]));
+      for (int i = 0; i < P; ++i) y[j][i] = fma(TB(b, j), Z0[i], fma(TD(b, j), Z1[i], y[j][i]));
   }
   griddep_wait();
 #pragma unroll

@@ -41,6 +41,9 @@
 #ifndef FE_PLANE_MONO
 #define FE_PLANE_MONO 1   // monomial trilinear geometry (round 2)
 #endif
+#ifndef FE_PLANE_SYM
+#define FE_PLANE_SYM 1
+#endif
 #ifndef FE_PLANE_RCP
 #define FE_PLANE_RCP 1    // MUFU-seeded reciprocal instead of the IEEE division at P = 4 (C3-Q3 224.2 -> 222.2 us;
 #endif                    // slower at P = 5: 529 -> 565 us, profiles/r02/ab_plane_rcp.txt)
@@ -127,6 +130,14 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   int32_t* sM0 = reinterpret_cast<int32_t*>(wbase + L::M0);
 
   const int64_t ncs = p.mesh.nc_stride;
+  // mirror-symmetric table reads (verified at plan time) when the column loop
+  // is fully unrolled (every index compile-time): half the distinct constants,
+  // so all of them stay in uniform registers across the persistent loop
+  constexpr bool SYM = FE_PLANE_SYM && COLU == Q;
+  auto TB = [&](int q, int i) { return (!SYM || 2 * q < Q) ? p.B[q][i] : p.B[Q - 1 - q][P - 1 - i]; };
+  auto TD = [&](int q, int i) { return (!SYM || 2 * q < Q) ? p.D[q][i] : -p.D[Q - 1 - q][P - 1 - i]; };
+  auto TXc = [&](int q) { return (!SYM || 2 * q < Q) ? p.x[q] : 1.0 - p.x[Q - 1 - q]; };
+  auto TWc = [&](int q) { return (!SYM || 2 * q < Q) ? p.w[q] : p.w[Q - 1 - q]; };
   const int nwb = (p.end - p.start + TPW - 1) / TPW;  // warp batches
   const int GW = gridDim.x * WARPS;
   auto cell_of = [&](int wb) { return p.start + wb * TPW + T; };
@@ -244,8 +255,8 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
           for (int k = 0; k < P; ++k) {
-            s0 = fma(p.B[c][k], pu[k][i], s0);
-            s1 = fma(p.D[c][k], pu[k][i], s1);
+            s0 = fma(TB(c, k), pu[k][i], s0);
+            s1 = fma(TD(c, k), pu[k][i], s1);
           }
           z0[i] = s0;
           z1[i] = s1;
@@ -255,9 +266,9 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           double v0 = 0.0, v1 = 0.0, v2 = 0.0;
 #pragma unroll
           for (int i = 0; i < P; ++i) {
-            v0 = fma(p.B[a][i], z0[i], v0);
-            v1 = fma(p.D[a][i], z0[i], v1);
-            v2 = fma(p.B[a][i], z1[i], v2);
+            v0 = fma(TB(a, i), z0[i], v0);
+            v1 = fma(TD(a, i), z0[i], v1);
+            v2 = fma(TB(a, i), z1[i], v2);
           }
           sT[a * SA + t] = v0;
           sT[SF + a * SA + t] = v1;
@@ -274,7 +285,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           V1[j] = sT[SF + t * SA + j];
           V2[j] = sT[2 * SF + t * SA + j];
         }
-        const double xi = p.x[t], zeta = p.x[c], wac = p.w[t] * p.w[c];
+        const double xi = p.x[t], zeta = TXc(c), wac = p.w[t] * TWc(c);
         const double lx0 = 1.0 - xi, lz0 = 1.0 - zeta;
         // d/dxi column: linear in eta; d/deta: constant on the line; d/dzeta: linear in eta
         double g0[3], dg[3], J1[3], h0[3], dh[3];
@@ -308,13 +319,13 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         for (int j = 0; j < P; ++j) W0[j] = W1[j] = W2[j] = 0.0;
 #pragma unroll
         for (int b = 0; b < Q; ++b) {
-          const double eta = p.x[b];
+          const double eta = TXc(b);
           double gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            gx = fma(p.B[b][j], V1[j], gx);
-            gy = fma(p.D[b][j], V0[j], gy);
-            gz = fma(p.B[b][j], V2[j], gz);
+            gx = fma(TB(b, j), V1[j], gx);
+            gy = fma(TD(b, j), V0[j], gy);
+            gz = fma(TB(b, j), V2[j], gz);
           }
           double J[3][3];
 #pragma unroll
@@ -334,7 +345,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wac * p.w[b]) * recip<(FE_PLANE_RCP != 0) && P == 4>(fabs(det));
+          const double s = (wac * TWc(b)) * recip<(FE_PLANE_RCP != 0) && P == 4>(fabs(det));
           // v = adj^T g (= det * physical gradient), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;
@@ -344,9 +355,9 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double fz = s * (a20 * v0 + a21 * v1 + a22 * v2);
 #pragma unroll
           for (int j = 0; j < P; ++j) {
-            W1[j] = fma(p.B[b][j], fx, W1[j]);
-            W0[j] = fma(p.D[b][j], fy, W0[j]);
-            W2[j] = fma(p.B[b][j], fz, W2[j]);
+            W1[j] = fma(TB(b, j), fx, W1[j]);
+            W0[j] = fma(TD(b, j), fy, W0[j]);
+            W2[j] = fma(TB(b, j), fz, W2[j]);
           }
         }
 #pragma unroll
@@ -367,15 +378,15 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double w0 = sT[a * SA + t], w1 = sT[SF + a * SA + t], w2 = sT[2 * SF + a * SA + t];
 #pragma unroll
           for (int i = 0; i < P; ++i) {
-            zb0[i] = fma(p.B[a][i], w0, zb0[i]);
-            zb0[i] = fma(p.D[a][i], w1, zb0[i]);
-            zb1[i] = fma(p.B[a][i], w2, zb1[i]);
+            zb0[i] = fma(TB(a, i), w0, zb0[i]);
+            zb0[i] = fma(TD(a, i), w1, zb0[i]);
+            zb1[i] = fma(TB(a, i), w2, zb1[i]);
           }
         }
 #pragma unroll
         for (int k = 0; k < P; ++k)
 #pragma unroll
-          for (int i = 0; i < P; ++i) yp[k][i] = fma(p.B[c][k], zb0[i], fma(p.D[c][k], zb1[i], yp[k][i]));
+          for (int i = 0; i < P; ++i) yp[k][i] = fma(TB(c, k), zb0[i], fma(TD(c, k), zb1[i], yp[k][i]));
       }
     }
     if (jt) {

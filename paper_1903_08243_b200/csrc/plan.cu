@@ -968,6 +968,19 @@ int plane_prepare(fe_plan* p) {
     delete hp;
     return rc;
   }
+  if constexpr (!V1 && FE_PLANE_SYM && CU == Q) {
+    // the fully unrolled plane kernel reads the mirror-symmetric half of the 1D tables
+    for (int q = 0; q < Q; ++q) {
+      bool ok = std::fabs(hp->x[q] - (1.0 - hp->x[Q - 1 - q])) <= 1e-13 && std::fabs(hp->w[q] - hp->w[Q - 1 - q]) <= 1e-13;
+      for (int i = 0; i < P; ++i)
+        ok = ok && std::fabs(hp->B[q][i] - hp->B[Q - 1 - q][P - 1 - i]) <= 1e-12 &&
+             std::fabs(hp->D[q][i] + hp->D[Q - 1 - q][P - 1 - i]) <= 1e-11;
+      if (!ok) {
+        delete hp;
+        return fail(FE_EUNSUPPORTED, "plane kernel needs mirror-symmetric 1D tables");
+      }
+    }
+  }
   p->host_params = hp;
   p->host_params_bytes = sizeof(TP);
   p->tables_bytes = (size_t)WARPS * L::WARP_DOUBLES * sizeof(double);
@@ -1171,14 +1184,20 @@ int pair_prepare(fe_plan* p) {
   const char* env = getenv("FE_PAIR_CFG");
   p->dmma_cfg = env ? atoi(env) : FE_PAIR_CFG;
   if (p->dmma_cfg < 0 || p->dmma_cfg > 1) p->dmma_cfg = FE_PAIR_CFG;
-  // the pipelined kernel reads the mirror-symmetric half of the 1D tables
+  // the pipelined kernel (and the round-1 kernel under FE_PAIR_SYM) reads the
+  // mirror-symmetric half of the 1D tables
+  bool sym = true;
   for (int q = 0; q < Q; ++q) {
     if (std::fabs(hp->x[q] - (1.0 - hp->x[Q - 1 - q])) > 1e-13 || std::fabs(hp->w[q] - hp->w[Q - 1 - q]) > 1e-13)
-      p->dmma_cfg = 0;
+      sym = false;
     for (int i = 0; i < P; ++i)
       if (std::fabs(hp->B[q][i] - hp->B[Q - 1 - q][P - 1 - i]) > 1e-12 ||
           std::fabs(hp->D[q][i] + hp->D[Q - 1 - q][P - 1 - i]) > 1e-11)
-        p->dmma_cfg = 0;
+        sym = false;
+  }
+  if (!sym) {
+    if (FE_PAIR_SYM) return fail(FE_EUNSUPPORTED, "pair kernel needs mirror-symmetric 1D tables");
+    p->dmma_cfg = 0;
   }
   int dev = 0, sms = 0;
   CUDA_TRY(cudaGetDevice(&dev));
