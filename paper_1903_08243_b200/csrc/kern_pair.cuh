@@ -24,6 +24,9 @@
 
 namespace fe {
 
+#ifndef FE_PAIR_NOSEL
+#define FE_PAIR_NOSEL 1
+#endif
 #ifndef FE_PAIR_SYM
 #define FE_PAIR_SYM 1   // C4-quad-Q3 0.3205 -> 0.2960 ms, Q4 0.5808 -> 0.5746 (profiles/r02/ab_pair_sym.txt)
 #endif
@@ -74,6 +77,18 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   for (int v = 0; v < 4; ++v) {
     const int vid = __ldg(p.mesh.vmap + v * cs + cell);
     load_vertex<2>(p.mesh.coords, vid, X[v]);
+#if FE_PAIR_NOSEL
+    // lane 1 works in the frame with the physical axes swapped (its own
+    // component's axis first): both lanes then run the same formulas on
+    // (own-axis, cross-axis) pairs and the per-point selects on c disappear.
+    // The swap flips the sign of det J in lane 1, so the partner's values
+    // arrive with the opposite sign convention and are SUBTRACTED below.
+    {
+      const double x0 = X[v][0], x1 = X[v][1];
+      X[v][0] = c ? x1 : x0;
+      X[v][1] = c ? x0 : x1;
+    }
+#endif
     if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
       mv[v] = __ldg(p.mu + vid);
       lv[v] = __ldg(p.lam + vid);
@@ -139,10 +154,16 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       // own row of g adj, the partner's by shuffle
       const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
       const double o0 = __shfl_xor_sync(live, g0, 1), o1 = __shfl_xor_sync(live, g1, 1);
+#if FE_PAIR_NOSEL
+      // (own, cross) = (g0, g1): trace = own + partner's own, shear = cross + partner's cross
+      const double tr = g0 - o0;
+      const double t0 = fma(mu, g0 + g0, lam * tr), t1 = mu * (g1 - o1);
+#else
       const double tr = c ? (g1 + o0) : (g0 + o1);
       // (G + G^T)[c][:] and the Lame stress row (the scale folded into mu, lambda)
       const double s0 = g0 + (c ? o1 : g0), s1 = g1 + (c ? g1 : o0);
       const double t0 = fma(mu, s0, c ? 0.0 : lam * tr), t1 = fma(mu, s1, c ? lam * tr : 0.0);
+#endif
       const double f0 = t0 * J11 - t1 * J01, f1 = t1 * J0[0] - t0 * J0[1];
 #pragma unroll
       for (int i = 0; i < P; ++i) {
