@@ -24,6 +24,9 @@
 
 namespace fe {
 
+#ifndef FE_PAIR_RCP_MAXP
+#define FE_PAIR_RCP_MAXP 5   // MUFU-seeded reciprocal up to this P: with the select-free kernel it wins at P = 5 too (0.5255 -> 0.4967 ms, profiles/r02/ab_pair_rcp.txt)
+#endif
 #ifndef FE_PAIR_NOSEL
 #define FE_PAIR_NOSEL 1
 #endif
@@ -149,7 +152,7 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       // inverse is formed; det is linear in xi along the row
       const double J01 = fma(xi, d1[0], j1[0]), J11 = fma(xi, d1[1], j1[1]);
       const double det = fma(xi, ddet, det0);
-      const double sc = (TW(a) * wb) * recip<(P <= 4)>(fabs(det));  // fast at Q3, IEEE at Q4 (measured)
+      const double sc = (TW(a) * wb) * recip<(P <= FE_PAIR_RCP_MAXP)>(fabs(det));  // fast at Q3, IEEE at Q4 (measured)
       const double mu = sc * fma(xi, dm, m0), lam = sc * fma(xi, dl, l0);
       // own row of g adj, the partner's by shuffle
       const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
@@ -361,7 +364,7 @@ pair_pipe_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           }
           const double J01 = fma(xi, d1[0], j1[0]), J11 = fma(xi, d1[1], j1[1]);
           const double det = fma(xi, ddet, det0);
-          const double sc = (TW(a) * wb) * recip<(P <= 4)>(fabs(det));
+          const double sc = (TW(a) * wb) * recip<(P <= FE_PAIR_RCP_MAXP)>(fabs(det));
           const double mu = sc * fma(xi, dm, mm0), lam = sc * fma(xi, dl, l0);
           const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
           const double o0 = __shfl_xor_sync(live, g0, 1), o1 = __shfl_xor_sync(live, g1, 1);

@@ -345,7 +345,7 @@ plane_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           const double a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
           const double a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
           const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
-          const double s = (wac * TWc(b)) * recip<(FE_PLANE_RCP != 0) && P == 4>(fabs(det));
+          const double s = (wac * TWc(b)) * recip<(FE_PLANE_RCP == 2) || ((FE_PLANE_RCP == 1) && P == 4)>(fabs(det));
           // v = adj^T g (= det * physical gradient), f = s adj v
           const double v0 = a00 * gx + a10 * gy + a20 * gz;
           const double v1 = a01 * gx + a11 * gy + a21 * gz;

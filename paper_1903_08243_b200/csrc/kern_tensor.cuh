@@ -106,6 +106,9 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 #ifndef FE_TK_FLATZ
 #define FE_TK_FLATZ 0   // 1: one z stage for all components of a vector form; measured neutral
 #endif                  // (C4-hex-Q2 0.456 -> 0.460 ms, C4-hex-Q3 1.244 -> 1.239 ms, profiles/r02/ab_tensor_flatz.txt)
+#ifndef FE_TK_RCPALL
+#define FE_TK_RCPALL 0
+#endif
 #ifndef FE_TK_CPENCIL
 #define FE_TK_CPENCIL 1
 #endif
@@ -204,6 +207,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   using L = TensorLayout<DIM, P, Q, VS, DIRECT, tensor_block<MINB>(), ASYNC>;
   constexpr int TS = L::TS, CPB = L::CPB, ND = L::ND, NV = L::NV, RU = L::RU;
   constexpr bool COLLOC = L::COLLOC;
+  constexpr bool FASTR = FE_TK_RCPALL || !DIRECT;   // MUFU-seeded reciprocal (IEEE division in the DIRECT variants: measured)
   constexpr bool CPEN = COLLOC && FE_TK_CPENCIL && Q >= 6 && VS == 1;   // pencil-stage collocation derivatives
   constexpr int QQ = Q * Q;
   extern __shared__ double smem_all[];
@@ -732,8 +736,8 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         // linear gradient forms: Ji holds adj(J), the weight w / |det J|
         // absorbs both 1/det factors (no inverse formed)
         constexpr bool ADJ = TK_ADJ && linear_grad_form(FORM);
-        const double det = ADJ ? det_adj<DIM>(J, Ji) : det_inv<DIM, !DIRECT>(J, Ji);
-        const double tw = ADJ ? (TW(a) * wbc) * recip<!DIRECT>(fabs(det)) : (TW(a) * wbc) * fabs(det);
+        const double det = ADJ ? det_adj<DIM>(J, Ji) : det_inv<DIM, FASTR>(J, Ji);
+        const double tw = ADJ ? (TW(a) * wbc) * recip<FASTR>(fabs(det)) : (TW(a) * wbc) * fabs(det);
         double mu = p.p0, lam = p.p1;
         if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
           mu = fma(xi, dm, m0);
@@ -746,7 +750,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 #pragma unroll
           for (int d = 0; d < DIM; ++d) gq[comp][d] = g[comp][d][a];
         }
-        pointwise<FORM, DIM, VS, !DIRECT>(Ji, tw, uq, gq, mu, lam, cv, cg);
+        pointwise<FORM, DIM, VS, FASTR>(Ji, tw, uq, gq, mu, lam, cv, cg);
 #pragma unroll
         for (int comp = 0; comp < VS; ++comp)
 #pragma unroll
