@@ -6,6 +6,7 @@
 // template instantiations instead of generated C -- plus the bound mesh in
 // the GPU layout (element-batched SoA maps, padded coordinates).
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <omp.h>
@@ -161,6 +162,12 @@ struct fe_plan {
   std::vector<int32_t> chunk_cell;
   std::vector<uint64_t> chunk_mask;
   int64_t hblock = 0;
+  // two-phase overwrite apply (fe_apply): the zero-fill of the blocks of y the
+  // first cell chunk scatters into runs first, the rest of the fill runs on a
+  // side stream underneath that chunk's arithmetic
+  cudaStream_t fill_stream = nullptr;
+  cudaEvent_t ev_fill_a = nullptr, ev_fill_b = nullptr;
+  std::mutex fill_mutex;
   double* d_u = nullptr;
   double* d_y = nullptr;
   double* d_y0 = nullptr;
@@ -1440,6 +1447,22 @@ __global__ void __launch_bounds__(256) k_zero_pdl(double* __restrict__ y, int64_
   if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) y[n - 1] = 0.0;
 }
 
+// Zero-fill of the blocks of y (bsz entries each, bsz % 2 == 0) selected by
+// mask; lets a dependent kernel launch early like k_zero_pdl.
+__global__ void __launch_bounds__(256) k_zero_blocks(double* __restrict__ y, int64_t n, int64_t bsz,
+                                                     unsigned long long mask, int nblk) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  for (int b = 0; b < nblk; ++b) {
+    if (!((mask >> b) & 1)) continue;
+    const int64_t a = (int64_t)b * bsz, e = a + bsz < n ? a + bsz : n;
+    double2* y2 = reinterpret_cast<double2*>(y + a);
+    const int64_t n2 = (e - a) / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+      y2[i] = make_double2(0.0, 0.0);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ((e - a) & 1)) y[e - 1] = 0.0;
+  }
+}
+
 __global__ void k_add(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1914,6 +1937,19 @@ int fe_plan_bind_mesh(fe_plan* p, int32_t ncells, int32_t nverts, int64_t ngloba
   return FE_OK;
 }
 
+// the two-phase overwrite path pays when y is large and the range straddles
+// the first cell chunk (FE_FILL_2PHASE_MB: threshold in MB, 0 disables)
+static bool fill_two_phase(const fe_plan* p, int32_t start, int32_t end, int64_t ny) {
+  // default off: measured SLOWER than the one-phase programmatic-dependent fill (C3-Q3 0.212 -> 0.238 ms,
+  // C4-quad-Q3 0.271 -> 0.289 ms, profiles/r02/ab_fill_2phase.txt) -- the second operator launch and the
+  // side-stream fill's CTAs cost more than the 2-10% of the apply the fill takes
+  static const long mb = getenv("FE_FILL_2PHASE_MB") ? atol(getenv("FE_FILL_2PHASE_MB")) : 0;
+  if (mb <= 0 || p->hblock <= 0 || p->chunk_mask.empty() || p->chunk_cell.size() < 3) return false;
+  if (ny * (int64_t)sizeof(double) < (int64_t)mb << 20 || (p->hblock & 1)) return false;
+  const int32_t ca = p->chunk_cell[1];
+  return start < ca && ca < end && start >= p->chunk_cell[0];
+}
+
 int fe_apply(const fe_plan* p, int32_t start, int32_t end, double* y, const double* u,
              const double* c0, const double* c1, uint32_t apply_flags, void* stream) {
   if (!p) return fail(FE_EINVAL, "null plan");
@@ -1929,6 +1965,44 @@ int fe_apply(const fe_plan* p, int32_t start, int32_t end, double* y, const doub
   const int64_t ny = (int64_t)p->vs * p->nglobal;
   if ((apply_flags & FE_APPLY_OVERWRITE) && (end == start || (reinterpret_cast<uintptr_t>(y) & 15) ||
                                               getenv("FE_NO_PDL"))) {
+    CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)ny * sizeof(double), s));
+  } else if ((apply_flags & FE_APPLY_OVERWRITE) && fill_two_phase(p, start, end, ny)) {
+    // Large y (the fill is 2-10% of the apply and the operator is FP64-bound):
+    // hide the fill under the arithmetic.  Phase A: zero the blocks of y the
+    // first cell chunk scatters into (chunk_mask[0], found at bind) and start
+    // that chunk as a programmatic dependent of this short fill; the rest of y
+    // is zeroed on a side stream while the chunk computes, and the remaining
+    // cells are launched behind both.  Serialised per plan (try_lock): a
+    // concurrent overwrite apply on the same plan takes the one-phase path.
+    fe_plan* mp = const_cast<fe_plan*>(p);
+    std::unique_lock<std::mutex> lk(mp->fill_mutex, std::try_to_lock);
+    if (lk.owns_lock()) {
+      if (!mp->fill_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&mp->fill_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&mp->ev_fill_a, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&mp->ev_fill_b, cudaEventDisableTiming));
+      }
+      const int nblk = (int)((ny + p->hblock - 1) / p->hblock);
+      const uint64_t all = nblk >= 64 ? ~0ull : ((1ull << nblk) - 1);
+      const uint64_t ma = p->chunk_mask[0] & all, mb = all & ~ma;
+      const int32_t ca = p->chunk_cell[1];
+      const unsigned grid = 148 * 4;
+      // both fills are ordered after what is already queued on s (ev_fill_a);
+      // no node sits between fill A and the first operator launch, so that
+      // launch stays its programmatic dependent
+      CUDA_TRY(cudaEventRecord(mp->ev_fill_a, s));
+      CUDA_TRY(cudaStreamWaitEvent(mp->fill_stream, mp->ev_fill_a, 0));
+      k_zero_blocks<<<grid, 256, 0, s>>>(y, ny, p->hblock, ma, nblk);
+      k_zero_blocks<<<grid, 256, 0, mp->fill_stream>>>(y, ny, p->hblock, mb, nblk);
+      CUDA_TRY(cudaEventRecord(mp->ev_fill_b, mp->fill_stream));
+      CUDA_TRY(cudaGetLastError());
+      g_pdl_next = true;
+      int rc = p->var->launch(p, start, ca, y, u, c0, c1, s);
+      g_pdl_next = false;
+      CUDA_TRY(cudaStreamWaitEvent(s, mp->ev_fill_b, 0));
+      if (!rc) rc = p->var->launch(p, ca, end, y, u, c0, c1, s);
+      return rc;
+    }
     CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)ny * sizeof(double), s));
   } else if (apply_flags & FE_APPLY_OVERWRITE) {
     // zero-fill as a kernel the operator launch depends on programmatically:
@@ -2206,6 +2280,9 @@ void fe_plan_destroy(fe_plan* p) {
   cudaFree(p->d_y0);
   cudaFree(p->d_c0);
   cudaFree(p->d_c1);
+  if (p->fill_stream) cudaStreamDestroy(p->fill_stream);
+  if (p->ev_fill_a) cudaEventDestroy(p->ev_fill_a);
+  if (p->ev_fill_b) cudaEventDestroy(p->ev_fill_b);
   if (p->hstream) cudaStreamDestroy(p->hstream);
   if (p->hstream2) cudaStreamDestroy(p->hstream2);
   if (p->ev_u) cudaEventDestroy(p->ev_u);
