@@ -286,6 +286,7 @@ class DistributedOperator:
         self.layer_cells = slab.mesh.ncells // nzl
         self.nlayers = nzl
         self._bufs = None
+        self._idx = {}
 
     def _buffers(self, y):
         import torch
@@ -293,18 +294,22 @@ class DistributedOperator:
             self._bufs = tuple(torch.empty(self.n_if, dtype=y.dtype, device=y.device) for _ in range(4))
         return self._bufs
 
+    def _index(self, y, side):
+        """Entries of y on the interface plane ``side`` (its contiguous blocks
+        concatenated), as one index tensor on y's device: pack and unpack-add
+        are then ONE kernel each instead of one per block."""
+        import torch
+        key = (side, y.device)
+        if key not in self._idx:
+            self._idx[key] = torch.cat([torch.arange(a, b, device=y.device) for a, b in self.ranges[side]])
+        return self._idx[key]
+
     def _pack(self, y, side, out):
-        o = 0
-        for a, b in self.ranges[side]:
-            out[o:o + b - a] = y[a:b]
-            o += b - a
-        return out
+        import torch
+        return torch.index_select(y, 0, self._index(y, side), out=out)
 
     def _unpack_add(self, y, side, buf):
-        o = 0
-        for a, b in self.ranges[side]:
-            y[a:b] += buf[o:o + b - a]
-            o += b - a
+        y.index_add_(0, self._index(y, side), buf)
 
     def _start_exchange(self, y):
         import torch.distributed as dist
