@@ -211,7 +211,7 @@ def build_problem_for_rank(name, seed, rank, world):
     from paper_1903_08243_b200 import configs as C
     from paper_1903_08243_b200.distributed import build_slab, global_dof_index, slab_split
     cfg = C.get_config(name)
-    return build_slab(cfg, seed, *slab_split(rank, world, cfg.n[-1]))
+    return build_slab(cfg, seed, *slab_split(rank, world, cfg.n[-1]), boundary_first=world > 1)
 
 
 def build_ops(names, seed, device, rank, world):
@@ -320,7 +320,7 @@ def gathered_parity(ops, rank, world, dev, seed):
         yg = torch.zeros(glob.ndofs, dtype=torch.float64, device=dev)
         g.apply(torch.tensor(glob.u, device=dev), yg, coef=coef, overwrite=True)
         for r in range(world):
-            sl = build_slab(cfg, seed, *slab_split(r, world, cfg.n[-1]))
+            sl = build_slab(cfg, seed, *slab_split(r, world, cfg.n[-1]), boundary_first=world > 1)
             ref = yg[torch.as_tensor(global_dof_index(sl), device=dev)]
             worst = max(worst, float(torch.linalg.norm(ys[r] - ref) / torch.linalg.norm(ref)))
         del g, yg

@@ -63,6 +63,7 @@ class Slab:
     nvert: int = 0             # vertices of the slab (= vertex dofs, numbered first)
     nvp: int = 0               # vertices per layer plane
     global_index: np.ndarray = None   # single-domain scalar dof id of every slab dof
+    boundary_first: bool = False      # cell order: first layer, last layer, interior layers
 
     def interface_ranges(self, side: str):
         """Scalar-dof ranges [a, b) of the interface node plane at the bottom
@@ -144,12 +145,16 @@ def vertex_first_table(L, k):
     return np.where(isv, cv - 1, nv + lin - cv)
 
 
-def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab:
+def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int, boundary_first: bool = False) -> Slab:
     """Cell layers [z0, z1) along the slowest axis (z in 3D, y in 2D) of the
     global structured mesh of a config (nx x ny x nz_global cubes, or nx x
     nz_global squares), with slab-local lattice numbering.  2D cells follow
     the reference split (mesh.py:52-57): squares into (v00,v10,v01),
-    (v10,v11,v01), quads in tensor order."""
+    (v10,v11,v01), quads in tensor order.  ``boundary_first``: the cells of
+    the LAST layer follow those of the first (cell order only; the dof
+    numbering is unchanged), so the two boundary layers -- the only cells that
+    touch an interface plane -- are ONE contiguous cell range and
+    DistributedOperator applies them with one launch."""
     d = len(cfg.n)
     if d not in (2, 3):
         raise ValueError("slab partition needs a structured 2D or 3D config")
@@ -187,14 +192,18 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
             coords[lz][inner] += delta[inner]
     coords = coords.reshape(-1, d)
     # cells: layers slowest; 6 Kuhn tets / one hex per cube, 2 tris / one quad per square
+    boundary_first = bool(boundary_first) and nzl >= 3
+    layers = np.arange(nzl)
+    if boundary_first:
+        layers = np.concatenate([[0, nzl - 1], np.arange(1, nzl - 1)])
     if d == 3:
-        l, j, i = np.meshgrid(np.arange(nzl), np.arange(ny), np.arange(nx), indexing="ij")
+        l, j, i = np.meshgrid(layers, np.arange(ny), np.arange(nx), indexing="ij")
         base = (i + (nx + 1) * (j + (ny + 1) * l)).ravel()
         corner = np.array([(b & 1) + (nx + 1) * (((b >> 1) & 1) + (ny + 1) * ((b >> 2) & 1))
                            for b in range(8)], dtype=np.int64)
         cells_bits = kuhn_tets() if cfg.cell == "tetrahedron" else np.arange(8)[None, :]
     else:
-        l, i = np.meshgrid(np.arange(nzl), np.arange(nx), indexing="ij")
+        l, i = np.meshgrid(layers, np.arange(nx), indexing="ij")
         base = (i + (nx + 1) * l).ravel()
         corner = np.array([(b & 1) + (nx + 1) * ((b >> 1) & 1) for b in range(4)], dtype=np.int64)
         cells_bits = (np.array([[0, 1, 2], [1, 3, 2]]) if cfg.cell == "triangle"
@@ -255,7 +264,7 @@ def build_slab(cfg: Config, seed: int, z0: int, z1: int, nz_global: int) -> Slab
         state = slat.reshape(nlat, vs)[lat].ravel() * (0.01 / nmax)
     nvert = (nzl + 1) * nvp
     return Slab(cfg, spec, rule, mesh, dm, u, mu, lam, z0, z1, nz_global, plane, state,
-                nvert, nvp, global_index)
+                nvert, nvp, global_index, boundary_first)
 
 
 class DistributedOperator:
@@ -288,49 +297,57 @@ class DistributedOperator:
         self._bufs = None
         self._idx = {}
 
+    def _sides(self):
+        return [sd for sd, has in (("below", self.slab.has_below), ("above", self.slab.has_above)) if has]
+
     def _buffers(self, y):
+        """(recv, send): one contiguous buffer each, a segment of n_if entries
+        per interface this slab has (below first)."""
         import torch
         if self._bufs is None or self._bufs[0].device != y.device:
-            self._bufs = tuple(torch.empty(self.n_if, dtype=y.dtype, device=y.device) for _ in range(4))
+            n = self.n_if * max(1, len(self._sides()))
+            self._bufs = tuple(torch.empty(n, dtype=y.dtype, device=y.device) for _ in range(2))
         return self._bufs
 
-    def _index(self, y, side):
-        """Entries of y on the interface plane ``side`` (its contiguous blocks
-        concatenated), as one index tensor on y's device: pack and unpack-add
-        are then ONE kernel each instead of one per block."""
+    def _index(self, y):
+        """Entries of y on this slab's interface planes (the contiguous blocks
+        of every plane concatenated, below first), as one index tensor on y's
+        device: the pack and the unpack-add of ALL planes are one kernel each."""
         import torch
-        key = (side, y.device)
-        if key not in self._idx:
-            self._idx[key] = torch.cat([torch.arange(a, b, device=y.device) for a, b in self.ranges[side]])
-        return self._idx[key]
+        if y.device not in self._idx:
+            blocks = [torch.arange(a, b, device=y.device) for sd in self._sides() for a, b in self.ranges[sd]]
+            self._idx[y.device] = torch.cat(blocks) if blocks else torch.empty(0, dtype=torch.long, device=y.device)
+        return self._idx[y.device]
 
-    def _pack(self, y, side, out):
+    def _pack(self, y):
         import torch
-        return torch.index_select(y, 0, self._index(y, side), out=out)
+        recv, send = self._buffers(y)
+        return torch.index_select(y, 0, self._index(y), out=send)
 
-    def _unpack_add(self, y, side, buf):
-        y.index_add_(0, self._index(y, side), buf)
+    def _unpack_add(self, y):
+        recv, send = self._buffers(y)
+        y.index_add_(0, self._index(y), recv)
 
     def _start_exchange(self, y):
         import torch.distributed as dist
-        below, above, send_b, send_a = self._buffers(y)
+        recv, send = self._buffers(y)
+        sides = self._sides()
+        if not sides:
+            return []
+        self._pack(y)
         ops = []
-        if self.slab.has_below:
-            ops.append(dist.P2POp(dist.isend, self._pack(y, "below", send_b), self.rank - 1))
-            ops.append(dist.P2POp(dist.irecv, below, self.rank - 1))
-        if self.slab.has_above:
-            ops.append(dist.P2POp(dist.isend, self._pack(y, "above", send_a), self.rank + 1))
-            ops.append(dist.P2POp(dist.irecv, above, self.rank + 1))
-        return dist.batch_isend_irecv(ops) if ops else []
+        for k, sd in enumerate(sides):
+            peer = self.rank - 1 if sd == "below" else self.rank + 1
+            seg = slice(k * self.n_if, (k + 1) * self.n_if)
+            ops.append(dist.P2POp(dist.isend, send[seg], peer))
+            ops.append(dist.P2POp(dist.irecv, recv[seg], peer))
+        return dist.batch_isend_irecv(ops)
 
     def _finish_exchange(self, y, works):
         for w in works:
             w.wait()
-        below, above = (self._bufs[0], self._bufs[1]) if self._bufs else (None, None)
-        if self.slab.has_below:
-            self._unpack_add(y, "below", below)
-        if self.slab.has_above:
-            self._unpack_add(y, "above", above)
+        if works:
+            self._unpack_add(y)
 
     def exchange(self, y):
         """Sum the interface planes with the neighbours (in place)."""
@@ -343,6 +360,12 @@ class DistributedOperator:
             self.exchange(y)
             return y
         # boundary layers first (the only cells touching an interface plane)
+        if getattr(self.slab, "boundary_first", False):
+            self.range_apply(u, y, 0, 2 * lc, True)     # zero-fills y, then both boundary layers (one launch)
+            works = self._start_exchange(y)             # NCCL waits for the boundary cells
+            self.range_apply(u, y, 2 * lc, nc, False)   # interior overlaps the exchange
+            self._finish_exchange(y, works)
+            return y
         self.range_apply(u, y, 0, lc, True)           # zero-fills y, then layer 0
         self.range_apply(u, y, nc - lc, nc, False)
         works = self._start_exchange(y)                 # NCCL waits for the boundary cells

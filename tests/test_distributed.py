@@ -96,13 +96,13 @@ def test_distributed_equals_single_domain(name, world, nz, overlap):
         assert fo.rel_l2(y, y_glob[idx]) <= 1e-14, rank
 
 
-def _strong_worker(rank, world, port, name, n, q):
+def _strong_worker(rank, world, port, name, n, q, boundary_first=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = C.get_config(name, n)
     z0, z1, nzg = slab_split(rank, world, cfg.n[-1])
-    slab = build_slab(cfg, 5, z0, z1, nzg)
+    slab = build_slab(cfg, 5, z0, z1, nzg, boundary_first=boundary_first)
     apply, range_apply = _oracle_apply(slab)
     op = DistributedOperator(slab, apply, rank, world, range_apply)
     u = torch.from_numpy(slab.u.copy())
@@ -113,15 +113,17 @@ def _strong_worker(rank, world, port, name, n, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world,n", [
+@pytest.mark.parametrize("name,world,n,bfirst", [
     # strong scaling: ONE fixed mesh split into world slabs (bench.py --gpus N)
-    ("C5", 2, (2, 2, 6)), ("C2-P3", 2, (2, 2, 5)), ("C3-Q2", 3, (2, 3, 7)),
-    ("C1", 2, (4, 6)), ("C4-quad-Q2", 3, (3, 7)), ("C4-hex-Q1", 2, (2, 2, 4))])
-def test_strong_split_equals_single_domain(name, world, n):
+    ("C5", 2, (2, 2, 6), False), ("C2-P3", 2, (2, 2, 5), False), ("C3-Q2", 3, (2, 3, 7), False),
+    ("C1", 2, (4, 6), False), ("C4-quad-Q2", 3, (3, 7), False), ("C4-hex-Q1", 2, (2, 2, 4), False),
+    # the cell order bench.py uses at N > 1: both boundary layers first (one launch)
+    ("C5", 2, (2, 2, 8), True), ("C3-Q2", 3, (2, 3, 10), True), ("C4-quad-Q2", 2, (3, 8), True)])
+def test_strong_split_equals_single_domain(name, world, n, bfirst):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, name, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, name, n, q, bfirst)) for r in range(world)]
     for p in procs:
         p.start()
     results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])

@@ -18,7 +18,9 @@ pytestmark = pytest.mark.gpu
     ("C2-P2", 2, 2, False), ("C2-P4", 3, 2, False), ("C3-Q3", 2, 2, False), ("C4-hex-Q2", 2, 2, False),
     ("C5", 4, 2, False),
     # the overlapped order of DistributedOperator: boundary layers, then interior
-    ("C2-P3", 3, 3, True), ("C3-Q2", 2, 4, True), ("C4-hex-Q1", 2, 3, True)])
+    ("C2-P3", 3, 3, True), ("C3-Q2", 2, 4, True), ("C4-hex-Q1", 2, 3, True),
+    # boundary-first cell order (bench.py at N > 1): both boundary layers in one range
+    ("C5", 2, 4, "bfirst"), ("C3-Q3", 2, 3, "bfirst"), ("C4-hex-Q2", 2, 4, "bfirst")])
 def test_slabs_on_gpu_equal_single_domain(name, world, nz, split):
     import torch
     cfg = C.get_config(name, (3, 2, nz))
@@ -26,7 +28,7 @@ def test_slabs_on_gpu_equal_single_domain(name, world, nz, split):
     ys, slabs = [], []
     for r in range(world):
         z0, z1, nzg = slab_range(r, world, nz)
-        s = build_slab(cfg, 9, z0, z1, nzg)
+        s = build_slab(cfg, 9, z0, z1, nzg, boundary_first=(split == "bfirst"))
         h = fe.compile_and_load(fe.emit_for(s.spec, fe.Target(), s.rule))
         h.bind(torch.tensor(np.asarray(s.mesh.coords).ravel(), device=dev),
                torch.tensor(np.asarray(s.dofmap.cell2dof, np.int32).ravel(), device=dev),
@@ -35,7 +37,12 @@ def test_slabs_on_gpu_equal_single_domain(name, world, nz, split):
         u = torch.tensor(s.u, device=dev)
         y = torch.zeros_like(u)
         coef = None if s.mu is None else (torch.tensor(s.mu, device=dev), torch.tensor(s.lam, device=dev))
-        if split:
+        if split == "bfirst":
+            nc = s.mesh.ncells
+            lc = nc // nz
+            h.apply(u, y, 0, 2 * lc, coef=coef, overwrite=True)
+            h.apply(u, y, 2 * lc, nc, coef=coef)
+        elif split:
             nc = s.mesh.ncells
             lc = nc // nz
             h.apply(u, y, 0, lc, coef=coef, overwrite=True)

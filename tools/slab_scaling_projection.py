@@ -6,8 +6,8 @@ slab a middle rank would own (nz/N cell layers of the config's fixed mesh,
 two interfaces: the worst case) is built and the rank-local part of
 DistributedOperator.apply is timed on this GPU with the bench's protocol
 (cold L2, CUDA events, median): boundary layers first (overwrite + layer 0,
-last layer), the pack of both interface planes, the interior layers, the
-unpack-add of two received planes.  The NCCL send/recv itself is replaced by
+last layer), the pack of both interface planes (one kernel), the interior
+layers, the unpack-add of the received planes (one kernel).  The NCCL send/recv itself is replaced by
 nothing: its cost (message bytes below, ~2 us at NVLink peer bandwidth plus
 ~10 us of latency) is hidden behind the interior layers, which the table
 shows next to it.  Projected efficiency = T_1 / (N T_N): what wave
@@ -60,17 +60,22 @@ def main():
                 if world == 1:
                     h.apply(u, y, coef=coef, overwrite=True)
                     return
-                below, above, send_b, send_a = op._buffers(y)
-                rng(u, y, 0, lc, True)
-                rng(u, y, nc - lc, nc, False)
-                op._pack(y, "below", send_b)
-                op._pack(y, "above", send_a)
-                rng(u, y, lc, nc - lc, False)
-                op._unpack_add(y, "below", below)
-                op._unpack_add(y, "above", above)
+                if prob.boundary_first:
+                    rng(u, y, 0, 2 * lc, True)
+                    op._pack(y)
+                    rng(u, y, 2 * lc, nc, False)
+                else:
+                    rng(u, y, 0, lc, True)
+                    rng(u, y, nc - lc, nc, False)
+                    op._pack(y)
+                    rng(u, y, lc, nc - lc, False)
+                op._unpack_add(y)
 
             def interior():
-                rng(u, y, lc, nc - lc, False)
+                if prob.boundary_first:
+                    rng(u, y, 2 * lc, nc, False)
+                else:
+                    rng(u, y, lc, nc - lc, False)
 
             t = float(np.median(time_device(local_part, trials=10, warmup=3)))
             ti = float(np.median(time_device(interior, trials=10, warmup=3))) if world > 1 else t
