@@ -49,13 +49,23 @@ FE_DEVICE void load_vertex(const double* __restrict__ coords, int v, double* x) 
 // of a kernel.  Whether that helps is kernel-specific (it also frees ptxas to
 // hoist more work and raise register pressure), so every caller picks per
 // kernel variant from measurement (profiles/r01/sweep_rcp.txt).
+#ifndef FE_RCP3
+#define FE_RCP3 1   // C5 5.176 -> 5.127 ms, C4-quad-Q1/Q2, C4-hex-Q1 +1% (profiles/r02/ab_rcp3.txt); parity unchanged
+#endif
 FE_DEVICE double rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#if FE_RCP3
+  // one cubically convergent step: r (1 + e + e^2), e = 1 - x r (seed error
+  // 2^-23 -> 2^-69): three FMAs instead of two Newton steps' four
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+#else
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+#endif
 }
 template <bool FAST>
 FE_DEVICE double recip(double x) {

@@ -27,6 +27,9 @@ namespace fe {
 #ifndef FE_PAIR_RCP_MAXP
 #define FE_PAIR_RCP_MAXP 5   // MUFU-seeded reciprocal up to this P: with the select-free kernel it wins at P = 5 too (0.5255 -> 0.4967 ms, profiles/r02/ab_pair_rcp.txt)
 #endif
+#ifndef FE_PAIR_T0ALT
+#define FE_PAIR_T0ALT 1   // C4-quad-Q3 0.2733 -> 0.2652 ms (0.51 of its roof), Q4 0.4988 -> 0.4793 (profiles/r02/ab_pair_t0.txt)
+#endif
 #ifndef FE_PAIR_NOSEL
 #define FE_PAIR_NOSEL 1
 #endif
@@ -159,8 +162,13 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       const double o0 = __shfl_xor_sync(live, g0, 1), o1 = __shfl_xor_sync(live, g1, 1);
 #if FE_PAIR_NOSEL
       // (own, cross) = (g0, g1): trace = own + partner's own, shear = cross + partner's cross
+#if FE_PAIR_T0ALT
+      // lam tr + 2 mu own = (lam + 2 mu) own - lam partner_own: one instruction fewer
+      const double t0 = fma(fma(2.0, mu, lam), g0, -(lam * o0)), t1 = mu * (g1 - o1);
+#else
       const double tr = g0 - o0;
       const double t0 = fma(mu, g0 + g0, lam * tr), t1 = mu * (g1 - o1);
+#endif
 #else
       const double tr = c ? (g1 + o0) : (g0 + o1);
       // (G + G^T)[c][:] and the Lame stress row (the scale folded into mu, lambda)
