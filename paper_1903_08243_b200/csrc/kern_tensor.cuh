@@ -58,6 +58,11 @@ struct TensorParams {
   int32_t start, end;
   double p0, p1;
   double B[Q][P], D[Q][P], Dc[Q][Q], x[Q], w[Q];
+  // even / odd parts of the mirror-symmetric 1D tables, rows q < ceil(Q/2)
+  // (fill_tensor_tables): Xe[q][j] = (X[q][j] + X[q][P-1-j]) / 2 for j < P/2 and
+  // X[q][(P-1)/2] in the middle column of an odd P; Xo[q][j] = (X[q][j] - X[q][P-1-j]) / 2
+  double Be[(Q + 1) / 2][(P + 1) / 2], Bo[(Q + 1) / 2][(P + 1) / 2];
+  double De[(Q + 1) / 2][(P + 1) / 2], Do[(Q + 1) / 2][(P + 1) / 2];
 };
 
 // ---- compile-time bank-conflict-aware strides --------------------------------
@@ -106,6 +111,9 @@ constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b >
 #ifndef FE_TK_FLATZ
 #define FE_TK_FLATZ 0   // 1: one z stage for all components of a vector form; measured neutral
 #endif                  // (C4-hex-Q2 0.456 -> 0.460 ms, C4-hex-Q3 1.244 -> 1.239 ms, profiles/r02/ab_tensor_flatz.txt)
+#ifndef FE_TK_EO
+#define FE_TK_EO 1   // even-odd 1D contractions in the DIRECT variants: C3-Q5 0.967 -> 0.917 ms, C3-Q6 1.676 -> 1.532 ms (profiles/r02/ab_tensor_eo.txt)
+#endif
 #ifndef FE_TK_RCPALL
 #define FE_TK_RCPALL 0
 #endif
@@ -191,6 +199,11 @@ struct TensorLayout {
 // and at Q = 7 halving the tables tips ptxas from in-loop LDCU loads to
 // hoisting them into vector registers (459 R2UR, 1.68 -> 2.29 ms)
 template <int P, int Q> constexpr bool tensor_sym() { return FE_TK_SYM != 0 && P == 4 && Q == 5; }
+// even-odd 1D contractions: every 3D variant on the direct algorithm with P >= 4
+// (measured: C3-Q5/Q6 -5% / -9%, C4-hex-Q3 -2.7%; slower at P = 3, profiles/r02/ab_tensor_eo.txt)
+template <int DIM, int P, int Q, bool DIRECT> constexpr bool tensor_eo() {
+  return FE_TK_EO != 0 && DIM == 3 && (DIRECT || P != Q) && P >= 4;
+}
 template <int MINB> constexpr bool tensor_async() { return MINB >= 1000 || FE_TK_ASYNC; }
 template <int MINB> constexpr int tensor_block() {
   constexpr int m = MINB % 1000;
@@ -242,6 +255,97 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
   auto TD = [&](int q, int i) { return (!SYM || 2 * q < Q) ? p.D[q][i] : -p.D[Q - 1 - q][P - 1 - i]; };
   auto TX = [&](int q) { return (!SYM || 2 * q < Q) ? p.x[q] : 1.0 - p.x[Q - 1 - q]; };
   auto TW = [&](int q) { return (!SYM || 2 * q < Q) ? p.w[q] : p.w[Q - 1 - q]; };
+  // FE_TK_EO: even-odd decomposition of the 1D contractions (DIRECT 3D variants).
+  // With mirror-symmetric tables the rows q and Q-1-q share their products:
+  // out[q] = E + O, out[Q-1-q] = +-(E - O) with E = sum Xe[q][j] (x[j] + x[P-1-j]),
+  // O = sum Xo[q][j] (x[j] - x[P-1-j]): P + 2 instead of 2P FP64 slots per output pair.
+  constexpr bool EO = tensor_eo<DIM, P, Q, DIRECT>();
+  constexpr int HP = P / 2, NE = (P + 1) / 2, HQ = Q / 2;
+  auto eo_split = [&](const double (&x)[P], double (&xe)[NE], double (&xo)[NE]) {
+#pragma unroll
+    for (int j = 0; j < HP; ++j) {
+      xe[j] = x[j] + x[P - 1 - j];
+      xo[j] = x[j] - x[P - 1 - j];
+    }
+    if constexpr (P % 2) { xe[HP] = x[HP]; xo[HP] = 0.0; }
+  };
+  auto eo_fwdB = [&](const double (&xe)[NE], const double (&xo)[NE], double (&out)[Q]) {
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) {
+      double E = 0.0, O = 0.0;
+#pragma unroll
+      for (int j = 0; j < NE; ++j) E = fma(p.Be[q][j], xe[j], E);
+#pragma unroll
+      for (int j = 0; j < HP; ++j) O = fma(p.Bo[q][j], xo[j], O);
+      out[q] = E + O;
+      out[Q - 1 - q] = E - O;
+    }
+    if constexpr (Q % 2) {
+      double E = 0.0;
+#pragma unroll
+      for (int j = 0; j < NE; ++j) E = fma(p.Be[HQ][j], xe[j], E);
+      out[HQ] = E;
+    }
+  };
+  auto eo_fwdD = [&](const double (&xe)[NE], const double (&xo)[NE], double (&out)[Q]) {
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) {
+      double E = 0.0, O = 0.0;
+#pragma unroll
+      for (int j = 0; j < NE; ++j) E = fma(p.De[q][j], xe[j], E);
+#pragma unroll
+      for (int j = 0; j < HP; ++j) O = fma(p.Do[q][j], xo[j], O);
+      out[q] = O + E;
+      out[Q - 1 - q] = O - E;
+    }
+    if constexpr (Q % 2) {
+      double O = 0.0;
+#pragma unroll
+      for (int j = 0; j < HP; ++j) O = fma(p.Do[HQ][j], xo[j], O);
+      out[HQ] = O;
+    }
+  };
+  // adjoints: accumulate sum_q X[q][j] f[q] in even/odd form, then eo_merge
+  auto eo_adjB = [&](const double (&f)[Q], double (&ae)[NE], double (&ao)[NE]) {
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) {
+      const double fp = f[q] + f[Q - 1 - q], fm = f[q] - f[Q - 1 - q];
+#pragma unroll
+      for (int j = 0; j < NE; ++j) ae[j] = fma(p.Be[q][j], fp, ae[j]);
+#pragma unroll
+      for (int j = 0; j < HP; ++j) ao[j] = fma(p.Bo[q][j], fm, ao[j]);
+    }
+    if constexpr (Q % 2) {
+#pragma unroll
+      for (int j = 0; j < NE; ++j) ae[j] = fma(p.Be[HQ][j], f[HQ], ae[j]);
+    }
+  };
+  auto eo_adjD = [&](const double (&f)[Q], double (&ae)[NE], double (&ao)[NE]) {
+#pragma unroll
+    for (int q = 0; q < HQ; ++q) {
+      const double fp = f[q] + f[Q - 1 - q], fm = f[q] - f[Q - 1 - q];
+#pragma unroll
+      for (int j = 0; j < NE; ++j) ae[j] = fma(p.De[q][j], fm, ae[j]);
+#pragma unroll
+      for (int j = 0; j < HP; ++j) ao[j] = fma(p.Do[q][j], fp, ao[j]);
+    }
+    if constexpr (Q % 2) {
+#pragma unroll
+      for (int j = 0; j < HP; ++j) ao[j] = fma(p.Do[HQ][j], f[HQ], ao[j]);
+    }
+  };
+  auto eo_merge = [&](const double (&ae)[NE], const double (&ao)[NE], double (&out)[P]) {
+#pragma unroll
+    for (int j = 0; j < HP; ++j) {
+      out[j] = ae[j] + ao[j];
+      out[P - 1 - j] = ae[j] - ao[j];
+    }
+    if constexpr (P % 2) out[HP] = ae[HP];
+  };
+  auto eo_zero = [&](double (&ae)[NE], double (&ao)[NE]) {
+#pragma unroll
+    for (int j = 0; j < NE; ++j) ae[j] = ao[j] = 0.0;
+  };
 
   // ---- prefetch pipeline: map indices two batches ahead, data one ahead ----
   constexpr int RX = L::RX, RM = L::RM;
@@ -451,6 +555,18 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
       double pen[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) pen[k] = uc[k * P * P + e];
+      if constexpr (EO) {
+        double xe[NE], xo[NE], z0[Q], z1[Q];
+        eo_split(pen, xe, xo);
+        eo_fwdB(xe, xo, z0);
+        eo_fwdD(xe, xo, z1);
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          zb[j * L::SZ + c * P + i] = z0[c];
+          zb[P * L::SZ + j * L::SZ + c * P + i] = z1[c];
+        }
+        return;
+      }
 #pragma unroll
       for (int c = 0; c < Q; ++c) {
         double z0 = 0.0, z1 = 0.0;
@@ -492,6 +608,20 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
             p0[j] = s1[j * L::SZ + t];
             if constexpr (!COLLOC) p1[j] = s1[P * L::SZ + j * L::SZ + t];
           }
+          if constexpr (EO) {
+            double xe[NE], xo[NE], y0[Q], y1[Q], y2[Q];
+            eo_split(p0, xe, xo);
+            eo_fwdB(xe, xo, y0);
+            eo_fwdD(xe, xo, y1);
+            eo_split(p1, xe, xo);
+            eo_fwdB(xe, xo, y2);
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+              s2[i * L::SY + c * Q + b] = y0[b];
+              s2[P * L::SY + i * L::SY + c * Q + b] = y1[b];
+              s2[2 * P * L::SY + i * L::SY + c * Q + b] = y2[b];
+            }
+          } else
 #pragma unroll
           for (int b = 0; b < Q; ++b) {
             double y0 = 0.0, y1 = 0.0, y2 = 0.0;
@@ -600,6 +730,15 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               q1[i] = s2[P * L::SY + i * L::SY + t];
               q2[i] = s2[2 * P * L::SY + i * L::SY + t];
             }
+            if constexpr (EO) {
+              double xe[NE], xo[NE];
+              eo_split(q0, xe, xo);
+              eo_fwdD(xe, xo, g[comp][0]);
+              eo_split(q1, xe, xo);
+              eo_fwdB(xe, xo, g[comp][1]);
+              eo_split(q2, xe, xo);
+              eo_fwdB(xe, xo, g[comp][2]);
+            } else
 #pragma unroll
             for (int a = 0; a < Q; ++a) {
               double g0 = 0.0, g1 = 0.0, g2 = 0.0;
@@ -769,6 +908,16 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
         w1[c] = wb[c * L::SW + e];
         w2[c] = wb[Q * L::SW + c * L::SW + e];
       }
+      if constexpr (EO) {
+        double ae[NE], ao[NE], o[P];
+        eo_zero(ae, ao);
+        eo_adjB(w1, ae, ao);
+        eo_adjD(w2, ae, ao);
+        eo_merge(ae, ao, o);
+#pragma unroll
+        for (int k = 0; k < P; ++k) scatter_add(p.y, (int64_t)VS * __ldg(mrow + k * P * P + e) + comp, o[k]);
+        return;
+      }
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         double s = 0.0;
@@ -882,6 +1031,24 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
           // x^T: thread (b, c): A0 = D^T F0, A1 = B^T F1, A2 = B^T F2 over i  A[b][c][i]
           if (active) {
             const int b = t % Q, c = t / Q;
+            if constexpr (EO) {
+              double ae[NE], ao[NE], o0[P], o1[P], o2[P];
+              eo_zero(ae, ao);
+              eo_adjD(g[comp][0], ae, ao);
+              eo_merge(ae, ao, o0);
+              eo_zero(ae, ao);
+              eo_adjB(g[comp][1], ae, ao);
+              eo_merge(ae, ao, o1);
+              eo_zero(ae, ao);
+              eo_adjB(g[comp][2], ae, ao);
+              eo_merge(ae, ao, o2);
+#pragma unroll
+              for (int i = 0; i < P; ++i) {
+                s2[b * L::SA + c * P + i] = o0[i];
+                s2[Q * L::SA + b * L::SA + c * P + i] = o1[i];
+                s2[2 * Q * L::SA + b * L::SA + c * P + i] = o2[i];
+              }
+            } else
 #pragma unroll
             for (int i = 0; i < P; ++i) {
               double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -907,6 +1074,21 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
               a1[b] = s2[Q * L::SA + b * L::SA + t];
               a2[b] = s2[2 * Q * L::SA + b * L::SA + t];
             }
+            if constexpr (EO) {
+              double ae[NE], ao[NE], o1[P], o2[P];
+              eo_zero(ae, ao);
+              eo_adjB(a0, ae, ao);
+              eo_adjD(a1, ae, ao);
+              eo_merge(ae, ao, o1);
+              eo_zero(ae, ao);
+              eo_adjB(a2, ae, ao);
+              eo_merge(ae, ao, o2);
+#pragma unroll
+              for (int j = 0; j < P; ++j) {
+                sw[c * L::SW + j * P + i] = o1[j];
+                sw[Q * L::SW + c * L::SW + j * P + i] = o2[j];
+              }
+            } else
 #pragma unroll
             for (int j = 0; j < P; ++j) {
               double w1 = 0.0, w2 = 0.0;

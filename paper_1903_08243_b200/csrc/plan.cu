@@ -876,6 +876,16 @@ int fill_tensor_tables(const fe_plan* p, TensorParams<Q, P>* hp) {
     hp->w[a] = p->w1d[a];
   }
   for (int a = 0; a < Q; ++a) hp->x[a] = p->x1d[a];
+  // even / odd parts of the tables (used by the even-odd kernels, which also
+  // verify the mirror symmetry they rely on)
+  for (int q = 0; q < (Q + 1) / 2; ++q)
+    for (int j = 0; j < (P + 1) / 2; ++j) {
+      const bool mid = (P % 2) && j == P / 2;
+      hp->Be[q][j] = mid ? hp->B[q][j] : 0.5 * (hp->B[q][j] + hp->B[q][P - 1 - j]);
+      hp->Bo[q][j] = mid ? 0.0 : 0.5 * (hp->B[q][j] - hp->B[q][P - 1 - j]);
+      hp->De[q][j] = mid ? hp->D[q][j] : 0.5 * (hp->D[q][j] + hp->D[q][P - 1 - j]);
+      hp->Do[q][j] = mid ? 0.0 : 0.5 * (hp->D[q][j] - hp->D[q][P - 1 - j]);
+    }
   // collocation derivative at the Gauss points: Dc[a][e] = l_e'(x_a) for the
   // Lagrange basis l_e on the Gauss points (barycentric formula)
   double bw[Q];
@@ -908,7 +918,7 @@ int tensor_prepare(fe_plan* p) {
     return rc;
   }
   // the kernel reads the mirror-symmetric half of the 1D tables
-  for (int q = 0; tensor_sym<P, Q>() && q < Q; ++q) {
+  for (int q = 0; (tensor_sym<P, Q>() || tensor_eo<DIM, P, Q, DIRECT>()) && q < Q; ++q) {
     bool ok = std::fabs(hp->x[q] - (1.0 - hp->x[Q - 1 - q])) <= 1e-13 && std::fabs(hp->w[q] - hp->w[Q - 1 - q]) <= 1e-13;
     for (int i = 0; i < P; ++i)
       ok = ok && std::fabs(hp->B[q][i] - hp->B[Q - 1 - q][P - 1 - i]) <= 1e-12 &&
