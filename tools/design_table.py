@@ -24,15 +24,15 @@ LIMITER = {
     "C3-Q2": "thread per cell (round 2): FP64 pipe 63%, 255 registers (268 B spill), gather exposed at kernel start",
     "C3-Q3": "plane kernel, 8-warp CTAs: FP64 pipe 61%, 206 registers",
     "C3-Q4": "plane kernel: FP64 pipe 57%, 244 registers (P^2 dof + output planes per thread)",
-    "C3-Q5": "team kernel (36-thread teams, CTA barriers, cp.async gather): FP64 pipe 54%; direct algorithm executes 16 q^4 MACs (menu minimum 12 q^4); 319 -> in-loop LDCU table loads",
-    "C3-Q6": "team kernel (49-thread teams): FP64 pipe 55%, 128 registers with spills; direct algorithm",
+    "C3-Q5": "team kernel (36-thread teams, CTA barriers, cp.async gather), direct algorithm with even-odd 1D contractions (executes 58,788 flops); in-loop LDCU table loads",
+    "C3-Q6": "team kernel (49-thread teams), direct algorithm with even-odd 1D contractions (executes 97,644 flops); 128 registers with 112 B of spills, 135 R2UR",
     "C4-quad-Q1": "FP64",
     "C4-quad-Q2": "FP64",
-    "C4-quad-Q3": "pair kernel: FP64 pipe 52%, 255 registers, 2 warps/SMSP; MUL/ADD-heavy pointwise (F/2 = 79% of its FP64 issue slots)",
-    "C4-quad-Q4": "pair kernel: FP64 pipe 52%, 255 registers, instruction-cache misses (69 KB straight-line code)",
+    "C4-quad-Q3": "pair kernel (select-free, symmetric tables): 254 registers, 2 warps/SMSP; MUL/ADD-heavy pointwise (F/2 = 82% of its FP64 issue slots)",
+    "C4-quad-Q4": "pair kernel (select-free, symmetric tables, 2,952 instructions): 254 registers, 2 warps/SMSP, gather exposed; the 42 us zero-fill of its 269 MB y is 9% of the apply",
     "C4-hex-Q1": "FP64",
     "C4-hex-Q2": "team kernel (16-thread teams, 9 / 12 of 16 lanes busy in the z / y stages): FP64 pipe 57%",
-    "C4-hex-Q3": "team kernel (25-thread teams, one per warp: 78% of the lanes; 16 / 20 of 25 in the z / y stages): FP64 pipe 58%",
+    "C4-hex-Q3": "team kernel (25-thread teams, one per warp: 78% of the lanes; 16 / 20 of 25 in the z / y stages), even-odd contractions: FP64 pipe 58%",
     "C5": "FP64 pipe 73%, 254 registers -> 8 warps/SM; executes fewer flops than the menu's F (0.53 of the roof counted on executed flops)",
 }
 
