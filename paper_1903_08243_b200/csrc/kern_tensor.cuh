@@ -1167,7 +1167,7 @@ tensor_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 }  // namespace fe
 
 #ifndef FE_TK_Q5_MINB
-#define FE_TK_Q5_MINB 1002   // 256-thread CTAs, 2 per SM, cp.async gather
+#define FE_TK_Q5_MINB 2      // 256-thread CTAs, 2 per SM, register prefetch: with the even-odd contractions it beats the cp.async gather (0.9165 -> 0.8653 ms, profiles/r02/ab_tensor_eo.txt)
 #endif
 #ifndef FE_TK_Q6_MINB
 #define FE_TK_Q6_MINB 2
