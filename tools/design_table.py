@@ -24,7 +24,7 @@ LIMITER = {
     "C3-Q2": "thread per cell (round 2): FP64 pipe 63%, 255 registers (268 B spill), gather exposed at kernel start",
     "C3-Q3": "plane kernel, 8-warp CTAs: FP64 pipe 61%, 206 registers",
     "C3-Q4": "plane kernel: FP64 pipe 57%, 244 registers (P^2 dof + output planes per thread)",
-    "C3-Q5": "team kernel (36-thread teams, CTA barriers, cp.async gather), direct algorithm with even-odd 1D contractions (executes 58,788 flops); in-loop LDCU table loads",
+    "C3-Q5": "team kernel (36-thread teams, CTA barriers, register-prefetch gather), direct algorithm with even-odd 1D contractions (executes 58,788 flops)",
     "C3-Q6": "team kernel (49-thread teams), direct algorithm with even-odd 1D contractions (executes 97,644 flops); 128 registers with 112 B of spills, 135 R2UR",
     "C4-quad-Q1": "FP64",
     "C4-quad-Q2": "FP64",
