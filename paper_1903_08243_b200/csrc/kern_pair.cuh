@@ -197,6 +197,213 @@ pair_kernel(const __grid_constant__ TensorParams<Q, P> p) {
 
 
 // ---------------------------------------------------------------------------
+// Even-odd variant (round 2): pair_kernel's arithmetic with EVERY 1D
+// contraction in even-odd form, rows and points in mirror pairs (q, Q-1-q).
+// Only the even / odd tables Be, Bo, De, Do (half the distinct constants) are
+// read, so they stay in uniform registers; u is not held in registers but
+// re-read (L1) column by column for each row pair.
+// ---------------------------------------------------------------------------
+template <int FORM, int P, int Q, int MINB>
+__global__ void __launch_bounds__(kPairBlock, MINB)
+pair_eo_kernel(const __grid_constant__ TensorParams<Q, P> p) {
+  static_assert(FORM == FE_FORM_ELASTICITY_LAME || FORM == FE_FORM_ELASTICITY, "2D elasticity forms");
+  constexpr int NDS = P * P, HP = P / 2, NE = (P + 1) / 2, HQ = Q / 2, NQ = (Q + 1) / 2;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = gt & 1;
+  const int cell = p.start + (gt >> 1);
+  const unsigned live = __ballot_sync(0xffffffffu, cell < p.end);
+  if (cell >= p.end) return;
+  const int64_t cs = p.mesh.nc_stride;
+  const int32_t* mrow = p.maplex + (int64_t)cell * NDS;
+  double X[4][2], mv[4], lv[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int vid = __ldg(p.mesh.vmap + v * cs + cell);
+    load_vertex<2>(p.mesh.coords, vid, X[v]);
+    {  // lane 1 works in the axis-swapped frame (see pair_kernel)
+      const double x0 = X[v][0], x1 = X[v][1];
+      X[v][0] = c ? x1 : x0;
+      X[v][1] = c ? x0 : x1;
+    }
+    if constexpr (FORM == FE_FORM_ELASTICITY_LAME) {
+      mv[v] = __ldg(p.mu + vid);
+      lv[v] = __ldg(p.lam + vid);
+    } else {
+      mv[v] = 0.5;
+      lv[v] = 0.0;
+    }
+  }
+  double j1[2], d1[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    j1[d] = X[2][d] - X[0][d];
+    d1[d] = (X[3][d] - X[1][d]) - j1[d];
+  }
+  // y in even / odd form along j: y[j] = YE[j] + YO[j], y[P-1-j] = YE[j] - YO[j]
+  double YE[NE][P], YO[NE][P];
+#pragma unroll
+  for (int j = 0; j < NE; ++j)
+#pragma unroll
+    for (int i = 0; i < P; ++i) YE[j][i] = YO[j][i] = 0.0;
+
+  // one point row: (Y0, Y1) -> (Z0, Z1), even-odd along the row
+  auto row = [&](double eta, double wb, const double (&Y0)[P], const double (&Y1)[P], double (&Z0)[P],
+                 double (&Z1)[P]) {
+    const double le = 1.0 - eta;
+    double J0[2];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) J0[d] = (X[1][d] - X[0][d]) * le + (X[3][d] - X[2][d]) * eta;
+    const double det0 = J0[0] * j1[1] - j1[0] * J0[1], ddet = J0[0] * d1[1] - d1[0] * J0[1];
+    const double m0 = mv[0] * le + mv[2] * eta, dm = mv[1] * le + mv[3] * eta - m0;
+    const double l0 = lv[0] * le + lv[2] * eta, dl = lv[1] * le + lv[3] * eta - l0;
+    auto point = [&](double xi, double wa, double gx, double gy, double& f0, double& f1) {
+      const double J01 = fma(xi, d1[0], j1[0]), J11 = fma(xi, d1[1], j1[1]);
+      const double det = fma(xi, ddet, det0);
+      const double sc = (wa * wb) * rcp(fabs(det));
+      const double mu = sc * fma(xi, dm, m0), lam = sc * fma(xi, dl, l0);
+      const double g0 = gx * J11 - gy * J0[1], g1 = gy * J0[0] - gx * J01;
+      const double o0 = __shfl_xor_sync(live, g0, 1), o1 = __shfl_xor_sync(live, g1, 1);
+      const double t0 = fma(fma(2.0, mu, lam), g0, -(lam * o0)), t1 = mu * (g1 - o1);
+      f0 = t0 * J11 - t1 * J01;
+      f1 = t1 * J0[0] - t0 * J0[1];
+    };
+    double Y0e[NE], Y0o[NE], Y1e[NE], Y1o[NE], ZE0[NE], ZO0[NE], ZE1[NE], ZO1[NE];
+#pragma unroll
+    for (int i = 0; i < HP; ++i) {
+      Y0e[i] = Y0[i] + Y0[P - 1 - i];
+      Y0o[i] = Y0[i] - Y0[P - 1 - i];
+      Y1e[i] = Y1[i] + Y1[P - 1 - i];
+      Y1o[i] = Y1[i] - Y1[P - 1 - i];
+    }
+    if constexpr (P % 2) {
+      Y0e[HP] = Y0[HP];
+      Y1e[HP] = Y1[HP];
+      Y0o[HP] = Y1o[HP] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) ZE0[i] = ZO0[i] = ZE1[i] = ZO1[i] = 0.0;
+#pragma unroll
+    for (int r = 0; r < HQ; ++r) {
+      double ED = 0.0, OD = 0.0, EB = 0.0, OB = 0.0;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        ED = fma(p.De[r][i], Y0e[i], ED);
+        EB = fma(p.Be[r][i], Y1e[i], EB);
+      }
+#pragma unroll
+      for (int i = 0; i < HP; ++i) {
+        OD = fma(p.Do[r][i], Y0o[i], OD);
+        OB = fma(p.Bo[r][i], Y1o[i], OB);
+      }
+      double f0a, f1a, f0b, f1b;
+      point(p.x[r], p.w[r], OD + ED, EB + OB, f0a, f1a);
+      point(1.0 - p.x[r], p.w[r], OD - ED, EB - OB, f0b, f1b);
+      const double fm0 = f0a - f0b, fp0 = f0a + f0b, fp1 = f1a + f1b, fm1 = f1a - f1b;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        ZE0[i] = fma(p.De[r][i], fm0, ZE0[i]);
+        ZE1[i] = fma(p.Be[r][i], fp1, ZE1[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < HP; ++i) {
+        ZO0[i] = fma(p.Do[r][i], fp0, ZO0[i]);
+        ZO1[i] = fma(p.Bo[r][i], fm1, ZO1[i]);
+      }
+    }
+    if constexpr (Q % 2) {
+      double OD = 0.0, EB = 0.0;
+#pragma unroll
+      for (int i = 0; i < HP; ++i) OD = fma(p.Do[HQ][i], Y0o[i], OD);
+#pragma unroll
+      for (int i = 0; i < NE; ++i) EB = fma(p.Be[HQ][i], Y1e[i], EB);
+      double f0, f1;
+      point(p.x[HQ], p.w[HQ], OD, EB, f0, f1);
+#pragma unroll
+      for (int i = 0; i < HP; ++i) ZO0[i] = fma(p.Do[HQ][i], f0, ZO0[i]);
+#pragma unroll
+      for (int i = 0; i < NE; ++i) ZE1[i] = fma(p.Be[HQ][i], f1, ZE1[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < HP; ++i) {
+      Z0[i] = ZE0[i] + ZO0[i];
+      Z0[P - 1 - i] = ZE0[i] - ZO0[i];
+      Z1[i] = ZE1[i] + ZO1[i];
+      Z1[P - 1 - i] = ZE1[i] - ZO1[i];
+    }
+    if constexpr (P % 2) {
+      Z0[HP] = ZE0[HP];
+      Z1[HP] = ZE1[HP];
+    }
+  };
+
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const bool pair = q < HQ;
+    // forward along j for the row pair (q, Q-1-q): u re-read column by column
+    double Y0a[P], Y1a[P], Y0b[P], Y1b[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double uc[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) uc[j] = __ldg(p.u + 2 * (int64_t)__ldg(mrow + j * P + i) + c);
+      double EB = 0.0, OB = 0.0, ED = 0.0, OD = 0.0;
+#pragma unroll
+      for (int j = 0; j < HP; ++j) {
+        const double e = uc[j] + uc[P - 1 - j], o = uc[j] - uc[P - 1 - j];
+        EB = fma(p.Be[q][j], e, EB);
+        ED = fma(p.De[q][j], e, ED);
+        OB = fma(p.Bo[q][j], o, OB);
+        OD = fma(p.Do[q][j], o, OD);
+      }
+      if constexpr (P % 2) {
+        EB = fma(p.Be[q][HP], uc[HP], EB);
+        ED = fma(p.De[q][HP], uc[HP], ED);
+      }
+      Y0a[i] = EB + OB;
+      Y1a[i] = OD + ED;
+      Y0b[i] = EB - OB;
+      Y1b[i] = OD - ED;
+    }
+    double Z0a[P], Z1a[P], Z0b[P], Z1b[P];
+    row(p.x[q], p.w[q], Y0a, Y1a, Z0a, Z1a);
+    if (pair) {
+      row(1.0 - p.x[q], p.w[q], Y0b, Y1b, Z0b, Z1b);
+      // y += B^T Z0 + D^T Z1 over the two rows, in even / odd form along j
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double zp = Z0a[i] + Z0b[i], zm = Z0a[i] - Z0b[i];
+        const double z1m = Z1a[i] - Z1b[i], z1p = Z1a[i] + Z1b[i];
+#pragma unroll
+        for (int j = 0; j < NE; ++j) YE[j][i] = fma(p.Be[q][j], zp, fma(p.De[q][j], z1m, YE[j][i]));
+#pragma unroll
+        for (int j = 0; j < HP; ++j) YO[j][i] = fma(p.Bo[q][j], zm, fma(p.Do[q][j], z1p, YO[j][i]));
+      }
+    } else {
+      // middle row of an odd Q: B[mid] is even, D[mid] odd in j
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+#pragma unroll
+        for (int j = 0; j < NE; ++j) YE[j][i] = fma(p.Be[q][j], Z0a[i], YE[j][i]);
+#pragma unroll
+        for (int j = 0; j < HP; ++j) YO[j][i] = fma(p.Do[q][j], Z1a[i], YO[j][i]);
+      }
+    }
+  }
+  griddep_wait();
+#pragma unroll
+  for (int j = 0; j < HP; ++j)
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      scatter_add(p.y, 2 * (int64_t)__ldg(mrow + j * P + i) + c, YE[j][i] + YO[j][i]);
+      scatter_add(p.y, 2 * (int64_t)__ldg(mrow + (P - 1 - j) * P + i) + c, YE[j][i] - YO[j][i]);
+    }
+  if constexpr (P % 2) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) scatter_add(p.y, 2 * (int64_t)__ldg(mrow + HP * P + i) + c, YE[HP][i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Pipelined variant (round 2): the same arithmetic in PERSISTENT warps with
 // the indirect gather P_e u taken off the critical path.  pair_kernel above
 // issues map -> u loads and only then computes, with 8 warps per SM (255

@@ -1168,11 +1168,12 @@ int hexlp_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const 
 
 // component-pair 2D elasticity kernel (kern_pair.cuh).  FE_PAIR_CFG selects
 // the kernel: 0 = round-1 kernel (one cell pair per thread pair, gather on
-// the critical path), 1 = pipelined persistent kernel, 4-warp CTAs, 2 per SM
+// the critical path), 1 = pipelined persistent kernel, 4-warp CTAs, 2 per SM,
+// 2 = the round-1 structure with every 1D contraction in even-odd form
 #ifndef FE_PAIR_CFG
-#define FE_PAIR_CFG 0   // measured: the pipelined kernel is slower (0.37 / 0.68 vs 0.32 / 0.58 ms at Q3 / Q4,
-#endif                  // profiles/r02/ab_pair_pipe.txt): ptxas hoists the table constants out of the persistent
-                        // loop into vector registers (sm_100a has ~80 uniform registers) and the loop fills with moves
+#define FE_PAIR_CFG 2   // 0 = round-1 structure, 1 = pipelined persistent kernel (slower: ptxas hoists the table
+#endif                  // constants out of the loop, profiles/r02/ab_pair_pipe.txt), 2 = even-odd kernel (kept:
+                        // C4-quad-Q3 0.263 -> 0.257 ms, Q4 0.479 -> 0.444 ms, profiles/r02/ab_pair_eo.txt)
 constexpr int kPairPipeWarps = 4;
 
 template <int FORM, int P, int Q, int MINB>
@@ -1200,7 +1201,7 @@ int pair_prepare(fe_plan* p) {
   p->host_params_bytes = sizeof(TP);
   const char* env = getenv("FE_PAIR_CFG");
   p->dmma_cfg = env ? atoi(env) : FE_PAIR_CFG;
-  if (p->dmma_cfg < 0 || p->dmma_cfg > 1) p->dmma_cfg = FE_PAIR_CFG;
+  if (p->dmma_cfg < 0 || p->dmma_cfg > 2) p->dmma_cfg = FE_PAIR_CFG;   // 2: even-odd kernel
   // the pipelined kernel (and the round-1 kernel under FE_PAIR_SYM) reads the
   // mirror-symmetric half of the 1D tables
   bool sym = true;
@@ -1219,7 +1220,8 @@ int pair_prepare(fe_plan* p) {
   int dev = 0, sms = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (p->dmma_cfg != 0) return pair_pipe_setup<FORM, P, Q, 2>(p, sms);
+  if (p->dmma_cfg == 1) return pair_pipe_setup<FORM, P, Q, 2>(p, sms);
+  if (p->dmma_cfg == 2 && !sym) return fail(FE_EUNSUPPORTED, "even-odd pair kernel needs mirror-symmetric 1D tables");
   return FE_OK;
 }
 
@@ -1238,9 +1240,12 @@ int pair_launch(const fe_plan* p, int32_t start, int32_t end, double* y, const d
   hp->lam = c1;
   hp->start = start;
   hp->end = end;
-  if (p->dmma_cfg == 0) {
+  if (p->dmma_cfg == 0 || p->dmma_cfg == 2) {
     const int64_t nt = 2 * (int64_t)(end - start);
-    launch_op(pair_kernel<FORM, P, Q, MINB>, (unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s, *hp);
+    if (p->dmma_cfg == 2)
+      launch_op(pair_eo_kernel<FORM, P, Q, MINB>, (unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s, *hp);
+    else
+      launch_op(pair_kernel<FORM, P, Q, MINB>, (unsigned)((nt + kPairBlock - 1) / kPairBlock), kPairBlock, 0, s, *hp);
   } else {
     const int nbatch = (end - start + 15) / 16;
     const int need = (nbatch + kPairPipeWarps - 1) / kPairPipeWarps;

@@ -189,6 +189,11 @@ def flops_per_cell(spec: OperatorSpec, rule=None, menu: str = "min") -> int:
         P, g = (76, 8) if d == 2 else (254, 36)
         sf = 2 * d * _interp_sumfact(d, p, q) + P * q ** d + g
         dense = 4 * d * d * p ** d * q ** d + P * q ** d + g
+        if menu == "executed" and d == 2 and k in (3, 4) and q == p + 1:
+            # round 2 even-odd pair kernel (kern_pair.cuh pair_eo_kernel): counted
+            # from its SASS (profiles/r02/sass_hist.txt), 2 DFMA + DMUL + DADD per
+            # lane, two lanes per cell
+            return min(sf, dense, {3: 2 * (2 * 726 + 271 + 339), 4: 2 * (2 * 1152 + 378 + 500)}[k])
         return min(sf, dense)
     # vertex-gradient P2 (round 1): grad_ref u is P1, so it is interpolated
     # from its 4 vertex values (9 x 4 FMA = 72 flops per point instead of 180)

@@ -88,6 +88,8 @@ ALTERNATIVES = [
     ("neohookean_tangent", "tetrahedron", 2, {"FE_NO_VTX": "1"}, "quad_const"),
     ("elasticity_lame", "quadrilateral", 3, {"FE_PAIR_CFG": "1"}, "component_pair"),
     ("elasticity_lame", "quadrilateral", 4, {"FE_PAIR_CFG": "1"}, "component_pair"),
+    ("elasticity_lame", "quadrilateral", 3, {"FE_PAIR_CFG": "0"}, "component_pair"),
+    ("elasticity_lame", "quadrilateral", 4, {"FE_PAIR_CFG": "0"}, "component_pair"),
 ]
 
 
