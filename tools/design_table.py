@@ -28,8 +28,8 @@ LIMITER = {
     "C3-Q6": "team kernel (49-thread teams), direct algorithm with even-odd 1D contractions (executes 97,644 flops); 128 registers with 112 B of spills, 135 R2UR",
     "C4-quad-Q1": "FP64",
     "C4-quad-Q2": "FP64",
-    "C4-quad-Q3": "pair kernel (select-free, symmetric tables): 254 registers, 2 warps/SMSP; MUL/ADD-heavy pointwise (F/2 = 82% of its FP64 issue slots)",
-    "C4-quad-Q4": "pair kernel (select-free, symmetric tables, 2,952 instructions): 254 registers, 2 warps/SMSP, gather exposed; the 42 us zero-fill of its 269 MB y is 9% of the apply",
+    "C4-quad-Q3": "even-odd pair kernel (select-free): 255 registers, 2 warps/SMSP, gather exposed; executes 4,124 flops",
+    "C4-quad-Q4": "even-odd pair kernel (select-free, 2,632 instructions; executes 6,364 flops): 255 registers, 2 warps/SMSP, gather exposed; the 42 us zero-fill of its 269 MB y is 9% of the apply",
     "C4-hex-Q1": "FP64",
     "C4-hex-Q2": "team kernel (16-thread teams, 9 / 12 of 16 lanes busy in the z / y stages): FP64 pipe 57%",
     "C4-hex-Q3": "team kernel (25-thread teams, one per warp: 78% of the lanes; 16 / 20 of 25 in the z / y stages), even-odd contractions: FP64 pipe 58%",
